@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""bench.py — SteepGS hot path on B200 (BASELINE.json metric: "fwd+bwd+splitting-matrix ms/view
+@1M Gaussians; densify Gaussians/s; x1-8 GPU").
+
+One step = the whole hot path over one batch of V views per GPU:
+restore the densified planes from the pristine copy (checkpoint restore, cudaMemcpy2D) ->
+project -> bin/sort -> render fwd -> l1 gradient -> render bwd (moments) -> per-Gaussian bwd + S
+-> [NCCL allreduce of grads + S across ranks, N > 1] -> SDC densify.
+Workload: BASELINE configs[1] (C2): 1.0M Gaussians, 980x545, synthetic surface-like scene (seeded,
+SURVEY §8(d1)); views are sharded over ranks (rank r takes ring views r::N, weak scaling).
+
+value = ms per view for the whole job = max-over-ranks step time / (V * N).
+Prints ONE JSON line on rank 0.  `--impl reference` times the CPU oracle (bounded sample).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "fwd+bwd+splitting-matrix ms/view @1M Gaussians; densify Gaussians/s; x1-8 GPU"
+UNIT = "ms/view"
+FP32_LANES_PER_SM = 128
+N_SM = 148
+# algorithmic work per unit
+BWD_LANE_OPS_PER_PAIR = 45.0   # contributing pair in the backward replay
+FWD_LANE_OPS_PER_PAIR = 20.0
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return dict(hbm_gbs=float(d["hbm_gbs"]), sm_max_mhz=float(d.get("sm_max_mhz", 1965.0)), src="measured")
+    return dict(hbm_gbs=6650.0, sm_max_mhz=1965.0, src="fallback")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return dict(sm_mhz=None, sm_max_mhz=None, reasons=["nvidia-smi unavailable"])
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.p.kill()
+        self.f.flush()
+        self.f.seek(0)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            c = [x.strip() for x in line.split(",")]
+            if len(c) < 9:
+                continue
+            try:
+                sm.append(float(c[1]))
+                mx.append(float(c[2]))
+            except ValueError:
+                continue
+            for k, nm in enumerate(names):
+                if c[5 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        return dict(sm_mhz=statistics.median(sm) if sm else None, sm_max_mhz=max(mx) if mx else None,
+                    reasons=sorted(reasons), samples=len(sm))
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------------------------------------------
+# CPU oracle (baseline + reference arm): bounded sample of the same workload
+# ------------------------------------------------------------------------------------------------
+def oracle_sample(cfg, params, cam, dl_full, window):
+    """One sampled view of the hot path on the CPU oracle: fp32 decision chain + fp64 projection of
+    all n Gaussians, then fwd + bwd + S (per-pair, fp64) over `window`.  Returns (seconds, est ms
+    per full view, sample description)."""
+    import oracle
+    x0, y0, w, h = window
+    t0 = time.perf_counter()
+    dec = oracle.decide(params, cam)
+    t1 = time.perf_counter()
+    oracle.render(params, cam, window=window, dl_dimage=dl_full[:, y0:y0 + h, x0:x0 + w], decision=dec)
+    t2 = time.perf_counter()
+    frac = (w * h) / float(cfg.width * cfg.height)
+    est_ms = 1e3 * ((t1 - t0) + (t2 - t1) / frac)
+    desc = (f"1 view of {cfg.name} ({cfg.n} Gaussians, {cfg.width}x{cfg.height}): fp32 decision chain over all "
+            f"Gaussians + fp64 fwd+bwd+S over a {w}x{h} window ({100 * frac:.1f}% of the pixels), "
+            f"window time scaled by pixel count")
+    return t2 - t0, est_ms, desc
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+    cfg = synth.CONFIGS[args.config]
+    params = synth.scene_for(cfg)
+    cam = synth.cameras_for(cfg, views=1)[0]
+    dl = synth.dl_dimage(1, cfg.width, cfg.height, 7)[0]
+    window = (cfg.width // 2 - 48, cfg.height // 2 - 32, 96, 64)
+    for _ in range(args.warmup):
+        oracle_sample(cfg, params, cam, dl, window)
+    ests = []
+    for _ in range(args.steps):
+        _, est, desc = oracle_sample(cfg, params, cam, dl, window)
+        ests.append(est)
+    v = float(np.mean(ests))
+    cores = oracle.num_threads()
+    out = dict(metric=METRIC, value=v, unit=UNIT, n_gpus=args.gpus, steps=args.steps, warmup=args.warmup,
+               ms_per_step=v, higher_is_better=False, scaling="weak", vs_baseline=None, dtype="f64",
+               data="synthetic", impl="reference",
+               config=dict(workload=f"{cfg.name}: {cfg.cite}", n=cfg.n, width=cfg.width, height=cfg.height,
+                           views_per_step=1),
+               cpu_baseline=dict(value=v, unit=UNIT, cores=cores, kind="oracle", sample=desc),
+               e2e=dict(value=v, unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------------------
+# GPU arm
+# ------------------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--views", type=int, default=8, help="views per GPU per step")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_05587_b200 import _lib
+    from paper_2505_05587_b200.pipeline import Rasterizer
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    cfg = synth.CONFIGS[args.config]
+    V = args.views
+    n = cfg.n
+    cap = 2 * n
+    p_np = synth.scene_for(cfg)
+    all_cams = synth.cameras_for(cfg, views=V * ws)
+    cams = all_cams[rank::ws]                                 # view sharding
+    tg_all = synth.targets_for(cfg, views=V * ws)
+    tg_np = np.ascontiguousarray(tg_all[rank::ws])
+
+    pristine = torch.zeros(14, cap, dtype=torch.float32, device=dev)
+    pristine[:, :n] = torch.from_numpy(p_np).to(dev)
+    params = pristine.clone()
+    grad_S = torch.zeros(20, cap, dtype=torch.float32, device=dev)
+    targets = torch.from_numpy(tg_np).to(dev)
+    rz = Rasterizer(cap, V, cfg.width, cfg.height, max_instances=int(3.0 * V * n), device=dev)
+    pair_counts = torch.zeros(2, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    stage_names = ["restore", "project", "bin_sort", "render_fwd", "l1_grad", "render_bwd", "gauss_bwd_S",
+                   "allreduce", "densify"]
+
+    def step(ev=None):
+        def mark(k):
+            if ev is not None:
+                ev[k].record(stream)
+        mark(0)
+        _lib.copy_planes(params, pristine, n, 0, 3)          # undo last step's densify (positions,
+        _lib.copy_planes(params, pristine, n, 10, 1)         # opacity) -- checkpoint restore, no kernel
+        mark(1)
+        rz.project(params, n, cams)
+        mark(2)
+        rz.bin_sort()
+        mark(3)
+        rz.render_fwd(pair_counts)
+        mark(4)
+        rz.l1_grad(targets)
+        mark(5)
+        rz.render_bwd_moments()
+        mark(6)
+        rz.gauss_bwd(params, grad_S, accumulate=False)
+        mark(7)
+        if ws > 1:
+            dist.all_reduce(grad_S)
+        mark(8)
+        rz.densify(params, grad_S, n, cap, denom=float(V * ws), want_lambda=False)
+        mark(9)
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3) if args.warmup >= 3 else args.warmup):
+        step()
+    barrier()
+    pair_counts.zero_()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(10)] for _ in range(args.steps)]
+    launches0 = _lib.launch_count()
+    sampler = ClockSampler(local)
+    time.sleep(0.3)
+    barrier()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for k in range(args.steps):
+        step(evs[k])
+    t_end.record(stream)
+    barrier()
+    clocks = sampler.stop()
+    launches = _lib.launch_count() - launches0
+    elapsed = t_start.elapsed_time(t_end)
+    if ws > 1:
+        tt = torch.tensor([elapsed], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        elapsed = float(tt.item())
+    ms_step = elapsed / args.steps
+    stage_ms = {nm: float(np.mean([evs[k][i].elapsed_time(evs[k][i + 1]) for k in range(args.steps)]))
+                for i, nm in enumerate(stage_names)}
+
+    # ---- counts for the roofline model (device -> host after the timed region) ----
+    b = rz.binning_arrays()
+    n_vis, n_inst = b["n_visible"], b["n_instances"]
+    comp_pairs, eval_pairs = (int(x) for x in pair_counts.cpu().tolist())
+    comp_pairs //= args.steps
+    eval_pairs //= args.steps
+    n_split = int(rz.n_split.item())
+    px = cfg.width * cfg.height
+    tiles = ((cfg.width + 15) // 16) * ((cfg.height + 15) // 16)
+    peaks = measured_peaks()
+    hbm = peaks["hbm_gbs"]
+    sm_mhz = clocks["sm_mhz"] or 1342.0
+    alu_peak = N_SM * FP32_LANES_PER_SM * sm_mhz * 1e6       # lane-ops/s at the measured clock
+    # algorithmic (compulsory) bytes per launch of each stage
+    byts = {
+        "restore": 2 * 16 * n,
+        "project": 56 * n + V * 16 * n + 48 * n_vis,
+        "bin_sort": V * 16 * n + 8 * n_vis + 20 * n_inst + 8 * tiles * V,
+        "render_fwd": 4 * n_inst + 48 * n_vis + 20 * px * V,
+        "l1_grad": 36 * px * V,
+        "render_bwd": 4 * n_inst + 48 * n_vis + 28 * px * V + 48 * n_vis,
+        "gauss_bwd_S": 56 * n + 4 * V * n + 96 * n_vis + 80 * n,
+        "densify": 24 * n + 8 * n + 24 * n + n_split * (56 + 56 + 80),
+    }
+    stages = {}
+    for nm in stage_names:
+        t = stage_ms[nm]
+        e = dict(ms=round(t, 4))
+        if nm in byts and t > 0:
+            gbs = byts[nm] / (t * 1e-3) / 1e9
+            e.update(alg_bytes=int(byts[nm]), gbs=round(gbs, 1), hbm_frac=round(gbs / hbm, 4))
+        stages[nm] = e
+    bwd_ops = BWD_LANE_OPS_PER_PAIR * comp_pairs
+    stages["render_bwd"].update(alu_lane_ops=bwd_ops, alu_frac=round(bwd_ops / (stage_ms["render_bwd"] * 1e-3) / alu_peak, 4))
+    stages["render_fwd"].update(alu_lane_ops=FWD_LANE_OPS_PER_PAIR * comp_pairs,
+                                alu_frac=round(FWD_LANE_OPS_PER_PAIR * comp_pairs / (stage_ms["render_fwd"] * 1e-3) / alu_peak, 4))
+    kernel_stages = [s for s in stage_names if s not in ("restore", "allreduce")]
+    dom = max(kernel_stages, key=lambda s: stage_ms[s])
+    if dom in ("render_bwd", "render_fwd"):
+        ops = stages[dom]["alu_lane_ops"]
+        ach = ops / (stage_ms[dom] * 1e-3) / 1e12
+        roofline = dict(bound="alu", kernel=dom, achieved=round(ach, 3), peak=round(alu_peak / 1e12, 3),
+                        unit="T lane-op/s", frac=round(ach * 1e12 / alu_peak, 4), traffic=None,
+                        units_per_launch=dict(contributing_pairs=comp_pairs,
+                                              lane_ops_per_pair=BWD_LANE_OPS_PER_PAIR if dom == "render_bwd" else FWD_LANE_OPS_PER_PAIR),
+                        peak_basis=f"{N_SM} SMs x {FP32_LANES_PER_SM} FP32 lanes x median SM clock {sm_mhz:.0f} MHz")
+    else:
+        ach = byts[dom] / (stage_ms[dom] * 1e-3) / 1e9
+        roofline = dict(bound="hbm", kernel=dom, achieved=round(ach, 1), peak=hbm, unit="GB/s",
+                        frac=round(ach / hbm, 4), traffic=None, peak_basis=f"MEASURED_PEAKS.json ({peaks['src']})")
+    path_bytes = sum(byts[s] for s in byts)
+    path_ms = sum(stage_ms[s] for s in byts)
+    value = ms_step / (V * ws)
+
+    # ---- e2e: host buffers through the public API (H2D of the targets, D2H of loss + n_split) ----
+    e2e = None
+    if not args.no_e2e:
+        tg_host = torch.from_numpy(tg_np).pin_memory()
+        loss_host = torch.zeros(V, dtype=torch.float32).pin_memory()
+        ns_host = torch.zeros(1, dtype=torch.int64).pin_memory()
+
+        def e2e_step():
+            targets.copy_(tg_host, non_blocking=True)
+            step()
+            loss_host.copy_(rz.loss, non_blocking=True)
+            ns_host.copy_(rz.n_split, non_blocking=True)
+            stream.synchronize()
+
+        for _ in range(2):
+            e2e_step()
+        barrier()
+        a = torch.cuda.Event(enable_timing=True)
+        z = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        z.record(stream)
+        barrier()
+        et = a.elapsed_time(z)
+        if ws > 1:
+            tt = torch.tensor([et], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            et = float(tt.item())
+        e2e = dict(value=et / args.steps / (V * ws), unit=UNIT, h2d_bytes_per_step=int(tg_host.numel() * 4),
+                   d2h_bytes_per_step=int(loss_host.numel() * 4 + 8))
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        import oracle
+        oracle.build()
+        dl = synth.dl_dimage(1, cfg.width, cfg.height, 7)[0]
+        window = (cfg.width // 2 - 48, cfg.height // 2 - 32, 96, 64)
+        _, est, desc = oracle_sample(cfg, p_np, all_cams[0], dl, window)
+        cpu = dict(value=est, unit=UNIT, cores=oracle.num_threads(), kind="oracle", sample=desc)
+
+    if rank == 0:
+        out = dict(
+            metric=METRIC, value=round(value, 5), unit=UNIT, n_gpus=ws, steps=args.steps, warmup=args.warmup,
+            ms_per_step=round(ms_step, 4), higher_is_better=False, scaling="weak", vs_baseline=None, dtype="f32",
+            data="synthetic",
+            config=dict(workload=f"{cfg.name}: {cfg.cite}", n=n, width=cfg.width, height=cfg.height,
+                        views_per_gpu_per_step=V, views_per_step=V * ws, capacity=cap,
+                        parallelism=f"view-sharded dp{ws}" + (" + NCCL allreduce(grads+S)" if ws > 1 else ""),
+                        l2="no flush: per-step working set (params 56 MB + splats 48 B x V x n + sort/moment "
+                           "buffers) exceeds the 126 MB L2",
+                        scene="synthetic surface-like (SURVEY 8(d1)), procedural targets"),
+            roofline=roofline,
+            path_hbm=dict(alg_bytes_per_step=int(path_bytes), ms=round(path_ms, 4),
+                          frac=round(path_bytes / (path_ms * 1e-3) / 1e9 / hbm, 4), peak_gbs=hbm),
+            stages=stages,
+            counts=dict(n_visible=n_vis, n_instances=n_inst, contributing_pairs=comp_pairs, evaluated_pairs=eval_pairs,
+                        n_split=n_split, split_frac=round(n_split / n, 4)),
+            densify_gaussians_per_s=round(n / (stage_ms["densify"] * 1e-3), 1),
+            gaussians_per_s=round(n * V * ws / (ms_step * 1e-3), 1),
+            e2e=e2e, cpu_baseline=cpu, clocks=clocks, gpu_launches=int(launches),
+            gpu_launches_per_step=round(launches / args.steps, 2),
+        )
+        print(json.dumps(out), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

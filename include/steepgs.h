@@ -1,0 +1,201 @@
+/* steepgs.h — C ABI of the SteepGS hot path on B200 (sm_100a only).
+ *
+ * Paper: arXiv 2505.05587 (SteepGS, "Steepest Density Control").  Citations P:L<n> are lines of
+ * /root/reference/PAPER.md; canonical definitions C1..C16 and readings Z1..Z27 are DESIGN.md §3.
+ *
+ * Conventions for every call
+ *  - Pointers are CUDA DEVICE pointers owned by the caller unless tagged [host].  The library never
+ *    allocates, frees or reallocates device memory and keeps no global state except a
+ *    thread-local error string and a launch counter.
+ *  - `stream` is a cudaStream_t passed as void*.  Calls are asynchronous on `stream` and never
+ *    synchronise it, except steepgs_densify_host_count (documented below).  Nothing is
+ *    read back to the host, so every call can be captured in a CUDA graph.
+ *  - Reentrant; concurrent calls must not share output or workspace buffers.
+ *  - Errors are returned as steepgs_status; no exception crosses the ABI.  Asynchronous device
+ *    faults surface as STEEPGS_ERR_CUDA at a later call.  steepgs_last_error() gives detail.
+ *  - No CPU fallback: without a compute-capability 10.x device every call returns
+ *    STEEPGS_ERR_UNSUPPORTED_DEVICE.
+ *
+ * Data layouts
+ *  - params  [14][ld] fp32 planar (ld >= capacity >= n): 0-2 mean p, 3-5 log-scale, 6-9 quaternion
+ *            (w,x,y,z; normalised on use), 10 opacity logit, 11-13 rgb.          (C1)
+ *  - grad_S  [20][ldg] fp32 planar: 0-13 dL/d(param plane k), 14-19 splitting matrix S
+ *            (xx,xy,xz,yy,yz,zz).  Summed over views (and, by the caller, over steps/ranks).
+ *  - splats  [V][n] steepgs_splat (48 B): the per-(view, Gaussian) projected record.
+ *  - images  [V][3][H][W] fp32; per-pixel planes [V][H][W].  All views of a call share W, H.
+ */
+#ifndef STEEPGS_H
+#define STEEPGS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  STEEPGS_OK = 0,
+  STEEPGS_ERR_INVALID_ARGUMENT = 1,    /* null/misaligned pointer, n < 0, V outside [1, 64],
+                                          width/height <= 0 or differing across views, ld < n,
+                                          tile != 16, denom <= 0 */
+  STEEPGS_ERR_WORKSPACE_TOO_SMALL = 2, /* ws_bytes < steepgs_bin_sort_workspace_size(...) */
+  STEEPGS_ERR_CAPACITY = 3,            /* densify: n + n_split > capacity (host-count variant) */
+  STEEPGS_ERR_UNSUPPORTED_DEVICE = 5,  /* no CUDA device of compute capability 10.x */
+  STEEPGS_ERR_CUDA = 6                 /* launch / runtime error, see steepgs_last_error() */
+} steepgs_status;
+
+/* One camera (view), [host].  World -> camera: t_c = R p + t, R row-major.  Camera looks down +z,
+ * image y down, pixel (j, k) samples (j + 0.5, k + 0.5) (Z5).
+ * model 0: pinhole, EWA local affine P = J(t_c) R ("approx"); model 1: affine
+ * Pi(p) = diag(fx, fy)[R p + t]_xy + (cx, cy), the paper's exact Eq. eqn:sigma_2D footnote.
+ * Pinhole culls: z <= znear, |x/z| > guard (W/2)/fx, |y/z| > guard (H/2)/fy (C3). */
+typedef struct {
+  float R[9], t[3];
+  float fx, fy, cx, cy;
+  int32_t width, height, model;
+  float znear, guard;
+} steepgs_camera;
+
+/* Compositing parameters (C8, Z3).  Defaults 1/255, 0.99, 1e-4, 0.3, {0,0,0}, 16.
+ * Smooth mode (used by the theorem pins): 0, 1, 0, 0.  tile must be 16. */
+typedef struct {
+  float alpha_min, alpha_max, t_min, dilation;
+  float bg[3];
+  int32_t tile;
+} steepgs_raster_params;
+
+/* Densify parameters (Thm 2, Alg. 1).  eps_split default -1e-6; eta >= 0:
+ * eps = eta sqrt(v^T Sigma v) (default 0.5, Z13), eta < 0: eps = eps_abs; denom = number of
+ * accumulated views/steps (S_bar = S / denom), must be > 0.  gate must be 0 (the
+ * compactest gate of P:L578 is reserved, NEXT f2); eps_grad is ignored. */
+typedef struct {
+  float eps_split, eta, eps_abs, eps_grad, denom;
+  int32_t gate;
+} steepgs_densify_params;
+
+/* Projected splat (a1 output).  mean Pi(p) in pixels kept in fp64 so that per-pair offsets are
+ * exact to ~1e-7 px after tile-relative rounding; conic Q = Pi(Sigma)^-1 (xx, xy, yy) with
+ * dilation; opacity o = sigmoid(logit); rgb; tau = 2 ln(o / alpha_min) (alpha-support bound). */
+typedef struct {
+  double mean[2];
+  float conic[3];
+  float opacity;
+  float rgb[3];
+  float tau;
+} steepgs_splat;
+
+/* Binning result: device pointers into the caller's workspace.  [host] struct. */
+typedef struct {
+  const uint32_t* ids;          /* [max_instances] Gaussian index per tile instance, ordered by
+                                   (view, tile, depth key, index); valid prefix = *n_instances */
+  const uint32_t* ranges;       /* [V * tiles_x * tiles_y][2] (start, end) into ids */
+  const int64_t* n_instances;   /* device scalar I */
+  const int64_t* n_visible;     /* device scalar: visible (view, Gaussian) pairs */
+  const int32_t* overflow;      /* device flag: 1 if I > max_instances (results then invalid) */
+  int64_t max_instances;
+  int32_t tiles_x, tiles_y, V;
+} steepgs_binning;
+
+/* ---- a1: projection (Eq. eqn:sigma_2D + footnote P:L135-139).  Per (view, Gaussian):
+ * activations, camera transform, culls, P = J R, Pi(Sigma) = P Sigma P^T + dil I, conic, opacity,
+ * alpha-support tile rect and tiles_touched, depth key (DESIGN.md §3.2 decision chain, bit-exact
+ * with the oracle).  Culled Gaussians get tiles_touched = 0.
+ * Outputs: splats [V][n]; depth_key [V][n] (orderable uint32 of fp32 z); tile_rect [V][n] packed
+ * uint32x2 (x0 | x1 << 16, y0 | y1 << 16, inclusive tile coords); tiles_touched [V][n] int32. */
+steepgs_status steepgs_project(const float* params, int64_t ld, int64_t n, const steepgs_camera* cams,
+                               int32_t V, const steepgs_raster_params* rp, steepgs_splat* splats,
+                               uint32_t* depth_key, uint32_t* tile_rect, int32_t* tiles_touched,
+                               void* stream);
+
+/* ---- a2: bin & sort ("sorts points according to view-dependent depth"; C7).
+ * Stable depth sort of visible (view, Gaussian) pairs, duplication per touched tile, stable sort
+ * by (view, tile), tile ranges.  Result order within a tile: ascending (depth key, index) —
+ * bit-exact.  No host synchronisation: sizes live on the device; max_instances bounds I. */
+steepgs_status steepgs_bin_sort_workspace_size(int64_t n, int32_t V, int32_t width, int32_t height,
+                                               int64_t max_instances, size_t* bytes /*[host]*/);
+steepgs_status steepgs_bin_sort(const uint32_t* depth_key, const uint32_t* tile_rect,
+                                const int32_t* tiles_touched, int64_t n, const steepgs_camera* cams,
+                                int32_t V, const steepgs_raster_params* rp, void* workspace,
+                                size_t ws_bytes, int64_t max_instances,
+                                steepgs_binning* out /*[host]*/, void* stream);
+
+/* ---- a3: forward compositing, Eq. eqn:alpha_blend, C8.
+ * image [V][3][H][W]; final_T [V][H][W]; n_contrib [V][H][W] = length of the tile-list prefix
+ * up to the last composited Gaussian (consumed by the backward).
+ * pair_counts: NULL, or a device int64[2] that receives += (composited pairs, evaluated pairs)
+ * (the units of the roofline model). */
+steepgs_status steepgs_render_fwd(const steepgs_splat* splats, int64_t n, const steepgs_binning* b,
+                                  const steepgs_camera* cams, int32_t V, const steepgs_raster_params* rp,
+                                  float* image, float* final_T, int32_t* n_contrib, int64_t* pair_counts,
+                                  void* stream);
+
+/* ---- a4: l1 loss gradient helper (Eq. eqn:loss; C9, Z8):
+ * dL_dimage = scale * sign(image - target) (sign(0) = 0) over V*count elements; if loss != NULL,
+ * loss[v] (device, [V]) = scale * sum |image - target| over view v. */
+steepgs_status steepgs_l1_grad(const float* image, const float* target, int32_t V, int64_t count,
+                               float scale, float* dL_dimage, float* loss, void* stream);
+
+/* ---- a5 + a6: backward with the splitting matrix (Thm 1; S per P:L356-358; Alg. 1
+ * P:L537-538).  Replays each pixel back to front, accumulates per (view, Gaussian) 9 moments of
+ * w = dL/dsigma * sigma (sum w, sum w d, sum w d d^T, sum alpha T dL/dC) into moments_ws, then per
+ * Gaussian chains them to dL/dparams and S_view = P^T (Q M Q - m0 Q) P, summed over the V views.
+ * grad_S: if accumulate != 0 grad_S += result, else grad_S = result (columns [0, n)).
+ * moments_ws [V][n][12] fp32 must be all-zero on first use; the call leaves it all-zero. */
+steepgs_status steepgs_render_bwd_split(const float* params, int64_t ld, int64_t n,
+                                        const steepgs_splat* splats, const steepgs_binning* b,
+                                        const steepgs_camera* cams, int32_t V,
+                                        const steepgs_raster_params* rp, const float* final_T,
+                                        const int32_t* n_contrib, const float* dL_dimage,
+                                        float* moments_ws, float* grad_S, int64_t ldg, int32_t accumulate,
+                                        void* stream);
+
+/* The two halves of steepgs_render_bwd_split, exported separately so each kernel can be timed:
+ * a5 (per-pixel replay -> moments_ws) and a6 (moments -> grad_S, S; clears moments_ws). */
+steepgs_status steepgs_render_bwd_moments(const steepgs_splat* splats, int64_t n, const steepgs_binning* b,
+                                          const steepgs_camera* cams, int32_t V, const steepgs_raster_params* rp,
+                                          const float* final_T, const int32_t* n_contrib, const float* dL_dimage,
+                                          float* moments_ws, void* stream);
+steepgs_status steepgs_gauss_bwd_split(const float* params, int64_t ld, int64_t n, const steepgs_camera* cams,
+                                       int32_t V, const steepgs_raster_params* rp,
+                                       float* moments_ws, float* grad_S, int64_t ldg, int32_t accumulate,
+                                       void* stream);
+
+/* ---- a8: steepest density control (Thm 2; Alg. 1; eigen App. A.3
+ * P:L584-604).  Per Gaussian: S_bar = S / denom; lambda_min by the trigonometric roots (fp32,
+ * recomputed in fp64 within a guard band of eps_split); v_min (unit, canonical sign); split iff
+ * lambda_min < eps_split; rank by exclusive scan; offspring A in slot i at p + eps v, B in slot
+ * n + rank at p - eps v, both logit(o/2), other planes copied (C15).  S planes zeroed on
+ * [0, n + n_split); all 20 accumulator planes of new slots zeroed.
+ * Outputs: split_mask [n] u8, dest_index [n] i32 (n + rank or -1), lambda_min [n] f32 or NULL,
+ * n_split [1] int64 device scalar, status [1] int32 device scalar (0 ok, 3 = capacity exceeded:
+ * then params/grad_S are untouched).  workspace: >= steepgs_densify_workspace_size(n) bytes. */
+steepgs_status steepgs_densify_workspace_size(int64_t n, size_t* bytes /*[host]*/);
+steepgs_status steepgs_densify(float* params, int64_t ld, int64_t n, int64_t capacity, float* grad_S,
+                               int64_t ldg, const steepgs_densify_params* dp, uint8_t* split_mask,
+                               int32_t* dest_index, float* lambda_min, int64_t* n_split,
+                               int32_t* status, void* workspace, size_t ws_bytes, void* stream);
+/* Convenience: same as steepgs_densify, then synchronises `stream` and returns the count in
+ * *n_split_host; STEEPGS_ERR_CAPACITY if n + n_split > capacity. */
+steepgs_status steepgs_densify_host_count(float* params, int64_t ld, int64_t n, int64_t capacity,
+                                          float* grad_S, int64_t ldg, const steepgs_densify_params* dp,
+                                          uint8_t* split_mask, int32_t* dest_index, float* lambda_min,
+                                          int64_t* n_split, int32_t* status, void* workspace,
+                                          size_t ws_bytes, int64_t* n_split_host, void* stream);
+
+/* Copy planes [first, first + count) of a planar [*][ld] fp32 array, columns [0, n), device to
+ * device (cudaMemcpy2DAsync; no kernel).  Used to checkpoint / restore Gaussian sets. */
+steepgs_status steepgs_copy_planes(float* dst, int64_t ld_dst, const float* src, int64_t ld_src, int64_t n,
+                                   int32_t first, int32_t count, void* stream);
+
+const char* steepgs_status_string(steepgs_status s);
+const char* steepgs_last_error(void);
+/* Number of kernels this library has launched in this process (all threads). */
+uint64_t steepgs_launch_count(void);
+/* Library version / build string. */
+const char* steepgs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STEEPGS_H */

@@ -1,0 +1,201 @@
+"""Thin ctypes binding of libsteepgs.so (include/steepgs.h).  Argument marshalling only: every step
+of the hot path runs in the library's sm_100a kernels.  There is no fallback: if the library or a
+compute-capability-10.x device is missing, every call raises."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsteepgs.so")
+
+STATUS = {0: "ok", 1: "invalid argument", 2: "workspace too small", 3: "capacity exceeded",
+          5: "unsupported device", 6: "CUDA error"}
+
+
+class SteepGSError(RuntimeError):
+    def __init__(self, fn: str, status: int, detail: str):
+        super().__init__(f"{fn}: {STATUS.get(status, status)} ({detail})")
+        self.status = status
+
+
+class Camera(C.Structure):
+    _fields_ = [("R", C.c_float * 9), ("t", C.c_float * 3), ("fx", C.c_float), ("fy", C.c_float),
+                ("cx", C.c_float), ("cy", C.c_float), ("width", C.c_int32), ("height", C.c_int32),
+                ("model", C.c_int32), ("znear", C.c_float), ("guard", C.c_float)]
+
+
+class RasterParams(C.Structure):
+    _fields_ = [("alpha_min", C.c_float), ("alpha_max", C.c_float), ("t_min", C.c_float),
+                ("dilation", C.c_float), ("bg", C.c_float * 3), ("tile", C.c_int32)]
+
+
+class DensifyParams(C.Structure):
+    _fields_ = [("eps_split", C.c_float), ("eta", C.c_float), ("eps_abs", C.c_float),
+                ("eps_grad", C.c_float), ("denom", C.c_float), ("gate", C.c_int32)]
+
+
+class Binning(C.Structure):
+    _fields_ = [("ids", C.c_void_p), ("ranges", C.c_void_p), ("n_instances", C.c_void_p),
+                ("n_visible", C.c_void_p), ("overflow", C.c_void_p), ("max_instances", C.c_int64),
+                ("tiles_x", C.c_int32), ("tiles_y", C.c_int32), ("V", C.c_int32)]
+
+
+SPLAT_BYTES = 48
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: build it with __graft_entry__.build() "
+                               "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        P, I64, I32, F = C.c_void_p, C.c_int64, C.c_int32, C.c_float
+        sig = {
+            "steepgs_project": [P, I64, I64, P, I32, P, P, P, P, P, P],
+            "steepgs_bin_sort_workspace_size": [I64, I32, I32, I32, I64, P],
+            "steepgs_bin_sort": [P, P, P, I64, P, I32, P, P, C.c_size_t, I64, P, P],
+            "steepgs_render_fwd": [P, I64, P, P, I32, P, P, P, P, P, P],
+            "steepgs_render_bwd_moments": [P, I64, P, P, I32, P, P, P, P, P, P],
+            "steepgs_gauss_bwd_split": [P, I64, I64, P, I32, P, P, P, I64, I32, P],
+            "steepgs_copy_planes": [P, I64, P, I64, I64, I32, I32, P],
+            "steepgs_l1_grad": [P, P, I32, I64, F, P, P, P],
+            "steepgs_render_bwd_split": [P, I64, I64, P, P, P, I32, P, P, P, P, P, P, I64, I32, P],
+            "steepgs_densify_workspace_size": [I64, P],
+            "steepgs_densify": [P, I64, I64, I64, P, I64, P, P, P, P, P, P, P, C.c_size_t, P],
+            "steepgs_densify_host_count": [P, I64, I64, I64, P, I64, P, P, P, P, P, P, P, C.c_size_t, P, P],
+        }
+        for name, args in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = C.c_int
+        L.steepgs_last_error.restype = C.c_char_p
+        L.steepgs_launch_count.restype = C.c_uint64
+        L.steepgs_version.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(fn: str, status: int):
+    if status != 0:
+        raise SteepGSError(fn, status, lib().steepgs_last_error().decode())
+
+
+def ptr(t) -> int | None:
+    if t is None:
+        return None
+    if isinstance(t, torch.Tensor):
+        return t.data_ptr()
+    return int(t)
+
+
+def stream_ptr(stream=None) -> int:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream
+
+
+def cameras(cams: list[dict]):
+    arr = (Camera * len(cams))()
+    for k, c in enumerate(cams):
+        arr[k].R[:] = [float(x) for x in np.asarray(c["R"], dtype=np.float32).reshape(9)]
+        arr[k].t[:] = [float(x) for x in np.asarray(c["t"], dtype=np.float32).reshape(3)]
+        arr[k].fx, arr[k].fy, arr[k].cx, arr[k].cy = (float(np.float32(c[key])) for key in ("fx", "fy", "cx", "cy"))
+        arr[k].width, arr[k].height, arr[k].model = int(c["width"]), int(c["height"]), int(c["model"])
+        arr[k].znear, arr[k].guard = float(np.float32(c["znear"])), float(np.float32(c["guard"]))
+    return arr
+
+
+def raster_params(alpha_min=1.0 / 255.0, alpha_max=0.99, t_min=1e-4, dilation=0.3, bg=(0.0, 0.0, 0.0), tile=16):
+    r = RasterParams()
+    r.alpha_min, r.alpha_max, r.t_min, r.dilation = alpha_min, alpha_max, t_min, dilation
+    r.bg[:] = [float(b) for b in bg]
+    r.tile = tile
+    return r
+
+
+def densify_params(eps_split=-1e-6, eta=0.5, eps_abs=0.0, denom=1.0):
+    d = DensifyParams()
+    d.eps_split, d.eta, d.eps_abs, d.eps_grad, d.denom, d.gate = eps_split, eta, eps_abs, 0.0, denom, 0
+    return d
+
+
+def project(params, ld, n, cams_arr, V, rp, splats, depth_key, tile_rect, tiles_touched, stream=None):
+    _check("steepgs_project", lib().steepgs_project(ptr(params), ld, n, cams_arr, V, C.byref(rp), ptr(splats),
+                                                    ptr(depth_key), ptr(tile_rect), ptr(tiles_touched),
+                                                    stream_ptr(stream)))
+
+
+def bin_sort_workspace_size(n, V, width, height, max_instances) -> int:
+    out = C.c_size_t(0)
+    _check("steepgs_bin_sort_workspace_size",
+           lib().steepgs_bin_sort_workspace_size(n, V, width, height, max_instances, C.byref(out)))
+    return int(out.value)
+
+
+def bin_sort(depth_key, tile_rect, tiles_touched, n, cams_arr, V, rp, ws, max_instances, stream=None) -> Binning:
+    b = Binning()
+    _check("steepgs_bin_sort", lib().steepgs_bin_sort(ptr(depth_key), ptr(tile_rect), ptr(tiles_touched), n, cams_arr,
+                                                      V, C.byref(rp), ptr(ws), ws.numel() * ws.element_size(),
+                                                      max_instances, C.byref(b), stream_ptr(stream)))
+    return b
+
+
+def render_fwd(splats, n, binning, cams_arr, V, rp, image, final_T, n_contrib, pair_counts=None, stream=None):
+    _check("steepgs_render_fwd", lib().steepgs_render_fwd(ptr(splats), n, C.byref(binning), cams_arr, V, C.byref(rp),
+                                                          ptr(image), ptr(final_T), ptr(n_contrib), ptr(pair_counts),
+                                                          stream_ptr(stream)))
+
+
+def render_bwd_moments(splats, n, binning, cams_arr, V, rp, final_T, n_contrib, dL, moments, stream=None):
+    _check("steepgs_render_bwd_moments",
+           lib().steepgs_render_bwd_moments(ptr(splats), n, C.byref(binning), cams_arr, V, C.byref(rp), ptr(final_T),
+                                            ptr(n_contrib), ptr(dL), ptr(moments), stream_ptr(stream)))
+
+
+def gauss_bwd_split(params, ld, n, cams_arr, V, rp, moments, grad_S, ldg, accumulate, stream=None):
+    _check("steepgs_gauss_bwd_split",
+           lib().steepgs_gauss_bwd_split(ptr(params), ld, n, cams_arr, V, C.byref(rp),
+                                         ptr(moments), ptr(grad_S), ldg, int(accumulate), stream_ptr(stream)))
+
+
+def copy_planes(dst, src, n, first, count, stream=None):
+    _check("steepgs_copy_planes", lib().steepgs_copy_planes(ptr(dst), dst.shape[1], ptr(src), src.shape[1], n, first,
+                                                            count, stream_ptr(stream)))
+
+
+def l1_grad(image, target, V, count, scale, dL, loss=None, stream=None):
+    _check("steepgs_l1_grad", lib().steepgs_l1_grad(ptr(image), ptr(target), V, count, scale, ptr(dL), ptr(loss),
+                                                    stream_ptr(stream)))
+
+
+def render_bwd_split(params, ld, n, splats, binning, cams_arr, V, rp, final_T, n_contrib, dL,
+                     moments, grad_S, ldg, accumulate, stream=None):
+    _check("steepgs_render_bwd_split",
+           lib().steepgs_render_bwd_split(ptr(params), ld, n, ptr(splats), C.byref(binning),
+                                          cams_arr, V, C.byref(rp), ptr(final_T), ptr(n_contrib), ptr(dL),
+                                          ptr(moments), ptr(grad_S), ldg, int(accumulate), stream_ptr(stream)))
+
+
+def densify_workspace_size(n) -> int:
+    out = C.c_size_t(0)
+    _check("steepgs_densify_workspace_size", lib().steepgs_densify_workspace_size(n, C.byref(out)))
+    return int(out.value)
+
+
+def densify(params, ld, n, capacity, grad_S, ldg, dp, mask, dest, lam, n_split, status, ws, stream=None):
+    _check("steepgs_densify", lib().steepgs_densify(ptr(params), ld, n, capacity, ptr(grad_S), ldg, C.byref(dp),
+                                                    ptr(mask), ptr(dest), ptr(lam), ptr(n_split), ptr(status),
+                                                    ptr(ws), ws.numel() * ws.element_size(), stream_ptr(stream)))
+
+
+def launch_count() -> int:
+    return int(lib().steepgs_launch_count())
+
+
+def version() -> str:
+    return lib().steepgs_version().decode()

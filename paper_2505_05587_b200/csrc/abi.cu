@@ -1,0 +1,282 @@
+// abi.cu — the extern "C" boundary of libsteepgs (declared in include/steepgs.h): argument
+// validation, device check (compute capability 10.x only), launch bookkeeping, error strings.
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+
+namespace sgs {
+
+static thread_local std::string g_last_error;
+static std::atomic<uint64_t> g_launches{0};
+
+void note_launch(int k) { g_launches.fetch_add((uint64_t)k, std::memory_order_relaxed); }
+
+cudaError_t check_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+  return e;
+}
+
+static steepgs_status fail(steepgs_status s, const char* msg) {
+  g_last_error = msg;
+  return s;
+}
+
+static steepgs_status cuda_fail(cudaError_t e, const char* where) {
+  if (g_last_error.empty() || g_last_error.find(cudaGetErrorString(e)) == std::string::npos)
+    g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+  return STEEPGS_ERR_CUDA;
+}
+
+static steepgs_status device_ok() {
+  int dev = -1;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return fail(STEEPGS_ERR_UNSUPPORTED_DEVICE, "no CUDA device");
+  int major = 0;
+  e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (e != cudaSuccess || major != 10)
+    return fail(STEEPGS_ERR_UNSUPPORTED_DEVICE, "libsteepgs is built for sm_100a (compute capability 10.x) only");
+  return STEEPGS_OK;
+}
+
+static steepgs_status check_views(const steepgs_camera* cams, int32_t V, CamPack* pack) {
+  if (!cams || V < 1 || V > kMaxViews) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "V must be in [1, 64] and cams non-null");
+  for (int v = 0; v < V; ++v) {
+    if (cams[v].width <= 0 || cams[v].height <= 0 || cams[v].width != cams[0].width || cams[v].height != cams[0].height)
+      return fail(STEEPGS_ERR_INVALID_ARGUMENT, "all views need the same positive width/height");
+    if (cams[v].width >= 65536 * kTile || cams[v].height >= 65536 * kTile)
+      return fail(STEEPGS_ERR_INVALID_ARGUMENT, "image too large");
+    if (cams[v].model != 0 && cams[v].model != 1) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "camera model must be 0 or 1");
+    if (pack) pack->cam[v] = cams[v];
+  }
+  return STEEPGS_OK;
+}
+
+static steepgs_status check_raster(const steepgs_raster_params* rp) {
+  if (!rp) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "raster params null");
+  if (rp->tile != kTile) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "tile must be 16");
+  if (!(rp->alpha_min >= 0.f) || !(rp->alpha_max > 0.f) || !(rp->alpha_max <= 1.f) || !(rp->t_min >= 0.f) ||
+      !(rp->dilation >= 0.f))
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "raster params out of range");
+  return STEEPGS_OK;
+}
+
+static bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+static steepgs_status check_binning(const steepgs_binning* b, int32_t V, const steepgs_camera* cams) {
+  if (!b || !b->ids || !b->ranges || !b->n_instances) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "binning null");
+  const int tx = (cams[0].width + kTile - 1) / kTile, ty = (cams[0].height + kTile - 1) / kTile;
+  if (b->V != V || b->tiles_x != tx || b->tiles_y != ty)
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "binning does not match the views of this call");
+  return STEEPGS_OK;
+}
+
+}  // namespace sgs
+
+using namespace sgs;
+
+extern "C" {
+
+const char* steepgs_status_string(steepgs_status s) {
+  switch (s) {
+    case STEEPGS_OK: return "ok";
+    case STEEPGS_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case STEEPGS_ERR_WORKSPACE_TOO_SMALL: return "workspace too small";
+    case STEEPGS_ERR_CAPACITY: return "capacity exceeded";
+    case STEEPGS_ERR_UNSUPPORTED_DEVICE: return "unsupported device (need compute capability 10.x)";
+    case STEEPGS_ERR_CUDA: return "CUDA error";
+  }
+  return "unknown status";
+}
+
+const char* steepgs_last_error(void) { return g_last_error.c_str(); }
+uint64_t steepgs_launch_count(void) { return g_launches.load(); }
+const char* steepgs_version(void) { return "steepgs-b200 0.1 (sm_100a)"; }
+
+steepgs_status steepgs_project(const float* params, int64_t ld, int64_t n, const steepgs_camera* cams, int32_t V,
+                               const steepgs_raster_params* rp, steepgs_splat* splats, uint32_t* depth_key,
+                               uint32_t* tile_rect, int32_t* tiles_touched, void* stream) {
+  steepgs_status s;
+  if ((s = device_ok()) != STEEPGS_OK) return s;
+  CamPack pack;
+  if ((s = check_views(cams, V, &pack)) != STEEPGS_OK) return s;
+  if ((s = check_raster(rp)) != STEEPGS_OK) return s;
+  if (n < 0 || ld < n) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "need 0 <= n <= ld");
+  if ((int64_t)V * n >= (1ll << 32)) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "V * n must be < 2^32");
+  if (n > 0 && (!params || !splats || !depth_key || !tile_rect || !tiles_touched))
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "null pointer");
+  if (!aligned(splats, 16) || !aligned(tile_rect, 8)) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "misaligned output");
+  const cudaError_t e = launch_project(params, ld, n, pack, V, raster_k(rp), splats, depth_key, tile_rect,
+                                       tiles_touched, (cudaStream_t)stream);
+  return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_project");
+}
+
+steepgs_status steepgs_bin_sort_workspace_size(int64_t n, int32_t V, int32_t width, int32_t height,
+                                               int64_t max_instances, size_t* bytes) {
+  if (!bytes || n < 0 || V < 1 || V > kMaxViews || width <= 0 || height <= 0 || max_instances < 0 ||
+      max_instances >= (1ll << 31))
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "bad workspace-size arguments");
+  const int tiles = ((width + kTile - 1) / kTile) * ((height + kTile - 1) / kTile);
+  *bytes = bin_sort_ws_bytes(n, V, tiles, max_instances);
+  return STEEPGS_OK;
+}
+
+steepgs_status steepgs_bin_sort(const uint32_t* depth_key, const uint32_t* tile_rect, const int32_t* tiles_touched,
+                                int64_t n, const steepgs_camera* cams, int32_t V, const steepgs_raster_params* rp,
+                                void* workspace, size_t ws_bytes, int64_t max_instances, steepgs_binning* out,
+                                void* stream) {
+  steepgs_status s;
+  if ((s = device_ok()) != STEEPGS_OK) return s;
+  if ((s = check_views(cams, V, nullptr)) != STEEPGS_OK) return s;
+  if ((s = check_raster(rp)) != STEEPGS_OK) return s;
+  if (!out || !workspace || n < 0 || max_instances < 0 || max_instances >= (1ll << 31))
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "bad bin_sort arguments");
+  if (n > 0 && (!depth_key || !tile_rect || !tiles_touched)) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "null pointer");
+  if (!aligned(workspace, 256)) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
+  const int tx = (cams[0].width + kTile - 1) / kTile, ty = (cams[0].height + kTile - 1) / kTile;
+  if ((int64_t)tx * ty * V >= (1 << 24)) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "too many tiles");
+  size_t need = bin_sort_ws_bytes(n, V, tx * ty, max_instances);
+  if (ws_bytes < need) return fail(STEEPGS_ERR_WORKSPACE_TOO_SMALL, "bin_sort workspace too small");
+  const cudaError_t e = launch_bin_sort(depth_key, tile_rect, tiles_touched, n, V, tx, ty, workspace, ws_bytes,
+                                        max_instances, out, (cudaStream_t)stream);
+  return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_bin_sort");
+}
+
+steepgs_status steepgs_render_fwd(const steepgs_splat* splats, int64_t n, const steepgs_binning* b,
+                                  const steepgs_camera* cams, int32_t V, const steepgs_raster_params* rp, float* image,
+                                  float* final_T, int32_t* n_contrib, int64_t* pair_counts, void* stream) {
+  steepgs_status s;
+  if ((s = device_ok()) != STEEPGS_OK) return s;
+  if ((s = check_views(cams, V, nullptr)) != STEEPGS_OK) return s;
+  if ((s = check_raster(rp)) != STEEPGS_OK) return s;
+  if ((s = check_binning(b, V, cams)) != STEEPGS_OK) return s;
+  if (n < 0 || !image || !final_T || !n_contrib || (n > 0 && !splats))
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "null pointer");
+  const cudaError_t e = launch_render_fwd(splats, n, *b, cams[0].width, cams[0].height, raster_k(rp), image, final_T,
+                                          n_contrib, pair_counts, (cudaStream_t)stream);
+  return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_render_fwd");
+}
+
+steepgs_status steepgs_l1_grad(const float* image, const float* target, int32_t V, int64_t count, float scale,
+                               float* dL_dimage, float* loss, void* stream) {
+  steepgs_status s;
+  if ((s = device_ok()) != STEEPGS_OK) return s;
+  if (V < 1 || count < 0 || !image || !target || !dL_dimage) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "bad l1 arguments");
+  const cudaError_t e = launch_l1_grad(image, target, V, count, scale, dL_dimage, loss, (cudaStream_t)stream);
+  return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_l1_grad");
+}
+
+steepgs_status steepgs_render_bwd_split(const float* params, int64_t ld, int64_t n, const steepgs_splat* splats,
+                                        const steepgs_binning* b, const steepgs_camera* cams, int32_t V,
+                                        const steepgs_raster_params* rp,
+                                        const float* final_T, const int32_t* n_contrib, const float* dL_dimage,
+                                        float* moments_ws, float* grad_S, int64_t ldg, int32_t accumulate,
+                                        void* stream) {
+  steepgs_status s;
+  if ((s = device_ok()) != STEEPGS_OK) return s;
+  CamPack pack;
+  if ((s = check_views(cams, V, &pack)) != STEEPGS_OK) return s;
+  if ((s = check_raster(rp)) != STEEPGS_OK) return s;
+  if ((s = check_binning(b, V, cams)) != STEEPGS_OK) return s;
+  if (n < 0 || ld < n || ldg < n) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "need 0 <= n <= ld, ldg");
+  if (n > 0 && (!params || !splats || !final_T || !n_contrib || !dL_dimage || !moments_ws || !grad_S))
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "null pointer");
+  if (!aligned(moments_ws, 16)) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "moments_ws must be 16-byte aligned");
+  const RasterK rk = raster_k(rp);
+  cudaError_t e = launch_render_bwd(splats, *b, cams[0].width, cams[0].height, rk, final_T, n_contrib, dL_dimage, n,
+                                    moments_ws, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "steepgs_render_bwd_split");
+  e = launch_gauss_bwd(params, ld, n, pack, V, rk, moments_ws, grad_S, ldg, accumulate, (cudaStream_t)stream);
+  return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_render_bwd_split");
+}
+
+steepgs_status steepgs_render_bwd_moments(const steepgs_splat* splats, int64_t n, const steepgs_binning* b,
+                                          const steepgs_camera* cams, int32_t V, const steepgs_raster_params* rp,
+                                          const float* final_T, const int32_t* n_contrib, const float* dL_dimage,
+                                          float* moments_ws, void* stream) {
+  steepgs_status s;
+  if ((s = device_ok()) != STEEPGS_OK) return s;
+  if ((s = check_views(cams, V, nullptr)) != STEEPGS_OK) return s;
+  if ((s = check_raster(rp)) != STEEPGS_OK) return s;
+  if ((s = check_binning(b, V, cams)) != STEEPGS_OK) return s;
+  if (n < 0 || (n > 0 && (!splats || !final_T || !n_contrib || !dL_dimage || !moments_ws)))
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "null pointer");
+  if (!aligned(moments_ws, 16)) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "moments_ws must be 16-byte aligned");
+  const cudaError_t e = launch_render_bwd(splats, *b, cams[0].width, cams[0].height, raster_k(rp), final_T, n_contrib,
+                                          dL_dimage, n, moments_ws, (cudaStream_t)stream);
+  return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_render_bwd_moments");
+}
+
+steepgs_status steepgs_gauss_bwd_split(const float* params, int64_t ld, int64_t n, const steepgs_camera* cams,
+                                       int32_t V, const steepgs_raster_params* rp,
+                                       float* moments_ws, float* grad_S, int64_t ldg, int32_t accumulate,
+                                       void* stream) {
+  steepgs_status s;
+  if ((s = device_ok()) != STEEPGS_OK) return s;
+  CamPack pack;
+  if ((s = check_views(cams, V, &pack)) != STEEPGS_OK) return s;
+  if ((s = check_raster(rp)) != STEEPGS_OK) return s;
+  if (n < 0 || ld < n || ldg < n) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "need 0 <= n <= ld, ldg");
+  if (n > 0 && (!params || !moments_ws || !grad_S)) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "null pointer");
+  if (!aligned(moments_ws, 16)) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "moments_ws must be 16-byte aligned");
+  const cudaError_t e = launch_gauss_bwd(params, ld, n, pack, V, raster_k(rp), moments_ws, grad_S, ldg, accumulate,
+                                         (cudaStream_t)stream);
+  return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_gauss_bwd_split");
+}
+
+steepgs_status steepgs_copy_planes(float* dst, int64_t ld_dst, const float* src, int64_t ld_src, int64_t n,
+                                   int32_t first, int32_t count, void* stream) {
+  if (!dst || !src || n < 0 || ld_dst < n || ld_src < n || first < 0 || count < 0)
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "bad copy_planes arguments");
+  if (n == 0 || count == 0) return STEEPGS_OK;
+  const cudaError_t e = cudaMemcpy2DAsync(dst + first * ld_dst, (size_t)ld_dst * 4, src + first * ld_src,
+                                          (size_t)ld_src * 4, (size_t)n * 4, (size_t)count, cudaMemcpyDeviceToDevice,
+                                          (cudaStream_t)stream);
+  return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_copy_planes");
+}
+
+steepgs_status steepgs_densify_workspace_size(int64_t n, size_t* bytes) {
+  if (!bytes || n < 0) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "bad densify workspace arguments");
+  *bytes = densify_ws_bytes(n);
+  return STEEPGS_OK;
+}
+
+steepgs_status steepgs_densify(float* params, int64_t ld, int64_t n, int64_t capacity, float* grad_S, int64_t ldg,
+                               const steepgs_densify_params* dp, uint8_t* split_mask, int32_t* dest_index,
+                               float* lambda_min, int64_t* n_split, int32_t* status, void* workspace,
+                               size_t ws_bytes, void* stream) {
+  steepgs_status s;
+  if ((s = device_ok()) != STEEPGS_OK) return s;
+  if (!dp || !(dp->denom > 0.f) || dp->gate != 0) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "densify params: denom > 0, gate == 0");
+  if (n < 0 || capacity < n || ld < capacity || ldg < capacity || capacity >= (1ll << 31))
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "need 0 <= n <= capacity <= ld, ldg < 2^31");
+  if (!params || !grad_S || !n_split || !status || !workspace || (n > 0 && (!split_mask || !dest_index)))
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "null pointer");
+  if (ws_bytes < densify_ws_bytes(n)) return fail(STEEPGS_ERR_WORKSPACE_TOO_SMALL, "densify workspace too small");
+  const cudaError_t e = launch_densify(params, ld, n, capacity, grad_S, ldg, *dp, split_mask, dest_index, lambda_min,
+                                       n_split, status, workspace, ws_bytes, (cudaStream_t)stream);
+  return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_densify");
+}
+
+steepgs_status steepgs_densify_host_count(float* params, int64_t ld, int64_t n, int64_t capacity, float* grad_S,
+                                          int64_t ldg, const steepgs_densify_params* dp, uint8_t* split_mask,
+                                          int32_t* dest_index, float* lambda_min, int64_t* n_split, int32_t* status,
+                                          void* workspace, size_t ws_bytes, int64_t* n_split_host, void* stream) {
+  if (!n_split_host) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "n_split_host null");
+  steepgs_status s = steepgs_densify(params, ld, n, capacity, grad_S, ldg, dp, split_mask, dest_index, lambda_min,
+                                     n_split, status, workspace, ws_bytes, stream);
+  if (s != STEEPGS_OK) return s;
+  int64_t ns = 0;
+  int32_t st = 0;
+  cudaError_t e = cudaMemcpyAsync(&ns, n_split, sizeof ns, cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&st, status, sizeof st, cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "steepgs_densify_host_count");
+  *n_split_host = ns;
+  return st == 0 ? STEEPGS_OK : fail(STEEPGS_ERR_CAPACITY, "n + n_split > capacity");
+}
+
+}  // extern "C"

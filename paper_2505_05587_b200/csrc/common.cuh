@@ -1,0 +1,61 @@
+// common.cuh — internal declarations shared by the sm_100a kernels of libsteepgs.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "steepgs.h"
+
+namespace sgs {
+
+constexpr int kTile = 16;          // tile edge in pixels (16x16 = 256 threads per tile block)
+constexpr int kMaxViews = 64;      // cameras passed by value in kernel parameters
+
+struct CamPack {                   // by-value kernel parameter (<= 64 * 80 B)
+  steepgs_camera cam[kMaxViews];
+};
+
+struct RasterK {
+  float alpha_min, alpha_max, t_min, dilation;
+  float bg[3];
+};
+
+inline RasterK raster_k(const steepgs_raster_params* rp) {
+  RasterK r;
+  r.alpha_min = rp->alpha_min; r.alpha_max = rp->alpha_max; r.t_min = rp->t_min; r.dilation = rp->dilation;
+  r.bg[0] = rp->bg[0]; r.bg[1] = rp->bg[1]; r.bg[2] = rp->bg[2];
+  return r;
+}
+
+// ---- launch bookkeeping (abi.cu) ----
+void note_launch(int k = 1);
+cudaError_t check_launch(const char* what);
+
+// ---- launchers (one per .cu) ----
+cudaError_t launch_project(const float* params, int64_t ld, int64_t n, const CamPack& cams, int V,
+                           const RasterK& rk, steepgs_splat* splats, uint32_t* depth_key, uint32_t* tile_rect,
+                           int32_t* tiles_touched, cudaStream_t st);
+
+struct SortWs;  // bin_sort workspace carve-up (sort.cu)
+size_t bin_sort_ws_bytes(int64_t n, int V, int tiles, int64_t max_instances);
+cudaError_t launch_bin_sort(const uint32_t* depth_key, const uint32_t* tile_rect, const int32_t* tiles_touched,
+                            int64_t n, int V, int tiles_x, int tiles_y, void* ws, size_t ws_bytes,
+                            int64_t max_instances, steepgs_binning* out, cudaStream_t st);
+
+cudaError_t launch_render_fwd(const steepgs_splat* splats, int64_t n, const steepgs_binning& b, int W, int H,
+                              const RasterK& rk, float* image, float* final_T, int32_t* n_contrib,
+                              int64_t* pair_counts, cudaStream_t st);
+cudaError_t launch_l1_grad(const float* image, const float* target, int V, int64_t count, float scale,
+                           float* dL, float* loss, cudaStream_t st);
+cudaError_t launch_render_bwd(const steepgs_splat* splats, const steepgs_binning& b, int W, int H,
+                              const RasterK& rk, const float* final_T, const int32_t* n_contrib,
+                              const float* dL_dimage, int64_t n, float* moments, cudaStream_t st);
+cudaError_t launch_gauss_bwd(const float* params, int64_t ld, int64_t n, const CamPack& cams, int V,
+                             const RasterK& rk, float* moments, float* grad_S, int64_t ldg, int accumulate,
+                             cudaStream_t st);
+
+size_t densify_ws_bytes(int64_t n);
+cudaError_t launch_densify(float* params, int64_t ld, int64_t n, int64_t capacity, float* grad_S, int64_t ldg,
+                           const steepgs_densify_params& dp, uint8_t* mask, int32_t* dest, float* lambda,
+                           int64_t* n_split, int32_t* status, void* ws, size_t ws_bytes, cudaStream_t st);
+
+}  // namespace sgs

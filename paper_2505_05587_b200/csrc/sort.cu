@@ -1,0 +1,469 @@
+// sort.cu — a2: bin & sort ("3DGS first sorts points according to view-dependent depth", P:L129;
+// order C7 = ascending (depth key, index) within each (view, tile)).
+//
+// B200 design (no host synchronisation, graph-capturable):
+//   1. k_compact        visible (view, Gaussian) pairs -> (depth key, slot) + 16-B record; builds the
+//                       4 depth-digit histograms on the fly; decoupled look-back scan.
+//   2. 4 x k_radix_pass  stable LSD radix sort of the 32-bit depth keys (8-bit digits, onesweep-style:
+//                       warp match-based ranking, per-digit decoupled look-back, smem-staged coalesced
+//                       scatter).  Ties keep (view, index) order because the input is in that order.
+//   3. k_duplicate      exclusive scan of tiles_touched in depth order (look-back) and emission of one
+//                       (view*tiles + tile, index) instance per touched tile; builds the tile-digit
+//                       histograms on the fly.
+//   4. 1-2 x k_radix_pass stable sort by tile key -> (view, tile, depth, index) order.
+//   5. k_ranges         [start, end) per (view, tile).
+// Sizes that are only known on the device (visible count, instance count) are read by the kernels;
+// grids are sized by the host-known upper bounds and surplus blocks exit at once.
+#include "common.cuh"
+#include "scan.cuh"
+
+namespace sgs {
+
+namespace {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;                      // items per thread per scan tile
+constexpr int kScanTile = kScanThreads * kScanItems;  // 2048
+constexpr int kRadixThreads = 256;
+constexpr int kRadixItems = 12;
+constexpr int kRadixTile = kRadixThreads * kRadixItems;  // 3072
+constexpr int kRadixWarps = kRadixThreads / 32;
+
+constexpr uint32_t kRadFlagAgg = 1u << 30;
+constexpr uint32_t kRadFlagPre = 2u << 30;
+constexpr uint32_t kRadValMask = (1u << 30) - 1;
+
+// ------------------------------------------------------------------------------------------------
+// 1. compaction of visible pairs + depth-digit histograms
+// ------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kScanThreads) k_compact(const uint32_t* __restrict__ depth_key,
+                                                          const uint2* __restrict__ tile_rect,
+                                                          const int32_t* __restrict__ tiles_touched, int64_t n,
+                                                          int64_t total, uint32_t* __restrict__ keys_out,
+                                                          uint32_t* __restrict__ vals_out, uint4* __restrict__ recs,
+                                                          uint64_t* status, int* tile_counter, uint32_t* hist4,
+                                                          int64_t* n_visible) {
+  __shared__ int s_tile;
+  __shared__ uint32_t s_cnt[kScanItems][kScanThreads / 32];
+  __shared__ uint32_t s_hist[4][256];
+  __shared__ uint64_t s_excl;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) s_tile = atomicAdd(tile_counter, 1);
+  for (int k = tid; k < 4 * 256; k += kScanThreads) (&s_hist[0][0])[k] = 0;
+  __syncthreads();
+  const int tile = s_tile;
+  const int64_t base = (int64_t)tile * kScanTile;
+  bool flag[kScanItems];
+  uint32_t pos_in_warp[kScanItems];
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    const int64_t idx = base + (int64_t)j * kScanThreads + tid;
+    flag[j] = idx < total && tiles_touched[idx] > 0;
+    const uint32_t b = __ballot_sync(0xffffffffu, flag[j]);
+    pos_in_warp[j] = __popc(b & lanemask_lt());
+    if (lane == 0) s_cnt[j][warp] = __popc(b);
+  }
+  __syncthreads();
+  // exclusive scan of the 64 warp counts in (j, warp) order by warp 0
+  if (warp == 0) {
+    const int nw = kScanThreads / 32;
+    uint32_t a = s_cnt[(2 * lane) / nw][(2 * lane) % nw], b = s_cnt[(2 * lane + 1) / nw][(2 * lane + 1) % nw];
+    uint32_t sum = a + b, inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    const uint32_t ex = inc - sum;
+    s_cnt[(2 * lane) / nw][(2 * lane) % nw] = ex;
+    s_cnt[(2 * lane + 1) / nw][(2 * lane + 1) % nw] = ex + a;
+    const uint32_t agg = __shfl_sync(0xffffffffu, inc, 31);
+    const uint64_t excl = lookback_warp(status, tile, agg);
+    if (lane == 0) {
+      s_excl = excl;
+      if ((base + kScanTile >= total)) *n_visible = (int64_t)(excl + agg);  // last tile
+    }
+  }
+  __syncthreads();
+  const uint64_t bex = s_excl;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    if (!flag[j]) continue;
+    const int64_t idx = base + (int64_t)j * kScanThreads + tid;
+    const uint64_t pos = bex + s_cnt[j][warp] + pos_in_warp[j];
+    const uint32_t key = depth_key[idx];
+    keys_out[pos] = key;
+    vals_out[pos] = (uint32_t)pos;
+    const uint2 r = tile_rect[idx];
+    const uint32_t v = (uint32_t)(idx / n), i = (uint32_t)(idx - (int64_t)v * n);
+    recs[pos] = make_uint4(r.x, r.y, i, (v << 24) | (uint32_t)tiles_touched[idx]);
+#pragma unroll
+    for (int p = 0; p < 4; ++p) atomicAdd(&s_hist[p][(key >> (8 * p)) & 255u], 1u);
+  }
+  __syncthreads();
+  for (int k = tid; k < 4 * 256; k += kScanThreads) {
+    const uint32_t c = (&s_hist[0][0])[k];
+    if (c) atomicAdd(&hist4[k], c);
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// 2/4. one stable LSD radix pass (8-bit digit at `shift`), onesweep-style.
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t block_excl_scan_256(uint32_t v, uint32_t* s_warp /*[8]*/) {
+  // 256 threads, one value each -> exclusive scan (all threads participate)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint32_t inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) s_warp[warp] = inc;
+  __syncthreads();
+  uint32_t wpre = 0;
+#pragma unroll
+  for (int w = 0; w < kRadixWarps; ++w) wpre += (w < warp) ? s_warp[w] : 0u;
+  __syncthreads();
+  return wpre + inc - v;
+}
+
+__global__ void __launch_bounds__(kRadixThreads) k_radix_pass(const uint32_t* __restrict__ keys_in,
+                                                              const uint32_t* __restrict__ vals_in,
+                                                              uint32_t* __restrict__ keys_out,
+                                                              uint32_t* __restrict__ vals_out, const int64_t* n_dev,
+                                                              int64_t n_max, int shift,
+                                                              const uint32_t* __restrict__ ghist /*[256]*/,
+                                                              uint32_t* status /*[tiles][256]*/, int* tile_counter) {
+  __shared__ uint32_t s_keys[kRadixTile];
+  __shared__ uint32_t s_vals[kRadixTile];
+  __shared__ uint32_t s_whist[kRadixWarps][256];
+  __shared__ uint32_t s_local[256];
+  __shared__ uint32_t s_dbase[256];
+  __shared__ uint32_t s_tmp[kRadixWarps];
+  __shared__ int s_tile;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) s_tile = atomicAdd(tile_counter, 1);
+  for (int k = tid; k < kRadixWarps * 256; k += kRadixThreads) (&s_whist[0][0])[k] = 0;
+  __syncthreads();
+  const int tile = s_tile;
+  int64_t n = *n_dev;
+  if (n > n_max) n = n_max;
+  const int64_t base = (int64_t)tile * kRadixTile;
+  if (base >= n) return;
+  const int64_t wbase = base + (int64_t)warp * (32 * kRadixItems);
+  uint32_t k[kRadixItems], v[kRadixItems];
+  uint32_t d[kRadixItems], rank[kRadixItems];
+#pragma unroll
+  for (int j = 0; j < kRadixItems; ++j) {
+    const int64_t idx = wbase + j * 32 + lane;
+    const bool ok = idx < n;
+    k[j] = ok ? keys_in[idx] : 0u;
+    v[j] = ok ? vals_in[idx] : 0u;
+    d[j] = ok ? ((k[j] >> shift) & 255u) : 256u;
+  }
+  const uint32_t lt = lanemask_lt();
+#pragma unroll
+  for (int j = 0; j < kRadixItems; ++j) {
+    const uint32_t peers = __match_any_sync(0xffffffffu, d[j]);
+    const uint32_t before_lanes = __popc(peers & lt);
+    uint32_t before = 0;
+    if (d[j] < 256u) before = s_whist[warp][d[j]];
+    __syncwarp();
+    if (d[j] < 256u && before_lanes == 0) s_whist[warp][d[j]] = before + __popc(peers);
+    __syncwarp();
+    rank[j] = before + before_lanes;
+  }
+  __syncthreads();
+  // per digit (thread = digit): exclusive over warps, block total, look-back, bases
+  const uint32_t dig = (uint32_t)tid;
+  uint32_t tot = 0;
+#pragma unroll
+  for (int w = 0; w < kRadixWarps; ++w) {
+    const uint32_t c = s_whist[w][dig];
+    s_whist[w][dig] = tot;
+    tot += c;
+  }
+  uint32_t excl = 0;
+  if (tile == 0) {
+    st_volatile(&status[dig], kRadFlagPre | tot);
+  } else {
+    st_volatile(&status[(int64_t)tile * 256 + dig], kRadFlagAgg | tot);
+    int p = tile - 1;
+    while (true) {
+      uint32_t s;
+      do {
+        s = ld_volatile(&status[(int64_t)p * 256 + dig]);
+      } while ((s >> 30) == 0);
+      excl += s & kRadValMask;
+      if ((s >> 30) == 2) break;
+      --p;
+    }
+    st_volatile(&status[(int64_t)tile * 256 + dig], kRadFlagPre | (excl + tot));
+  }
+  const uint32_t gstart = block_excl_scan_256(ghist[dig], s_tmp);
+  const uint32_t lstart = block_excl_scan_256(tot, s_tmp);
+  s_local[dig] = lstart;
+  s_dbase[dig] = gstart + excl;
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kRadixItems; ++j) {
+    if (d[j] < 256u) {
+      const uint32_t lp = s_local[d[j]] + s_whist[warp][d[j]] + rank[j];
+      s_keys[lp] = k[j];
+      s_vals[lp] = v[j];
+    }
+  }
+  __syncthreads();
+  const int cnt = (int)((n - base) < kRadixTile ? (n - base) : kRadixTile);
+  for (int idx = tid; idx < cnt; idx += kRadixThreads) {
+    const uint32_t kk = s_keys[idx];
+    const uint32_t dd = (kk >> shift) & 255u;
+    const uint32_t g = s_dbase[dd] + (uint32_t)idx - s_local[dd];
+    keys_out[g] = kk;
+    vals_out[g] = s_vals[idx];
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// 3. duplication: scan of tiles_touched in depth order, one instance per touched tile
+// ------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kScanThreads) k_duplicate(const uint32_t* __restrict__ sorted_slots,
+                                                            const uint4* __restrict__ recs, const int64_t* n_vis_dev,
+                                                            int tiles_x, int tiles_per_view, int64_t max_instances,
+                                                            uint32_t* __restrict__ inst_keys,
+                                                            uint32_t* __restrict__ inst_ids, uint64_t* status,
+                                                            int* tile_counter, uint32_t* hist2, int64_t* n_inst,
+                                                            int32_t* overflow) {
+  __shared__ int s_tile;
+  __shared__ uint32_t s_cnt[kScanItems][kScanThreads / 32];
+  __shared__ uint32_t s_hist[3][256];
+  __shared__ uint64_t s_excl;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) s_tile = atomicAdd(tile_counter, 1);
+  for (int k = tid; k < 3 * 256; k += kScanThreads) (&s_hist[0][0])[k] = 0;
+  __syncthreads();
+  const int tile = s_tile;
+  const int64_t nvis = *n_vis_dev;
+  const int64_t base = (int64_t)tile * kScanTile;
+  if (base >= nvis) return;
+  uint4 rec[kScanItems];
+  uint32_t pre[kScanItems];
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    const int64_t idx = base + (int64_t)j * kScanThreads + tid;
+    rec[j] = idx < nvis ? recs[sorted_slots[idx]] : make_uint4(0, 0, 0, 0);
+    const uint32_t tt = rec[j].w & 0xFFFFFFu;
+    uint32_t inc = tt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    pre[j] = inc - tt;
+    if (lane == 31) s_cnt[j][warp] = inc;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = kScanThreads / 32;
+    uint32_t a = s_cnt[(2 * lane) / nw][(2 * lane) % nw], b = s_cnt[(2 * lane + 1) / nw][(2 * lane + 1) % nw];
+    uint32_t sum = a + b, inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    const uint32_t ex = inc - sum;
+    s_cnt[(2 * lane) / nw][(2 * lane) % nw] = ex;
+    s_cnt[(2 * lane + 1) / nw][(2 * lane + 1) % nw] = ex + a;
+    const uint32_t agg = __shfl_sync(0xffffffffu, inc, 31);
+    const uint64_t excl = lookback_warp(status, tile, agg);
+    if (lane == 0) {
+      s_excl = excl;
+      if (base + kScanTile >= nvis) {
+        const int64_t I = (int64_t)(excl + agg);
+        *n_inst = I;
+        *overflow = I > max_instances ? 1 : 0;
+      }
+    }
+  }
+  __syncthreads();
+  const uint64_t bex = s_excl;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    const uint32_t tt = rec[j].w & 0xFFFFFFu;
+    if (tt == 0) continue;
+    uint64_t pos = bex + s_cnt[j][warp] + pre[j];
+    const uint32_t view = rec[j].w >> 24;
+    const uint32_t x0 = rec[j].x & 0xFFFFu, x1 = rec[j].x >> 16, y0 = rec[j].y & 0xFFFFu, y1 = rec[j].y >> 16;
+    const uint32_t vbase = view * (uint32_t)tiles_per_view;
+    for (uint32_t ty = y0; ty <= y1; ++ty)
+      for (uint32_t tx = x0; tx <= x1; ++tx, ++pos) {
+        if ((int64_t)pos >= max_instances) continue;
+        const uint32_t key = vbase + ty * (uint32_t)tiles_x + tx;
+        inst_keys[pos] = key;
+        inst_ids[pos] = rec[j].z;
+        atomicAdd(&s_hist[0][key & 255u], 1u);
+        atomicAdd(&s_hist[1][(key >> 8) & 255u], 1u);
+        atomicAdd(&s_hist[2][(key >> 16) & 255u], 1u);
+      }
+  }
+  __syncthreads();
+  for (int k = tid; k < 3 * 256; k += kScanThreads) {
+    const uint32_t c = (&s_hist[0][0])[k];
+    if (c) atomicAdd(&hist2[k], c);
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// 5. tile ranges
+// ------------------------------------------------------------------------------------------------
+__global__ void k_ranges(const uint32_t* __restrict__ keys, const int64_t* n_inst, int64_t max_instances,
+                         uint2* __restrict__ ranges) {
+  int64_t I = *n_inst;
+  if (I > max_instances) I = max_instances;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < I; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = keys[i];
+    if (i == 0 || keys[i - 1] != k) ranges[k].x = (uint32_t)i;
+    if (i == I - 1 || keys[i + 1] != k) ranges[k].y = (uint32_t)(i + 1);
+  }
+}
+
+inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct Layout {
+  size_t keysA, valsA, keysB, valsB, recs, keysC, valsC, keysD, valsD, ranges;
+  size_t st_compact, st_dup, st_depth, st_tile, counters, hist, scalars, end;
+  size_t zero_begin, zero_end;
+  int64_t items;
+  int depth_tiles, inst_tiles, compact_tiles;
+};
+
+Layout layout(int64_t n, int V, int tiles_total, int64_t max_instances) {
+  Layout L;
+  const int64_t items = (int64_t)V * n;
+  L.items = items;
+  L.compact_tiles = (int)((items + kScanTile - 1) / kScanTile);
+  L.depth_tiles = (int)((items + kRadixTile - 1) / kRadixTile);
+  L.inst_tiles = (int)((max_instances + kRadixTile - 1) / kRadixTile);
+  size_t o = 0;
+  auto take = [&](size_t bytes) { const size_t at = o; o = align_up(o + bytes); return at; };
+  L.keysA = take(4 * (size_t)items);
+  L.valsA = take(4 * (size_t)items);
+  L.keysB = take(4 * (size_t)items);
+  L.valsB = take(4 * (size_t)items);
+  L.recs = take(16 * (size_t)items);
+  L.keysC = take(4 * (size_t)max_instances);
+  L.valsC = take(4 * (size_t)max_instances);
+  L.keysD = take(4 * (size_t)max_instances);
+  L.valsD = take(4 * (size_t)max_instances);
+  L.ranges = take(8 * (size_t)tiles_total);
+  L.zero_begin = o;
+  L.st_compact = take(8 * (size_t)L.compact_tiles);
+  L.st_dup = take(8 * (size_t)L.compact_tiles);
+  L.st_depth = take(4 * 256 * 4 * (size_t)L.depth_tiles);
+  L.st_tile = take(3 * 256 * 4 * (size_t)L.inst_tiles);
+  L.counters = take(16 * sizeof(int));
+  L.hist = take(7 * 256 * 4);
+  L.scalars = take(4 * 8);
+  L.zero_end = o;
+  L.end = o;
+  return L;
+}
+
+}  // namespace
+
+size_t bin_sort_ws_bytes(int64_t n, int V, int tiles, int64_t max_instances) {
+  return layout(n, V, tiles * V, max_instances).end;
+}
+
+cudaError_t launch_bin_sort(const uint32_t* depth_key, const uint32_t* tile_rect, const int32_t* tiles_touched,
+                            int64_t n, int V, int tiles_x, int tiles_y, void* ws, size_t ws_bytes,
+                            int64_t max_instances, steepgs_binning* out, cudaStream_t st) {
+  const int tiles_per_view = tiles_x * tiles_y;
+  const int tiles_total = tiles_per_view * V;
+  const Layout L = layout(n, V, tiles_total, max_instances);
+  if (ws_bytes < L.end) return cudaErrorInvalidValue;
+  char* w = static_cast<char*>(ws);
+  auto U32 = [&](size_t off) { return reinterpret_cast<uint32_t*>(w + off); };
+  uint32_t* keysA = U32(L.keysA);
+  uint32_t* valsA = U32(L.valsA);
+  uint32_t* keysB = U32(L.keysB);
+  uint32_t* valsB = U32(L.valsB);
+  uint4* recs = reinterpret_cast<uint4*>(w + L.recs);
+  uint32_t* keysC = U32(L.keysC);
+  uint32_t* valsC = U32(L.valsC);
+  uint32_t* keysD = U32(L.keysD);
+  uint32_t* valsD = U32(L.valsD);
+  uint2* ranges = reinterpret_cast<uint2*>(w + L.ranges);
+  uint64_t* st_compact = reinterpret_cast<uint64_t*>(w + L.st_compact);
+  uint64_t* st_dup = reinterpret_cast<uint64_t*>(w + L.st_dup);
+  uint32_t* st_depth = U32(L.st_depth);
+  uint32_t* st_tile = U32(L.st_tile);
+  int* counters = reinterpret_cast<int*>(w + L.counters);
+  uint32_t* hist = U32(L.hist);
+  int64_t* scalars = reinterpret_cast<int64_t*>(w + L.scalars);
+  int64_t* n_visible = scalars + 0;
+  int64_t* n_inst = scalars + 1;
+  int32_t* overflow = reinterpret_cast<int32_t*>(scalars + 2);
+
+  cudaError_t e = cudaMemsetAsync(w + L.zero_begin, 0, L.zero_end - L.zero_begin, st);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(ranges, 0, 8 * (size_t)tiles_total, st);
+  if (e != cudaSuccess) return e;
+  out->ids = valsC;
+  out->ranges = reinterpret_cast<const uint32_t*>(ranges);
+  out->n_instances = n_inst;
+  out->n_visible = n_visible;
+  out->overflow = overflow;
+  out->max_instances = max_instances;
+  out->tiles_x = tiles_x;
+  out->tiles_y = tiles_y;
+  out->V = V;
+  if (L.items == 0) return cudaSuccess;
+
+  k_compact<<<L.compact_tiles, kScanThreads, 0, st>>>(depth_key, reinterpret_cast<const uint2*>(tile_rect),
+                                                      tiles_touched, n, L.items, keysA, valsA, recs, st_compact,
+                                                      counters + 0, hist, n_visible);
+  note_launch();
+  if ((e = check_launch("k_compact")) != cudaSuccess) return e;
+  // depth sort: A -> B -> A -> B -> A
+  uint32_t *ki = keysA, *vi = valsA, *ko = keysB, *vo = valsB;
+  for (int p = 0; p < 4; ++p) {
+    k_radix_pass<<<L.depth_tiles, kRadixThreads, 0, st>>>(ki, vi, ko, vo, n_visible, L.items, 8 * p, hist + 256 * p,
+                                                          st_depth + (size_t)p * 256 * L.depth_tiles,
+                                                          counters + 1 + p);
+    note_launch();
+    if ((e = check_launch("k_radix_pass(depth)")) != cudaSuccess) return e;
+    uint32_t* t;
+    t = ki; ki = ko; ko = t;
+    t = vi; vi = vo; vo = t;
+  }
+  // sorted slots now in vi (== valsA)
+  k_duplicate<<<L.compact_tiles, kScanThreads, 0, st>>>(vi, recs, n_visible, tiles_x, tiles_per_view,
+                                                        max_instances, keysC, valsC, st_dup, counters + 5,
+                                                        hist + 4 * 256, n_inst, overflow);
+  note_launch();
+  if ((e = check_launch("k_duplicate")) != cudaSuccess) return e;
+  // tile sort: one 8-bit pass per byte of the largest tile key (C -> D -> C ...)
+  const int tile_passes = tiles_total <= 256 ? 1 : (tiles_total <= 65536 ? 2 : 3);
+  uint32_t *tki = keysC, *tvi = valsC, *tko = keysD, *tvo = valsD;
+  for (int p = 0; p < tile_passes; ++p) {
+    k_radix_pass<<<L.inst_tiles > 0 ? L.inst_tiles : 1, kRadixThreads, 0, st>>>(
+        tki, tvi, tko, tvo, n_inst, max_instances, 8 * p, hist + (4 + p) * 256, st_tile + (size_t)p * 256 * L.inst_tiles,
+        counters + 6 + p);
+    note_launch();
+    if ((e = check_launch("k_radix_pass(tile)")) != cudaSuccess) return e;
+    uint32_t* t;
+    t = tki; tki = tko; tko = t;
+    t = tvi; tvi = tvo; tvo = t;
+  }
+  out->ids = tvi;
+  int64_t rb = (max_instances + 255) / 256;
+  if (rb > 148 * 8) rb = 148 * 8;  // grid-stride: the true I is only known on the device
+  k_ranges<<<(unsigned)(rb > 0 ? rb : 1), 256, 0, st>>>(tki, n_inst, max_instances, ranges);
+  note_launch();
+  return check_launch("k_ranges");
+}
+
+}  // namespace sgs

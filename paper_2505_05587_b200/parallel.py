@@ -1,0 +1,40 @@
+"""Multi-GPU plumbing for the view-sharded hot path.
+
+The splitting matrix is an expectation over (Pi, x) (Thm 1) and the gradients are sums over
+views, so view shards combine by elementwise sum: each rank renders the views {v : v mod R = r} into
+its own [20][ld] accumulator (14 gradient planes + 6 S planes, one contiguous buffer), one NCCL
+allreduce sums them, and every rank then runs the densify kernels on bit-identical inputs, so the
+parameters stay replicated without a broadcast.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def shard_views(n_views: int, rank: int, world: int) -> list[int]:
+    """Round-robin view assignment: rank r takes views r, r + R, r + 2R, ..."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    return list(range(rank, n_views, world))
+
+
+def allreduce_accumulators(acc: torch.Tensor, group=None, n: int | None = None) -> torch.Tensor:
+    """Sum the [20][ld] gradient + splitting-matrix accumulator over ranks, in place.
+
+    With `n` given and ld > n, only the first n columns are reduced (20 row slices, coalesced into
+    one NCCL group call); otherwise the whole contiguous buffer is reduced in one call."""
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return acc
+    if n is None or n >= acc.shape[1]:
+        dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
+        return acc
+    flat = acc[:, :n].contiguous()
+    dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+    acc[:, :n].copy_(flat)
+    return acc
+
+
+def params_checksum(params: torch.Tensor, n: int) -> float:
+    """Debug aid: identical on every rank after densify (replicated parameters)."""
+    return float(params[:, :n].double().sum().item())

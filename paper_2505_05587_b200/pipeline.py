@@ -1,0 +1,148 @@
+"""Host-side orchestration of the hot path on torch-owned device buffers.
+
+`Rasterizer` owns the per-call buffers for a fixed (capacity, V, W, H) and issues the C-ABI calls
+in order on one CUDA stream with no host synchronisation (the whole step is graph-capturable).
+PyTorch is used for memory and streams only; every computation happens in libsteepgs.
+"""
+from __future__ import annotations
+
+import dataclasses
+
+import torch
+
+from . import _lib
+
+N_PLANES = 14
+N_ACC = 20
+
+
+@dataclasses.dataclass
+class Raster:
+    alpha_min: float = 1.0 / 255.0
+    alpha_max: float = 0.99
+    t_min: float = 1e-4
+    dilation: float = 0.3
+    bg: tuple = (0.0, 0.0, 0.0)
+
+    def c(self):
+        return _lib.raster_params(self.alpha_min, self.alpha_max, self.t_min, self.dilation, self.bg, 16)
+
+
+SMOOTH = Raster(0.0, 1.0, 0.0, 0.0)
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2505_05587_b200 needs a CUDA device of compute capability 10.x (no CPU fallback)")
+    major, _ = torch.cuda.get_device_capability()
+    if major != 10:
+        raise RuntimeError("paper_2505_05587_b200 is built for sm_100a only")
+
+
+class Rasterizer:
+    def __init__(self, capacity: int, V: int, width: int, height: int, raster: Raster | None = None,
+                 max_instances: int | None = None, device="cuda"):
+        require_cuda()
+        self.cap, self.V, self.W, self.H = int(capacity), int(V), int(width), int(height)
+        self.raster = raster or Raster()
+        self.rp = self.raster.c()
+        self.device = torch.device(device)
+        d = self.device
+        VN = self.V * self.cap
+        self.max_instances = int(max_instances if max_instances is not None else max(4 * VN, 1 << 16))
+        self.splats = torch.empty(max(VN, 1) * _lib.SPLAT_BYTES, dtype=torch.uint8, device=d)
+        self.depth_key = torch.empty(max(VN, 1), dtype=torch.int32, device=d)
+        self.tile_rect = torch.empty(max(VN, 1) * 2, dtype=torch.int32, device=d)
+        self.tiles_touched = torch.empty(max(VN, 1), dtype=torch.int32, device=d)
+        ws = _lib.bin_sort_workspace_size(self.cap, self.V, self.W, self.H, self.max_instances)
+        self.sort_ws = torch.empty(ws, dtype=torch.uint8, device=d)
+        HW = self.W * self.H
+        self.image = torch.empty(self.V, 3, self.H, self.W, dtype=torch.float32, device=d)
+        self.final_T = torch.empty(self.V, self.H, self.W, dtype=torch.float32, device=d)
+        self.n_contrib = torch.empty(self.V, self.H, self.W, dtype=torch.int32, device=d)
+        self.dL = torch.empty(self.V, 3, self.H, self.W, dtype=torch.float32, device=d)
+        self.loss = torch.zeros(self.V, dtype=torch.float32, device=d)
+        self.moments = torch.zeros(max(VN, 1) * 12, dtype=torch.float32, device=d)  # must start at zero
+        self.dens_ws = torch.empty(_lib.densify_workspace_size(self.cap), dtype=torch.uint8, device=d)
+        self.split_mask = torch.empty(self.cap, dtype=torch.uint8, device=d)
+        self.dest_index = torch.empty(self.cap, dtype=torch.int32, device=d)
+        self.lambda_min = torch.empty(self.cap, dtype=torch.float32, device=d)
+        self.n_split = torch.zeros(1, dtype=torch.int64, device=d)
+        self.dens_status = torch.zeros(1, dtype=torch.int32, device=d)
+        self.binning = None
+        self.cams_arr = None
+        self.n = 0
+        self._HW = HW
+
+    # ---- a1 ----
+    def project(self, params: torch.Tensor, n: int, cams: list[dict]):
+        assert len(cams) == self.V and params.shape[0] == N_PLANES and n <= self.cap
+        self.n = int(n)
+        self.cams_arr = _lib.cameras(cams)
+        _lib.project(params, params.shape[1], self.n, self.cams_arr, self.V, self.rp, self.splats, self.depth_key,
+                     self.tile_rect, self.tiles_touched)
+
+    # ---- a2 ----
+    def bin_sort(self):
+        self.binning = _lib.bin_sort(self.depth_key, self.tile_rect, self.tiles_touched, self.n, self.cams_arr, self.V,
+                                     self.rp, self.sort_ws, self.max_instances)
+
+    # ---- a3 ----
+    def render_fwd(self, pair_counts: torch.Tensor | None = None):
+        _lib.render_fwd(self.splats, self.n, self.binning, self.cams_arr, self.V, self.rp, self.image, self.final_T,
+                        self.n_contrib, pair_counts)
+
+    # ---- a4 ----
+    def l1_grad(self, targets: torch.Tensor, with_loss: bool = True):
+        count = 3 * self._HW
+        _lib.l1_grad(self.image, targets, self.V, count, 1.0 / count, self.dL, self.loss if with_loss else None)
+
+    # ---- a5 + a6 ----
+    def render_bwd(self, params: torch.Tensor, grad_S: torch.Tensor, dL: torch.Tensor | None = None,
+                   accumulate: bool = False):
+        dl = self.dL if dL is None else dL
+        _lib.render_bwd_split(params, params.shape[1], self.n, self.splats, self.binning, self.cams_arr, self.V, self.rp, self.final_T, self.n_contrib, dl, self.moments, grad_S,
+                              grad_S.shape[1], accumulate)
+
+    def render_bwd_moments(self, dL: torch.Tensor | None = None):
+        """a5 only (per-pixel replay -> moments)."""
+        _lib.render_bwd_moments(self.splats, self.n, self.binning, self.cams_arr, self.V, self.rp, self.final_T,
+                                self.n_contrib, self.dL if dL is None else dL, self.moments)
+
+    def gauss_bwd(self, params: torch.Tensor, grad_S: torch.Tensor, accumulate: bool = False):
+        """a6 only (moments -> dL/dparams and S)."""
+        _lib.gauss_bwd_split(params, params.shape[1], self.n, self.cams_arr, self.V, self.rp,
+                             self.moments, grad_S, grad_S.shape[1], accumulate)
+
+    # ---- a8 ----
+    def densify(self, params: torch.Tensor, grad_S: torch.Tensor, n: int, capacity: int, eps_split=-1e-6, eta=0.5,
+                eps_abs=0.0, denom=1.0, want_lambda=True):
+        dp = _lib.densify_params(eps_split, eta, eps_abs, denom)
+        _lib.densify(params, params.shape[1], n, capacity, grad_S, grad_S.shape[1], dp, self.split_mask,
+                     self.dest_index, self.lambda_min if want_lambda else None, self.n_split, self.dens_status,
+                     self.dens_ws)
+
+    def forward_backward(self, params, n, cams, targets=None, grad_S=None, dL=None, accumulate=False):
+        """a1..a6 for the V views of this call (no host sync)."""
+        self.project(params, n, cams)
+        self.bin_sort()
+        self.render_fwd()
+        if dL is None:
+            self.l1_grad(targets)
+        self.render_bwd(params, grad_S, dL=dL, accumulate=accumulate)
+
+    # ---- host-side readers (tests / diagnostics; they synchronise) ----
+    def binning_arrays(self):
+        """(ids[I], ranges[V*tiles][2], I, overflow) copied to host."""
+        b = self.binning
+        base = self.sort_ws.data_ptr()
+        def view(ptr_, nbytes, dtype):
+            off = ptr_ - base
+            return self.sort_ws[off:off + nbytes].view(dtype)
+        I = int(view(b.n_instances, 8, torch.int64).item())
+        ovf = int(view(b.overflow, 4, torch.int32).item())
+        nv = int(view(b.n_visible, 8, torch.int64).item())
+        tiles = b.tiles_x * b.tiles_y * b.V
+        ids = view(b.ids, 4 * min(I, self.max_instances), torch.int32).cpu()
+        ranges = view(b.ranges, 8 * tiles, torch.int32).view(tiles, 2).cpu()
+        return dict(ids=ids, ranges=ranges, n_instances=I, overflow=ovf, n_visible=nv)

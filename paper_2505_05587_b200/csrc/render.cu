@@ -2,23 +2,26 @@
 // (Eq. eqn:loss), a5 backward replay with the splitting-matrix moments (Thm 1 P:L232,
 // §4.3).
 //
-// Work decomposition (B200): one 256-thread block per 16x16 tile and view, one pixel per thread;
-// warp w owns the 8x4 sub-block (x: 8 (w & 1) .. +7, y: 4 (w >> 1) .. +3).  The tile's
-// depth-ordered splats are staged through shared memory in batches of 256 (one gathered 48-B record
-// per thread).  While staging, each splat gets an 8-bit mask of the sub-blocks its alpha support
-// {m <= tau} (padded y/x extents sqrt(tau Sigma2D)) can reach; each warp then compacts the batch to
-// the splats of its own sub-block with 8 ballots, so it iterates only over splats that can touch its
-// 32 pixels (SIMT lanes never evaluate pairs outside the sub-block's candidate set).
+// Work decomposition (B200): one 288-thread block per 16x16 tile and view, warp-specialised:
+//   * warps 0..7 (consumers) own one pixel per thread; warp w covers the 8x4 sub-block
+//     x in 8 (w & 1) .. +7, y in 4 (w >> 1) .. +3;
+//   * warp 8 (producer) stages the tile's depth-ordered splats into a ring of kStages shared-memory
+//     buffers of kBatch splats (gathered 48-B records), computes for each splat the 8-bit mask of
+//     sub-blocks its alpha support {m <= tau} (padded extents sqrt(tau Sigma2D)) can reach, and
+//     compacts each batch into one list per consumer warp.
+// Full/empty mbarriers per buffer replace block-wide barriers, so consumer warps with short lists
+// run ahead by up to kStages batches instead of waiting for the slowest warp, and a consumer
+// iterates only over the splats that can touch its 32 pixels.
 //
-// Per-pair arithmetic: the mean is made tile-relative in fp64 before rounding (offsets d = x - Pi(p)
-// carry ~1e-7 px error); the conic is pre-scaled by log2(e)/2 at staging so that
+// Per-pair arithmetic: the mean is made tile-relative in fp64 before rounding (offsets
+// d = x - Pi(p) carry ~1e-7 px error); the conic is pre-scaled by log2(e)/2 at staging so that
 //   e = log2(o) - m',  m' = a + dy (b + Qyy' dy),  a = Qxx' dx^2,  b = 2 Qxy' dx,
-//   skip if e < log2(alpha_min) (<=> sigma < alpha_min),  sigma = exp2(e),  alpha = min(amax, sigma)
-// with explicit round-to-nearest intrinsics in one shared function, so forward and backward take
-// bit-identical decisions.
+//   skip if e < log2(alpha_min) (<=> sigma < alpha_min),  sigma = 2^e,  alpha = min(amax, sigma)
+// in one function shared by both kernels (explicit round-to-nearest intrinsics), so forward and
+// backward take bit-identical decisions.
 //
 // Backward: back to front over each pixel's composited prefix (n_contrib from the forward), T_i
-// recovered as T_{i+1} / (1 - alpha_i) (fast reciprocal; relative error ~1 ulp per step),
+// recovered as T_{i+1} / (1 - alpha_i) (approximate reciprocal; relative error ~1 ulp per step),
 // dL/dalpha_i = T_i sum_ch dL/dC_ch (c_ch - B_ch) with B the normalised colour behind (C10),
 // w = dL/dsigma * sigma.  The 9 per-pair values (w, w d, w d d^T, alpha T dL/dC) are reduced across
 // the warp with a transposed butterfly (12 shuffles instead of 45) and added with one 9-lane RED per
@@ -30,71 +33,63 @@ namespace sgs {
 
 namespace {
 
-constexpr int kThreads = 256;          // one pixel per thread, 8 warps per 16x16 tile
-constexpr int kBatch = 256;            // splats staged per batch (one per thread)
+constexpr int kConsumers = 8;                       // one pixel per thread, 8 warps per 16x16 tile
+constexpr int kThreads = 32 * (kConsumers + 1);     // + 1 producer warp
+constexpr int kBatch = 128;                         // splats per staged batch
+constexpr int kStages = 3;                          // ring depth
 constexpr float kHalfLog2e = 0.72134752044448170f;  // log2(e) / 2
 
-struct Staged {
-  float4* geo;      // (mu_x - ox, mu_y - oy, Qxx', 2 Qxy')   Q' = Q log2(e)/2
-  float4* par;      // (Qyy', log2(o), -, -)
-  float4* col;      // (r, g, b, -)
-  uint32_t* gid;
-  uint32_t* mask;   // bit k: alpha support reaches sub-block k (8x4 px)
+struct Buffer {
+  float4 geo[kBatch];            // (mu_x - ox, mu_y - oy, Qxx', 2 Qxy')   Q' = Q log2(e)/2
+  float4 par[kBatch];            // (Qyy', log2(o), -, -)
+  float4 col[kBatch];            // (r, g, b, -)
+  float* mptr[kBatch];           // backward: &moments[view][gid][0]
+  uint8_t list[kConsumers][kBatch];
+  int count[kConsumers];
+  int base;                      // list position (relative to the tile start) of slot 0
+  int stop;                      // 1: no more batches (forward early termination)
 };
 
-// Stage splat `gid` into slot k: tile-relative mean (fp64 -> fp32), pre-scaled conic, log2(o), and
-// the sub-block mask from the padded extents of {m <= tau} (a degenerate det keeps every block).
-__device__ __forceinline__ void stage(const steepgs_splat* __restrict__ vs, uint32_t gid, double ox, double oy,
-                                      Staged S, int k) {
-  const steepgs_splat* sp = vs + gid;
-  const double2 mean = *reinterpret_cast<const double2*>(sp);
-  const float4 a = *(reinterpret_cast<const float4*>(sp) + 1);
-  const float4 b = *(reinterpret_cast<const float4*>(sp) + 2);
-  const float gx = (float)(mean.x - ox), gy = (float)(mean.y - oy);
-  S.geo[k] = make_float4(gx, gy, __fmul_rn(a.x, kHalfLog2e), __fmul_rn(2.0f * a.y, kHalfLog2e));
-  S.par[k] = make_float4(__fmul_rn(a.z, kHalfLog2e), __log2f(a.w), 0.0f, 0.0f);
-  S.col[k] = make_float4(b.x, b.y, b.z, 0.0f);
-  S.gid[k] = gid;
-  const float detq = a.x * a.z - a.y * a.y;
-  uint32_t m = 0xFFu;
-  if (detq > 0.0f) {
-    const float ex = sqrtf(b.w * (a.z / detq)) * 1.001f + 0.01f;
-    const float ey = sqrtf(b.w * (a.x / detq)) * 1.001f + 0.01f;
-    if (ex == ex && ey == ey) {
-      uint32_t xb = 0u, yb = 0u;
-#pragma unroll
-      for (int q = 0; q < 2; ++q)
-        if (gx - ex <= 8.0f * q + 7.5f && gx + ex >= 8.0f * q + 0.5f) xb |= 1u << q;
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (gy - ey <= 4.0f * q + 3.5f && gy + ey >= 4.0f * q + 0.5f) yb |= 1u << q;
-      m = 0u;
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (yb & (1u << q)) m |= xb << (2 * q);
-    }
-  }
-  S.mask[k] = m;
+struct Smem {
+  Buffer buf[kStages];
+  unsigned long long full[kStages], empty[kStages];
+  int done_warps;
+  int maxlast;
+};
+
+__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity) {
+  uint32_t ok = 0;
+  const uint32_t a = saddr(b);
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!ok);
 }
 
-// Per-warp compaction of the staged batch to the splats whose mask has bit `w`; returns the count.
-__device__ __forceinline__ int warp_list(const uint32_t* __restrict__ s_mask, int cnt, int w, int lane,
-                                         uint8_t* __restrict__ list) {
-  int total = 0;
-  const uint32_t lt = (1u << lane) - 1u;
-#pragma unroll
-  for (int c = 0; c < kBatch / 32; ++c) {
-    const int j = c * 32 + lane;
-    const bool hit = j < cnt && ((s_mask[j] >> w) & 1u);
-    const uint32_t bal = __ballot_sync(0xffffffffu, hit);
-    if (hit) list[total + __popc(bal & lt)] = (uint8_t)j;
-    total += __popc(bal);
-  }
-  __syncwarp();
-  return total;
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
-// The pair test shared by forward and backward: returns e = log2(sigma) (skip if e < lmin).
+// The pair test shared by forward and backward: e = log2(sigma) (skip if e < log2(alpha_min)).
 __device__ __forceinline__ float pair_e(float dx, float dy, const float4 g, const float4 p) {
   const float a = __fmul_rn(__fmul_rn(g.z, dx), dx);
   const float bq = __fmul_rn(g.w, dx);
@@ -102,59 +97,149 @@ __device__ __forceinline__ float pair_e(float dx, float dy, const float4 g, cons
   return __fsub_rn(p.y, m);
 }
 
-__global__ void __launch_bounds__(kThreads) k_render_fwd(const steepgs_splat* __restrict__ splats,
+// Producer: stage splats [first, first + cnt) of the tile list into `B` (lane-strided), then build
+// the 8 per-consumer lists.  Runs on the producer warp only.
+__device__ __forceinline__ void produce(Buffer& B, const uint32_t* __restrict__ ids, const steepgs_splat* __restrict__ vs,
+                                        uint32_t first, int cnt, double ox, double oy, float* mom_view, int lane) {
+  uint32_t mask[kBatch / 32];
+#pragma unroll
+  for (int q = 0; q < kBatch / 32; ++q) {
+    const int k = q * 32 + lane;
+    mask[q] = 0u;
+    if (k < cnt) {
+      const uint32_t gid = ids[first + k];
+      const steepgs_splat* sp = vs + gid;
+      const double2 mean = __ldg(reinterpret_cast<const double2*>(sp));
+      const float4 a = __ldg(reinterpret_cast<const float4*>(sp) + 1);
+      const float4 b = __ldg(reinterpret_cast<const float4*>(sp) + 2);
+      const float gx = (float)(mean.x - ox), gy = (float)(mean.y - oy);
+      B.geo[k] = make_float4(gx, gy, __fmul_rn(a.x, kHalfLog2e), __fmul_rn(2.0f * a.y, kHalfLog2e));
+      B.par[k] = make_float4(__fmul_rn(a.z, kHalfLog2e), __log2f(a.w), 0.0f, 0.0f);
+      B.col[k] = make_float4(b.x, b.y, b.z, 0.0f);
+      if (mom_view) B.mptr[k] = mom_view + (size_t)gid * 12;
+      // padded extents of {m <= tau}; a degenerate det keeps every sub-block
+      const float detq = a.x * a.z - a.y * a.y;
+      uint32_t m = 0xFFu;
+      if (detq > 0.0f) {
+        const float ex = sqrtf(b.w * (a.z / detq)) * 1.001f + 0.01f;
+        const float ey = sqrtf(b.w * (a.x / detq)) * 1.001f + 0.01f;
+        if (ex == ex && ey == ey) {
+          uint32_t xb = 0u, yb = 0u;
+#pragma unroll
+          for (int s = 0; s < 2; ++s)
+            if (gx - ex <= 8.0f * s + 7.5f && gx + ex >= 8.0f * s + 0.5f) xb |= 1u << s;
+#pragma unroll
+          for (int s = 0; s < 4; ++s)
+            if (gy - ey <= 4.0f * s + 3.5f && gy + ey >= 4.0f * s + 0.5f) yb |= 1u << s;
+          m = 0u;
+#pragma unroll
+          for (int s = 0; s < 4; ++s)
+            if (yb & (1u << s)) m |= xb << (2 * s);
+        }
+      }
+      mask[q] = m;
+    }
+  }
+  const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int w = 0; w < kConsumers; ++w) {
+    int total = 0;
+#pragma unroll
+    for (int q = 0; q < kBatch / 32; ++q) {
+      const bool hit = (mask[q] >> w) & 1u;
+      const uint32_t bal = __ballot_sync(0xffffffffu, hit);
+      if (hit) B.list[w][total + __popc(bal & lt)] = (uint8_t)(q * 32 + lane);
+      total += __popc(bal);
+    }
+    if (lane == 0) B.count[w] = total;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 4) k_render_fwd(const steepgs_splat* __restrict__ splats,
                                                          const uint32_t* __restrict__ ids,
                                                          const uint2* __restrict__ ranges, int64_t n, int W, int H,
                                                          int tiles_x, int tiles_per_view, const RasterK rk,
                                                          float* __restrict__ image, float* __restrict__ final_T,
                                                          int32_t* __restrict__ n_contrib,
                                                          unsigned long long* __restrict__ pair_counts) {
-  __shared__ float4 s_geo[kBatch], s_par[kBatch], s_col[kBatch];
-  __shared__ uint32_t s_gid[kBatch], s_mask[kBatch];
-  __shared__ uint8_t s_list[kThreads / 32][kBatch];
-  const Staged S{s_geo, s_par, s_col, s_gid, s_mask};
+  __shared__ Smem sm;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int tile = blockIdx.x, view = blockIdx.y;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
+  const double ox = (double)(tx * kTile), oy = (double)(ty * kTile);
+  const uint2 rg = ranges[(int64_t)view * tiles_per_view + tile];
+  const int nb = (int)((rg.y - rg.x + kBatch - 1) / kBatch);
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&sm.full[s], 32);
+      mbar_init(&sm.empty[s], 32 * kConsumers);
+    }
+    sm.done_warps = 0;
+  }
+  __syncthreads();
+
+  if (warp == kConsumers) {  // ---------------- producer ----------------
+    const steepgs_splat* vs = splats + (int64_t)view * n;
+    for (int k = 0; k < nb; ++k) {
+      const int s = k % kStages;
+      if (k >= kStages) mbar_wait(&sm.empty[s], ((k / kStages) & 1) ^ 1);
+      Buffer& B = sm.buf[s];
+      const int stop = *reinterpret_cast<volatile int*>(&sm.done_warps) == kConsumers;
+      if (!stop) {
+        const uint32_t first = rg.x + (uint32_t)k * kBatch;
+        produce(B, ids, vs, first, min((int)(rg.y - first), kBatch), ox, oy, nullptr, lane);
+      }
+      if (lane == 0) { B.base = k * kBatch; B.stop = stop; }
+      __syncwarp();
+      mbar_arrive(&sm.full[s]);
+      if (stop) break;
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
   const int lx = 8 * (warp & 1) + (lane & 7), ly = 4 * (warp >> 1) + (lane >> 3);
   const int px = tx * kTile + lx, py = ty * kTile + ly;
   const bool inside = px < W && py < H;
   const float fx = (float)lx + 0.5f, fy = (float)ly + 0.5f;  // pixel centre, tile-relative (Z5)
-  const double ox = (double)(tx * kTile), oy = (double)(ty * kTile);
-  const uint2 rg = ranges[(int64_t)view * tiles_per_view + tile];
-  const steepgs_splat* vs = splats + (int64_t)view * n;
-  const float lmin = __log2f(rk.alpha_min);  // -inf in smooth mode
+  const float lmin = __log2f(rk.alpha_min);                   // -inf in smooth mode
   float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
   int last = 0, ncomp = 0, neval = 0;
-  bool done = !inside;
-  uint8_t* mylist = s_list[warp];
-  for (uint32_t b = rg.x; b < rg.y; b += kBatch) {
-    if (__syncthreads_count(done) == kThreads) break;
-    if (b + tid < rg.y) stage(vs, ids[b + tid], ox, oy, S, tid);
-    __syncthreads();
-    const int cnt = min((int)(rg.y - b), kBatch);
-    const int nl = warp_list(s_mask, cnt, warp, lane, mylist);
-    for (int t = 0; t < nl; ++t) {
-      if (__all_sync(0xffffffffu, done)) break;
-      const int j = mylist[t];
-      const float4 g = s_geo[j];
-      const float4 p = s_par[j];
-      if (done) continue;
-      ++neval;
-      const float e = pair_e(__fsub_rn(fx, g.x), __fsub_rn(fy, g.y), g, p);
-      if (e < lmin) continue;                          // sigma < alpha_min: C8 skip
-      const float alpha = fminf(rk.alpha_max, exp2f(e));
-      const float Tn = __fmul_rn(T, __fsub_rn(1.0f, alpha));
-      if (Tn < rk.t_min) { done = true; continue; }    // C8 termination
-      const float4 c = s_col[j];
-      const float aT = __fmul_rn(alpha, T);
-      C0 = __fmaf_rn(aT, c.x, C0);
-      C1 = __fmaf_rn(aT, c.y, C1);
-      C2 = __fmaf_rn(aT, c.z, C2);
-      T = Tn;
-      last = (int)(b - rg.x) + j + 1;
-      ++ncomp;
+  bool done = !inside, warp_done = false;
+  for (int k = 0; k < nb; ++k) {
+    const int s = k % kStages;
+    mbar_wait(&sm.full[s], (k / kStages) & 1);
+    const Buffer& B = sm.buf[s];
+    if (B.stop) break;
+    if (!warp_done) {
+      const int nl = B.count[warp];
+      const uint8_t* lst = B.list[warp];
+      for (int t = 0; t < nl; ++t) {
+        const int j = lst[t];
+        const float4 g = B.geo[j];
+        const float4 p = B.par[j];
+        if (done) continue;
+        ++neval;
+        const float e = pair_e(__fsub_rn(fx, g.x), __fsub_rn(fy, g.y), g, p);
+        if (e < lmin) continue;                           // sigma < alpha_min: C8 skip
+        const float alpha = fminf(rk.alpha_max, ex2_approx(e));
+        const float Tn = __fmul_rn(T, __fsub_rn(1.0f, alpha));
+        if (Tn < rk.t_min) { done = true; continue; }     // C8 termination
+        const float4 c = B.col[j];
+        const float aT = __fmul_rn(alpha, T);
+        C0 = __fmaf_rn(aT, c.x, C0);
+        C1 = __fmaf_rn(aT, c.y, C1);
+        C2 = __fmaf_rn(aT, c.z, C2);
+        T = Tn;
+        last = B.base + j + 1;
+        ++ncomp;
+      }
+      if (__all_sync(0xffffffffu, done)) {
+        warp_done = true;
+        if (lane == 0) atomicAdd(&sm.done_warps, 1);
+      }
     }
+    mbar_arrive(&sm.empty[s]);
   }
   if (inside) {
     const int64_t HW = (int64_t)W * H;
@@ -180,42 +265,27 @@ __global__ void __launch_bounds__(kThreads) k_render_fwd(const steepgs_splat* __
   }
 }
 
-// Transposed warp reduction of 9 values (see header comment).  After the call, lane l holds in
-// v[0] the warp sum of value index slot_of(l) (lanes l and l^1 hold the same value).
-template <int NIN, int OFF>
-__device__ __forceinline__ void tstage(float* v, bool upper) {
-  constexpr int NK = (NIN + 1) / 2;
-#pragma unroll
-  for (int s = 0; s < NK; ++s) {
-    const float hi = (NK + s < NIN) ? v[NK + s] : 0.0f;
-    const float keep = upper ? hi : v[s];
-    const float send = upper ? v[s] : hi;
-    v[s] = keep + __shfl_xor_sync(0xffffffffu, send, OFF);
-  }
+constexpr int kChunk = 16;   // list entries per backward chunk (phase 1 -> phase 2)
+
+struct BwdScratch {
+  float w[kConsumers][kChunk][32];     // dL/dsigma * sigma per (entry, pixel), xor-swizzled columns
+  float at[kConsumers][kChunk][32];    // alpha * T per (entry, pixel)
+  uint32_t cmask[kConsumers][kChunk];  // contributing pixels of each entry (ballot)
+  float4 dl[kConsumers * 32];          // dL/dC of each pixel of the tile
+};
+
+__device__ __forceinline__ void red_v4(float* p, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
 }
 
-__device__ __forceinline__ void reduce9(float* v, int lane) {
-  tstage<9, 16>(v, lane & 16);
-  tstage<5, 8>(v, lane & 8);
-  tstage<3, 4>(v, lane & 4);
-  tstage<2, 2>(v, lane & 2);
-  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-}
-
-__device__ __forceinline__ int slot_of(int lane) {
-  int lo = 0, len = 9;
-  const int nins[4] = {9, 5, 3, 2};
-  const int bits[4] = {16, 8, 4, 2};
-#pragma unroll
-  for (int s = 0; s < 4; ++s) {
-    const int nk = (nins[s] + 1) / 2;
-    if (lane & bits[s]) { lo += nk; len -= nk; }
-    else if (len > nk) len = nk;
-  }
-  return (len >= 1 && (lane & 1) == 0) ? lo : -1;
-}
-
-__global__ void __launch_bounds__(kThreads) k_render_bwd(const steepgs_splat* __restrict__ splats,
+// Backward.  Per consumer warp and chunk of <= 16 list entries (back to front):
+//   phase 1 (pixel-parallel): each lane runs its pixel's recursion over the chunk and leaves
+//     w = dL/dsigma * sigma and alpha T in shared memory, plus a ballot of contributing pixels;
+//   phase 2 (splat-parallel): lanes e and e + 16 own entry e and sum its 9 moments over the
+//     contributing pixels (each half over 16 pixels), combine with one xor-16 shuffle per value, and
+//     add them with two 16-B + one 4-B vector REDs.
+// No per-(warp, splat) cross-lane reduction tree: the reduction costs O(contributing pairs).
+__global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat* __restrict__ splats,
                                                          const uint32_t* __restrict__ ids,
                                                          const uint2* __restrict__ ranges, int64_t n, int W, int H,
                                                          int tiles_x, int tiles_per_view, const RasterK rk,
@@ -223,24 +293,19 @@ __global__ void __launch_bounds__(kThreads) k_render_bwd(const steepgs_splat* __
                                                          const int32_t* __restrict__ n_contrib,
                                                          const float* __restrict__ dL_dimage,
                                                          float* __restrict__ moments) {
-  __shared__ float4 s_geo[kBatch], s_par[kBatch], s_col[kBatch];
-  __shared__ uint32_t s_gid[kBatch], s_mask[kBatch];
-  __shared__ uint8_t s_list[kThreads / 32][kBatch];
-  __shared__ int s_maxlast;
-  const Staged S{s_geo, s_par, s_col, s_gid, s_mask};
+  extern __shared__ __align__(16) unsigned char dsmem[];
+  Smem& sm = *reinterpret_cast<Smem*>(dsmem);
+  BwdScratch& sc = *reinterpret_cast<BwdScratch*>(dsmem + ((sizeof(Smem) + 15) & ~size_t(15)));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int tile = blockIdx.x, view = blockIdx.y;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
-  const int lx = 8 * (warp & 1) + (lane & 7), ly = 4 * (warp >> 1) + (lane >> 3);
-  const int px = tx * kTile + lx, py = ty * kTile + ly;
-  const bool inside = px < W && py < H;
-  const float fx = (float)lx + 0.5f, fy = (float)ly + 0.5f;
   const double ox = (double)(tx * kTile), oy = (double)(ty * kTile);
   const uint2 rg = ranges[(int64_t)view * tiles_per_view + tile];
-  const steepgs_splat* vs = splats + (int64_t)view * n;
   const int64_t HW = (int64_t)W * H;
+  const int lx = 8 * (warp & 1) + (lane & 7), ly = 4 * (warp >> 1) + (lane >> 3);
+  const int px = tx * kTile + lx, py = ty * kTile + ly;
+  const bool inside = warp < kConsumers && px < W && py < H;
   const int64_t pix = (int64_t)py * W + px;
-  const float lmin = __log2f(rk.alpha_min);
   float T = 1.0f, dl0 = 0.0f, dl1 = 0.0f, dl2 = 0.0f;
   int last = 0;
   if (inside) {
@@ -249,61 +314,131 @@ __global__ void __launch_bounds__(kThreads) k_render_bwd(const steepgs_splat* __
     const float* dl = dL_dimage + (int64_t)view * 3 * HW;
     dl0 = dl[pix]; dl1 = dl[HW + pix]; dl2 = dl[2 * HW + pix];
   }
-  if (tid == 0) s_maxlast = 0;
+  if (warp < kConsumers) sc.dl[tid] = make_float4(dl0, dl1, dl2, 0.0f);
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&sm.full[s], 32);
+      mbar_init(&sm.empty[s], 32 * kConsumers);
+    }
+    sm.maxlast = 0;
+  }
   __syncthreads();
   const int wmax = __reduce_max_sync(0xffffffffu, last);
-  if (lane == 0) atomicMax(&s_maxlast, wmax);
+  if (lane == 0 && wmax > 0) atomicMax(&sm.maxlast, wmax);
   __syncthreads();
-  const int L = s_maxlast;
-  float B0 = rk.bg[0], B1 = rk.bg[1], B2 = rk.bg[2];
-  const int my_slot = slot_of(lane);
-  float* mom_view = moments + (int64_t)view * n * 12;
-  uint8_t* mylist = s_list[warp];
+  const int L = sm.maxlast;              // list prefix any pixel of the tile composited
   const int nb = (L + kBatch - 1) / kBatch;
-  for (int bb = nb - 1; bb >= 0; --bb) {
-    const uint32_t b = rg.x + (uint32_t)bb * kBatch;
-    const int cnt = min(L - bb * kBatch, kBatch);
-    __syncthreads();
-    if (tid < cnt) stage(vs, ids[b + tid], ox, oy, S, tid);
-    __syncthreads();
-    const int nl = warp_list(s_mask, cnt, warp, lane, mylist);
-    for (int t = nl - 1; t >= 0; --t) {
-      const int j = mylist[t];
-      const int li = bb * kBatch + j;                  // list position relative to the tile start
-      const float4 g = s_geo[j];
-      const float4 p = s_par[j];
-      float v[9];
-      bool contrib = false;
-      const float dx = __fsub_rn(fx, g.x), dy = __fsub_rn(fy, g.y);
-      if (li < last) {
-        const float e = pair_e(dx, dy, g, p);
-        if (e >= lmin) {
-          contrib = true;
-          const float sigma = exp2f(e);
-          const float alpha = fminf(rk.alpha_max, sigma);
-          const float4 c = s_col[j];
-          const float om = 1.0f - alpha;
-          T = __fdividef(T, om);                          // T_i (before this splat)
-          const float gsum = dl0 * (c.x - B0) + dl1 * (c.y - B1) + dl2 * (c.z - B2);
-          const float w = T * gsum * sigma;               // dL/dalpha * sigma (straight-through, Z3)
-          B0 = alpha * c.x + om * B0;
-          B1 = alpha * c.y + om * B1;
-          B2 = alpha * c.z + om * B2;
-          const float aT = alpha * T;
+
+  if (warp == kConsumers) {  // ---------------- producer: batches from the back ----------------
+    const steepgs_splat* vs = splats + (int64_t)view * n;
+    float* mom_view = moments + (int64_t)view * n * 12;
+    for (int k = 0; k < nb; ++k) {
+      const int s = k % kStages;
+      if (k >= kStages) mbar_wait(&sm.empty[s], ((k / kStages) & 1) ^ 1);
+      Buffer& B = sm.buf[s];
+      const int bb = nb - 1 - k;
+      const uint32_t first = rg.x + (uint32_t)bb * kBatch;
+      produce(B, ids, vs, first, min(L - bb * kBatch, kBatch), ox, oy, mom_view, lane);
+      if (lane == 0) B.base = bb * kBatch;
+      __syncwarp();
+      mbar_arrive(&sm.full[s]);
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  const float fx = (float)lx + 0.5f, fy = (float)ly + 0.5f;
+  const float lmin = __log2f(rk.alpha_min);
+  float B0 = rk.bg[0], B1 = rk.bg[1], B2 = rk.bg[2];
+  float(*sw)[32] = sc.w[warp];
+  float(*sat)[32] = sc.at[warp];
+  uint32_t* scm = sc.cmask[warp];
+  const float4* sdl = sc.dl + warp * 32;
+  const int e2 = lane & (kChunk - 1), half = lane >> 4;
+  const float cx0 = (float)(8 * (warp & 1)) + 0.5f, cy0 = (float)(4 * (warp >> 1)) + 0.5f;
+  for (int k = 0; k < nb; ++k) {
+    const int s = k % kStages;
+    mbar_wait(&sm.full[s], (k / kStages) & 1);
+    const Buffer& B = sm.buf[s];
+    const uint8_t* lst = B.list[warp];
+    int nl = B.count[warp];
+    while (nl > 0 && B.base + lst[nl - 1] >= wmax) --nl;   // beyond every pixel's prefix (warp-uniform)
+    const int lim = last - B.base;                          // this pixel composited list positions < last
+    for (int t_hi = nl; t_hi > 0; t_hi -= kChunk) {
+      const int t_lo = max(0, t_hi - kChunk);
+      // ---- phase 1: pixel-parallel recursion over entries t_hi-1 .. t_lo ----
+      for (int t = t_hi - 1; t >= t_lo; --t) {
+        const int j = lst[t];
+        const int e = t - t_lo;
+        bool contrib = false;
+        if (j < lim) {
+          const float4 g = B.geo[j];
+          const float4 p = B.par[j];
+          const float ee = pair_e(__fsub_rn(fx, g.x), __fsub_rn(fy, g.y), g, p);
+          if (ee >= lmin) {
+            contrib = true;
+            const float sigma = ex2_approx(ee);
+            const float alpha = fminf(rk.alpha_max, sigma);
+            const float4 c = B.col[j];
+            const float om = 1.0f - alpha;
+            T = T * rcp_approx(om);                         // T_i (before this splat)
+            const float gsum = dl0 * (c.x - B0) + dl1 * (c.y - B1) + dl2 * (c.z - B2);
+            B0 = alpha * c.x + om * B0;
+            B1 = alpha * c.y + om * B1;
+            B2 = alpha * c.z + om * B2;
+            sw[e][lane ^ e] = T * gsum * sigma;             // dL/dalpha * sigma (straight-through, Z3)
+            sat[e][lane ^ e] = alpha * T;
+          }
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, contrib);
+        if (lane == 0) scm[e] = bal;
+      }
+      __syncwarp();
+      // ---- phase 2: splat-parallel sums (lanes e2 and e2 + 16 own entry e2) ----
+      const int ne = t_hi - t_lo;
+      float acc[9];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) acc[q] = 0.0f;
+      const bool valid = e2 < ne;
+      int j2 = 0;
+      uint32_t full_bits = 0u;
+      if (valid) {
+        j2 = lst[t_lo + e2];
+        full_bits = scm[e2];
+        uint32_t bits = half ? (full_bits >> 16) : (full_bits & 0xFFFFu);
+        const float4 g = B.geo[j2];
+        const float gx = g.x, gy = g.y;
+        while (bits) {
+          const int pp = (half << 4) + __ffs(bits) - 1;
+          bits &= bits - 1u;
+          const float w = sw[e2][pp ^ e2];
+          const float at = sat[e2][pp ^ e2];
+          const float dx = (cx0 + (float)(pp & 7)) - gx;
+          const float dy = (cy0 + (float)(pp >> 3)) - gy;
+          const float4 d = sdl[pp];
           const float wdx = w * dx, wdy = w * dy;
-          v[0] = w; v[1] = wdx; v[2] = wdy;
-          v[3] = wdx * dx; v[4] = wdx * dy; v[5] = wdy * dy;
-          v[6] = aT * dl0; v[7] = aT * dl1; v[8] = aT * dl2;
+          acc[0] += w;
+          acc[1] += wdx;
+          acc[2] += wdy;
+          acc[3] = fmaf(wdx, dx, acc[3]);
+          acc[4] = fmaf(wdx, dy, acc[4]);
+          acc[5] = fmaf(wdy, dy, acc[5]);
+          acc[6] = fmaf(at, d.x, acc[6]);
+          acc[7] = fmaf(at, d.y, acc[7]);
+          acc[8] = fmaf(at, d.z, acc[8]);
         }
       }
-      if (!__any_sync(0xffffffffu, contrib)) continue;
-      if (!contrib) {
 #pragma unroll
-        for (int q = 0; q < 9; ++q) v[q] = 0.0f;
+      for (int q = 0; q < 9; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], 16);
+      if (valid && half == 0 && full_bits) {
+        float* mp = B.mptr[j2];
+        red_v4(mp, acc[0], acc[1], acc[2], acc[3]);
+        red_v4(mp + 4, acc[4], acc[5], acc[6], acc[7]);
+        atomicAdd(mp + 8, acc[8]);
       }
-      reduce9(v, lane);
-      if (my_slot >= 0) atomicAdd(mom_view + (int64_t)s_gid[j] * 12 + my_slot, v[0]);
+      __syncwarp();
     }
+    mbar_arrive(&sm.empty[s]);
   }
 }
 
@@ -347,6 +482,7 @@ cudaError_t launch_render_fwd(const steepgs_splat* splats, int64_t n, const stee
   note_launch();
   return check_launch("k_render_fwd");
 }
+
 cudaError_t launch_l1_grad(const float* image, const float* target, int V, int64_t count, float scale, float* dL,
                            float* loss, cudaStream_t st) {
   if (loss) {
@@ -367,7 +503,14 @@ cudaError_t launch_render_bwd(const steepgs_splat* splats, const steepgs_binning
                               const float* dL_dimage, int64_t n, float* moments, cudaStream_t st) {
   const int tpv = b.tiles_x * b.tiles_y;
   dim3 grid(tpv, b.V);
-  k_render_bwd<<<grid, kThreads, 0, st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
+  const size_t smem = ((sizeof(Smem) + 15) & ~size_t(15)) + sizeof(BwdScratch);
+  static bool attr_set = false;  // per process; the attribute is a property of the function
+  if (!attr_set) {
+    const cudaError_t e = cudaFuncSetAttribute(k_render_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  k_render_bwd<<<grid, kThreads, smem, st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
                                           b.tiles_x, tpv, rk, final_T, n_contrib, dL_dimage, moments);
   note_launch();
   return check_launch("k_render_bwd");

@@ -276,11 +276,11 @@ def main():
     # algorithmic (compulsory) bytes per launch of each stage
     byts = {
         "restore": 2 * 16 * n,
-        "project": 56 * n + V * 16 * n + 48 * n_vis,
+        "project": 56 * n + V * 16 * n + 64 * n_vis,
         "bin_sort": V * 16 * n + 8 * n_vis + 20 * n_inst + 8 * tiles * V,
-        "render_fwd": 4 * n_inst + 48 * n_vis + 20 * px * V,
+        "render_fwd": 4 * n_inst + 64 * n_vis + 20 * px * V,
         "l1_grad": 36 * px * V,
-        "render_bwd": 4 * n_inst + 48 * n_vis + 28 * px * V + 48 * n_vis,
+        "render_bwd": 4 * n_inst + 64 * n_vis + 28 * px * V + 48 * n_vis,
         "gauss_bwd_S": 56 * n + 4 * V * n + 96 * n_vis + 80 * n,
         "densify": 24 * n + 8 * n + 24 * n + n_split * (56 + 56 + 80),
     }

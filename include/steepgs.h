@@ -21,7 +21,7 @@
  *            (w,x,y,z; normalised on use), 10 opacity logit, 11-13 rgb.          (C1)
  *  - grad_S  [20][ldg] fp32 planar: 0-13 dL/d(param plane k), 14-19 splitting matrix S
  *            (xx,xy,xz,yy,yz,zz).  Summed over views (and, by the caller, over steps/ranks).
- *  - splats  [V][n] steepgs_splat (48 B): the per-(view, Gaussian) projected record.
+ *  - splats  [V][n] steepgs_splat (64 B): the per-(view, Gaussian) projected record.
  *  - images  [V][3][H][W] fp32; per-pixel planes [V][H][W].  All views of a call share W, H.
  */
 #ifndef STEEPGS_H
@@ -74,15 +74,21 @@ typedef struct {
   int32_t gate;
 } steepgs_densify_params;
 
-/* Projected splat (a1 output).  mean Pi(p) in pixels kept in fp64 so that per-pair offsets are
- * exact to ~1e-7 px after tile-relative rounding; conic Q = Pi(Sigma)^-1 (xx, xy, yy) with
- * dilation; opacity o = sigmoid(logit); rgb; tau = 2 ln(o / alpha_min) (alpha-support bound). */
+/* Projected splat (a1 output), 64 B.  mean Pi(p) in pixels kept in fp64 so that per-pair offsets
+ * are exact to ~1e-7 px after tile-relative rounding; conic Q = Pi(Sigma)^-1 (with dilation)
+ * stored pre-scaled for exp2 as (Qxx, 2 Qxy, Qyy) * log2(e)/2, so sigma = 2^(log2_opacity - m'),
+ * m' = conic[0] dx^2 + conic[1] dx dy + conic[2] dy^2; opacity o = sigmoid(logit); rgb;
+ * extent = padded half-extents (pixels) of the alpha support {d^T Q d <= tau} along x and y;
+ * tau = 2 ln(o / alpha_min).  Conic, mean and extents are formed in fp64 and rounded once. */
 typedef struct {
   double mean[2];
   float conic[3];
-  float opacity;
+  float log2_opacity;
   float rgb[3];
+  float opacity;
+  float extent[2];
   float tau;
+  float reserved;
 } steepgs_splat;
 
 /* Binning result: device pointers into the caller's workspace.  [host] struct. */

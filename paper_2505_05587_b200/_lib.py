@@ -44,7 +44,7 @@ class Binning(C.Structure):
                 ("tiles_x", C.c_int32), ("tiles_y", C.c_int32), ("V", C.c_int32)]
 
 
-SPLAT_BYTES = 48
+SPLAT_BYTES = 64
 _lib = None
 
 

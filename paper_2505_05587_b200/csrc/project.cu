@@ -7,7 +7,7 @@
 // fp64 and kept in fp64 in the splat record.
 //
 // One thread per Gaussian; the 14 parameter planes are read once (coalesced SoA) and the V views
-// of the call are produced from registers.  Bound: HBM (56 B read + 48 B + 16 B written per
+// of the call are produced from registers.  Bound: HBM (56 B read + 64 B + 16 B written per
 // visible (view, Gaussian)).
 #include <math.h>
 
@@ -181,12 +181,19 @@ __global__ void __launch_bounds__(256) k_project(const float* __restrict__ param
     const double x0 = m0[1] * m1[2] - m0[2] * m1[1], x1 = m0[2] * m1[0] - m0[0] * m1[2], x2 = m0[0] * m1[1] - m0[1] * m1[0];
     const double ddet = (x0 * x0 + x1 * x1 + x2 * x2) + dil * (a00 + a11) + dil * dil;
     const double idet = 1.0 / ddet;
+    // exp2-ready record: conic * log2(e)/2, log2(o), and the padded half-extents of {m <= tau}
+    const double hl2e = 0.72134752044448170;  // log2(e) / 2
+    const double dtau = (double)tau;
+    const float hx = (float)(sqrt(dtau * (a00 + dil)) * 1.001 + 0.01);
+    const float hy = (float)(sqrt(dtau * (a11 + dil)) * 1.001 + 0.01);
     steepgs_splat* sp = splats + vi;
     double2* s0 = reinterpret_cast<double2*>(sp);
     float4* s1 = reinterpret_cast<float4*>(sp) + 1;
     *s0 = make_double2(mx, my);
-    s1[0] = make_float4((float)((a11 + dil) * idet), (float)(-a01 * idet), (float)((a00 + dil) * idet), o);
-    s1[1] = make_float4(cr, cg, cb, tau);
+    s1[0] = make_float4((float)((a11 + dil) * idet * hl2e), (float)(-2.0 * a01 * idet * hl2e),
+                        (float)((a00 + dil) * idet * hl2e), (float)log2((double)o));
+    s1[1] = make_float4(cr, cg, cb, o);
+    s1[2] = make_float4(hx, hy, tau, 0.0f);
   }
 }
 

@@ -6,15 +6,15 @@
 //   * warps 0..7 (consumers) own one pixel per thread; warp w covers the 8x4 sub-block
 //     x in 8 (w & 1) .. +7, y in 4 (w >> 1) .. +3;
 //   * warp 8 (producer) stages the tile's depth-ordered splats into a ring of kStages shared-memory
-//     buffers of kBatch splats (gathered 48-B records), computes for each splat the 8-bit mask of
-//     sub-blocks its alpha support {m <= tau} (padded extents sqrt(tau Sigma2D)) can reach, and
-//     compacts each batch into one list per consumer warp.
+//     buffers of kBatch splats (gathered 64-B records) with, for each splat, the 8-bit mask of
+//     sub-blocks its alpha support {m <= tau} (padded extents from a1) can reach; each consumer
+//     compacts a staged batch to its own sub-block's splats with 4 ballots.
 // Full/empty mbarriers per buffer replace block-wide barriers, so consumer warps with short lists
 // run ahead by up to kStages batches instead of waiting for the slowest warp, and a consumer
 // iterates only over the splats that can touch its 32 pixels.
 //
 // Per-pair arithmetic: the mean is made tile-relative in fp64 before rounding (offsets
-// d = x - Pi(p) carry ~1e-7 px error); the conic is pre-scaled by log2(e)/2 at staging so that
+// d = x - Pi(p) carry ~1e-7 px error); the conic arrives pre-scaled by log2(e)/2 (a1) so that
 //   e = log2(o) - m',  m' = a + dy (b + Qyy' dy),  a = Qxx' dx^2,  b = 2 Qxy' dx,
 //   skip if e < log2(alpha_min) (<=> sigma < alpha_min),  sigma = 2^e,  alpha = min(amax, sigma)
 // in one function shared by both kernels (explicit round-to-nearest intrinsics), so forward and
@@ -37,15 +37,14 @@ constexpr int kConsumers = 8;                       // one pixel per thread, 8 w
 constexpr int kThreads = 32 * (kConsumers + 1);     // + 1 producer warp
 constexpr int kBatch = 128;                         // splats per staged batch
 constexpr int kStages = 3;                          // ring depth
-constexpr float kHalfLog2e = 0.72134752044448170f;  // log2(e) / 2
 
 struct Buffer {
   float4 geo[kBatch];            // (mu_x - ox, mu_y - oy, Qxx', 2 Qxy')   Q' = Q log2(e)/2
   float4 par[kBatch];            // (Qyy', log2(o), -, -)
   float4 col[kBatch];            // (r, g, b, -)
   float* mptr[kBatch];           // backward: &moments[view][gid][0]
-  uint8_t list[kConsumers][kBatch];
-  int count[kConsumers];
+  uint32_t mask[kBatch];         // sub-blocks reached by the alpha support
+  uint8_t list[kConsumers][kBatch];  // per-consumer compacted lists (written by the consumer)
   int base;                      // list position (relative to the tile start) of slot 0
   int stop;                      // 1: no more batches (forward early termination)
 };
@@ -97,62 +96,60 @@ __device__ __forceinline__ float pair_e(float dx, float dy, const float4 g, cons
   return __fsub_rn(p.y, m);
 }
 
-// Producer: stage splats [first, first + cnt) of the tile list into `B` (lane-strided), then build
-// the 8 per-consumer lists.  Runs on the producer warp only.
+// Producer: stage splats [first, first + cnt) of the tile list into `B` (lane-strided) with the
+// 8-bit sub-block mask of each.  The record is exp2-ready (pre-scaled conic, log2 o, padded extents
+// from a1), so staging is a gather, two fp64 subtractions and eight interval tests.
 __device__ __forceinline__ void produce(Buffer& B, const uint32_t* __restrict__ ids, const steepgs_splat* __restrict__ vs,
                                         uint32_t first, int cnt, double ox, double oy, float* mom_view, int lane) {
-  uint32_t mask[kBatch / 32];
+  uint32_t gid[kBatch / 32];
 #pragma unroll
   for (int q = 0; q < kBatch / 32; ++q) {
     const int k = q * 32 + lane;
-    mask[q] = 0u;
-    if (k < cnt) {
-      const uint32_t gid = ids[first + k];
-      const steepgs_splat* sp = vs + gid;
-      const double2 mean = __ldg(reinterpret_cast<const double2*>(sp));
-      const float4 a = __ldg(reinterpret_cast<const float4*>(sp) + 1);
-      const float4 b = __ldg(reinterpret_cast<const float4*>(sp) + 2);
-      const float gx = (float)(mean.x - ox), gy = (float)(mean.y - oy);
-      B.geo[k] = make_float4(gx, gy, __fmul_rn(a.x, kHalfLog2e), __fmul_rn(2.0f * a.y, kHalfLog2e));
-      B.par[k] = make_float4(__fmul_rn(a.z, kHalfLog2e), __log2f(a.w), 0.0f, 0.0f);
-      B.col[k] = make_float4(b.x, b.y, b.z, 0.0f);
-      if (mom_view) B.mptr[k] = mom_view + (size_t)gid * 12;
-      // padded extents of {m <= tau}; a degenerate det keeps every sub-block
-      const float detq = a.x * a.z - a.y * a.y;
-      uint32_t m = 0xFFu;
-      if (detq > 0.0f) {
-        const float ex = sqrtf(b.w * (a.z / detq)) * 1.001f + 0.01f;
-        const float ey = sqrtf(b.w * (a.x / detq)) * 1.001f + 0.01f;
-        if (ex == ex && ey == ey) {
-          uint32_t xb = 0u, yb = 0u;
-#pragma unroll
-          for (int s = 0; s < 2; ++s)
-            if (gx - ex <= 8.0f * s + 7.5f && gx + ex >= 8.0f * s + 0.5f) xb |= 1u << s;
-#pragma unroll
-          for (int s = 0; s < 4; ++s)
-            if (gy - ey <= 4.0f * s + 3.5f && gy + ey >= 4.0f * s + 0.5f) yb |= 1u << s;
-          m = 0u;
-#pragma unroll
-          for (int s = 0; s < 4; ++s)
-            if (yb & (1u << s)) m |= xb << (2 * s);
-        }
-      }
-      mask[q] = m;
-    }
+    gid[q] = k < cnt ? __ldg(ids + first + k) : 0u;
   }
+#pragma unroll
+  for (int q = 0; q < kBatch / 32; ++q) {
+    const int k = q * 32 + lane;
+    if (k >= cnt) { B.mask[k] = 0u; continue; }
+    const steepgs_splat* sp = vs + gid[q];
+    const double2 mean = __ldg(reinterpret_cast<const double2*>(sp));
+    const float4 a = __ldg(reinterpret_cast<const float4*>(sp) + 1);   // conic', log2 o
+    const float4 b = __ldg(reinterpret_cast<const float4*>(sp) + 2);   // rgb, o
+    const float4 c = __ldg(reinterpret_cast<const float4*>(sp) + 3);   // extents, tau
+    const float gx = (float)(mean.x - ox), gy = (float)(mean.y - oy);
+    B.geo[k] = make_float4(gx, gy, a.x, a.y);
+    B.par[k] = make_float4(a.z, a.w, 0.0f, 0.0f);
+    B.col[k] = make_float4(b.x, b.y, b.z, 0.0f);
+    if (mom_view) B.mptr[k] = mom_view + (size_t)gid[q] * 12;
+    uint32_t xb = 0u, yb = 0u;
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+      if (gx - c.x <= 8.0f * s + 7.5f && gx + c.x >= 8.0f * s + 0.5f) xb |= 1u << s;
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+      if (gy - c.y <= 4.0f * s + 3.5f && gy + c.y >= 4.0f * s + 0.5f) yb |= 1u << s;
+    uint32_t m = 0u;
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+      if (yb & (1u << s)) m |= xb << (2 * s);
+    B.mask[k] = m;
+  }
+}
+
+// Consumer: compact the staged batch to the splats whose mask has bit `w` (ascending order) into
+// the warp's own list; returns the count.
+__device__ __forceinline__ int build_list(const Buffer& B, uint8_t* __restrict__ list, int w, int lane) {
+  int total = 0;
   const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
-  for (int w = 0; w < kConsumers; ++w) {
-    int total = 0;
-#pragma unroll
-    for (int q = 0; q < kBatch / 32; ++q) {
-      const bool hit = (mask[q] >> w) & 1u;
-      const uint32_t bal = __ballot_sync(0xffffffffu, hit);
-      if (hit) B.list[w][total + __popc(bal & lt)] = (uint8_t)(q * 32 + lane);
-      total += __popc(bal);
-    }
-    if (lane == 0) B.count[w] = total;
+  for (int q = 0; q < kBatch / 32; ++q) {
+    const bool hit = (B.mask[q * 32 + lane] >> w) & 1u;
+    const uint32_t bal = __ballot_sync(0xffffffffu, hit);
+    if (hit) list[total + __popc(bal & lt)] = (uint8_t)(q * 32 + lane);
+    total += __popc(bal);
   }
+  __syncwarp();
+  return total;
 }
 
 __global__ void __launch_bounds__(kThreads, 4) k_render_fwd(const steepgs_splat* __restrict__ splats,
@@ -212,8 +209,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_fwd(const steepgs_splat*
     const Buffer& B = sm.buf[s];
     if (B.stop) break;
     if (!warp_done) {
-      const int nl = B.count[warp];
-      const uint8_t* lst = B.list[warp];
+      uint8_t* lst = sm.buf[s].list[warp];
+      const int nl = build_list(B, lst, warp, lane);
       for (int t = 0; t < nl; ++t) {
         const int j = lst[t];
         const float4 g = B.geo[j];
@@ -360,8 +357,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
     const int s = k % kStages;
     mbar_wait(&sm.full[s], (k / kStages) & 1);
     const Buffer& B = sm.buf[s];
-    const uint8_t* lst = B.list[warp];
-    int nl = B.count[warp];
+    uint8_t* lst = sm.buf[s].list[warp];
+    int nl = build_list(B, lst, warp, lane);
     while (nl > 0 && B.base + lst[nl - 1] >= wmax) --nl;   // beyond every pixel's prefix (warp-uniform)
     const int lim = last - B.base;                          // this pixel composited list positions < last
     for (int t_hi = nl; t_hi > 0; t_hi -= kChunk) {

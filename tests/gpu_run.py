@@ -17,11 +17,14 @@ def to_dev(a, dtype=torch.float32):
 
 
 def splat_fields(rz: Rasterizer, n: int):
-    """Decode the [V][n] 48-byte splat records."""
-    raw = rz.splats[: rz.V * n * 48].view(rz.V, n, 48).cpu()
+    """Decode the [V][n] 64-byte splat records (include/steepgs.h)."""
+    raw = rz.splats[: rz.V * n * 64].view(rz.V, n, 64).cpu()
     mean = raw[:, :, 0:16].contiguous().view(torch.float64).view(rz.V, n, 2).numpy()
-    f = raw[:, :, 16:48].contiguous().view(torch.float32).view(rz.V, n, 8).numpy()
-    return dict(mean=mean, conic=f[:, :, 0:3], opacity=f[:, :, 3], rgb=f[:, :, 4:7], tau=f[:, :, 7])
+    f = raw[:, :, 16:64].contiguous().view(torch.float32).view(rz.V, n, 12).numpy().astype(np.float64)
+    hl2e = 0.5 / np.log(2.0)
+    conic = np.stack([f[..., 0] / hl2e, f[..., 1] / (2 * hl2e), f[..., 2] / hl2e], -1)
+    return dict(mean=mean, conic=conic, log2_opacity=f[..., 3], rgb=f[..., 4:7], opacity=f[..., 7],
+                extent=f[..., 8:10], tau=f[..., 10])
 
 
 def run_forward(params: np.ndarray, cams, rp: dict, max_instances=None):

@@ -310,6 +310,18 @@ def main():
         ach = byts[dom] / (stage_ms[dom] * 1e-3) / 1e9
         roofline = dict(bound="hbm", kernel=dom, achieved=round(ach, 1), peak=hbm, unit="GB/s",
                         frac=round(ach / hbm, 4), traffic=None, peak_basis=f"MEASURED_PEAKS.json ({peaks['src']})")
+    # DRAM traffic of the dominant kernel from the committed ncu --set full capture (profiles/)
+    kname = {"render_bwd": "k_render_bwd", "render_fwd": "k_render_fwd", "gauss_bwd_S": "k_gauss_bwd",
+             "project": "k_project"}.get(dom)
+    tfile = os.path.join(ROOT, "profiles", "traffic.json")
+    if kname and os.path.exists(tfile):
+        with open(tfile) as f:
+            tr = json.load(f).get(kname)
+        if tr and int(tr.get("views", -1)) == V and args.config == "C2":
+            roofline["traffic"] = tr["bytes_per_launch"]
+            roofline["traffic_unit"] = "bytes per launch (dram read + write)"
+            roofline["traffic_alg_bytes"] = int(byts[dom])
+            roofline["traffic_source"] = tr["source"]
     path_bytes = sum(byts[s] for s in byts)
     path_ms = sum(stage_ms[s] for s in byts)
     value = ms_step / (V * ws)

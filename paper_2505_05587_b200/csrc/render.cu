@@ -63,10 +63,12 @@ __device__ __forceinline__ void mbar_init(unsigned long long* b, uint32_t count)
 __device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity) {
+// Wait for the phase with the given parity to complete.  A failed probe backs off with
+// __nanosleep(backoff_ns) so a waiting warp does not steal issue slots from working warps.
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity, uint32_t backoff_ns) {
   uint32_t ok = 0;
   const uint32_t a = saddr(b);
-  do {
+  while (true) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
@@ -74,7 +76,9 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity
         : "=r"(ok)
         : "r"(a), "r"(parity)
         : "memory");
-  } while (!ok);
+    if (ok) break;
+    __nanosleep(backoff_ns);
+  }
 }
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -179,7 +183,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_fwd(const steepgs_splat*
     const steepgs_splat* vs = splats + (int64_t)view * n;
     for (int k = 0; k < nb; ++k) {
       const int s = k % kStages;
-      if (k >= kStages) mbar_wait(&sm.empty[s], ((k / kStages) & 1) ^ 1);
+      if (k >= kStages) mbar_wait(&sm.empty[s], ((k / kStages) & 1) ^ 1, 256);
       Buffer& B = sm.buf[s];
       const int stop = *reinterpret_cast<volatile int*>(&sm.done_warps) == kConsumers;
       if (!stop) {
@@ -200,35 +204,37 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_fwd(const steepgs_splat*
   const bool inside = px < W && py < H;
   const float fx = (float)lx + 0.5f, fy = (float)ly + 0.5f;  // pixel centre, tile-relative (Z5)
   const float lmin = __log2f(rk.alpha_min);                   // -inf in smooth mode
+  const float amax = rk.alpha_max, tmin = rk.t_min;
   float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
   int last = 0, ncomp = 0, neval = 0;
   bool done = !inside, warp_done = false;
   for (int k = 0; k < nb; ++k) {
     const int s = k % kStages;
-    mbar_wait(&sm.full[s], (k / kStages) & 1);
+    mbar_wait(&sm.full[s], (k / kStages) & 1, 32);
     const Buffer& B = sm.buf[s];
     if (B.stop) break;
     if (!warp_done) {
       uint8_t* lst = sm.buf[s].list[warp];
       const int nl = build_list(B, lst, warp, lane);
+      const int base1 = B.base + 1;
+      if (!done) neval += nl;
       for (int t = 0; t < nl; ++t) {
         const int j = lst[t];
         const float4 g = B.geo[j];
-        const float4 p = B.par[j];
+        const float2 p = *reinterpret_cast<const float2*>(&B.par[j]);
         if (done) continue;
-        ++neval;
-        const float e = pair_e(__fsub_rn(fx, g.x), __fsub_rn(fy, g.y), g, p);
+        const float e = pair_e(__fsub_rn(fx, g.x), __fsub_rn(fy, g.y), g, make_float4(p.x, p.y, 0.f, 0.f));
         if (e < lmin) continue;                           // sigma < alpha_min: C8 skip
-        const float alpha = fminf(rk.alpha_max, ex2_approx(e));
+        const float alpha = fminf(amax, ex2_approx(e));
         const float Tn = __fmul_rn(T, __fsub_rn(1.0f, alpha));
-        if (Tn < rk.t_min) { done = true; continue; }     // C8 termination
+        if (Tn < tmin) { done = true; continue; }         // C8 termination
         const float4 c = B.col[j];
         const float aT = __fmul_rn(alpha, T);
         C0 = __fmaf_rn(aT, c.x, C0);
         C1 = __fmaf_rn(aT, c.y, C1);
         C2 = __fmaf_rn(aT, c.z, C2);
         T = Tn;
-        last = B.base + j + 1;
+        last = base1 + j;
         ++ncomp;
       }
       if (__all_sync(0xffffffffu, done)) {
@@ -331,7 +337,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
     float* mom_view = moments + (int64_t)view * n * 12;
     for (int k = 0; k < nb; ++k) {
       const int s = k % kStages;
-      if (k >= kStages) mbar_wait(&sm.empty[s], ((k / kStages) & 1) ^ 1);
+      if (k >= kStages) mbar_wait(&sm.empty[s], ((k / kStages) & 1) ^ 1, 256);
       Buffer& B = sm.buf[s];
       const int bb = nb - 1 - k;
       const uint32_t first = rg.x + (uint32_t)bb * kBatch;
@@ -346,6 +352,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
   // ---------------- consumers ----------------
   const float fx = (float)lx + 0.5f, fy = (float)ly + 0.5f;
   const float lmin = __log2f(rk.alpha_min);
+  const float amax = rk.alpha_max;
   float B0 = rk.bg[0], B1 = rk.bg[1], B2 = rk.bg[2];
   float(*sw)[32] = sc.w[warp];
   float(*sat)[32] = sc.at[warp];
@@ -355,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
   const float cx0 = (float)(8 * (warp & 1)) + 0.5f, cy0 = (float)(4 * (warp >> 1)) + 0.5f;
   for (int k = 0; k < nb; ++k) {
     const int s = k % kStages;
-    mbar_wait(&sm.full[s], (k / kStages) & 1);
+    mbar_wait(&sm.full[s], (k / kStages) & 1, 32);
     const Buffer& B = sm.buf[s];
     uint8_t* lst = sm.buf[s].list[warp];
     int nl = build_list(B, lst, warp, lane);
@@ -375,7 +382,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
           if (ee >= lmin) {
             contrib = true;
             const float sigma = ex2_approx(ee);
-            const float alpha = fminf(rk.alpha_max, sigma);
+            const float alpha = fminf(amax, sigma);
             const float4 c = B.col[j];
             const float om = 1.0f - alpha;
             T = T * rcp_approx(om);                         // T_i (before this splat)

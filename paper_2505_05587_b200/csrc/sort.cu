@@ -128,7 +128,7 @@ __device__ __forceinline__ uint32_t block_excl_scan_256(uint32_t v, uint32_t* s_
   return wpre + inc - v;
 }
 
-__global__ void __launch_bounds__(kRadixThreads) k_radix_pass(const uint32_t* __restrict__ keys_in,
+__global__ void __launch_bounds__(kRadixThreads, 3) k_radix_pass(const uint32_t* __restrict__ keys_in,
                                                               const uint32_t* __restrict__ vals_in,
                                                               uint32_t* __restrict__ keys_out,
                                                               uint32_t* __restrict__ vals_out, const int64_t* n_dev,
@@ -189,15 +189,21 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_pass(const uint32_t* __
     st_volatile(&status[dig], kRadFlagPre | tot);
   } else {
     st_volatile(&status[(int64_t)tile * 256 + dig], kRadFlagAgg | tot);
+    // look back 4 predecessors per round trip (independent loads in flight), in order
     int p = tile - 1;
-    while (true) {
-      uint32_t s;
-      do {
-        s = ld_volatile(&status[(int64_t)p * 256 + dig]);
-      } while ((s >> 30) == 0);
-      excl += s & kRadValMask;
-      if ((s >> 30) == 2) break;
-      --p;
+    bool found = false;
+    while (!found) {
+      uint32_t sv[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) sv[q] = p - q >= 0 ? ld_volatile(&status[(int64_t)(p - q) * 256 + dig]) : kRadFlagPre;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (found) break;
+        while ((sv[q] >> 30) == 0) sv[q] = ld_volatile(&status[(int64_t)(p - q) * 256 + dig]);
+        excl += sv[q] & kRadValMask;
+        found = (sv[q] >> 30) == 2;
+      }
+      p -= 4;
     }
     st_volatile(&status[(int64_t)tile * 256 + dig], kRadFlagPre | (excl + tot));
   }

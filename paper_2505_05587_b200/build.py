@@ -1,7 +1,8 @@
 """Build libsteepgs.so in-tree with nvcc for sm_100a only (no JIT, no torch extension machinery).
 
-Each .cu is compiled separately (project.cu with -fmad=false so the fp32 decision chain of
-DESIGN.md §3.2 is evaluated operation by operation), then linked into one shared library.
+Each .cu is compiled separately (-O3 -lineinfo, IEEE division/sqrt, no fast-math; the fp32 decision
+chain of DESIGN.md §3.2 uses explicit round-to-nearest intrinsics, which are never contracted), then
+linked into one shared library.
 """
 from __future__ import annotations
 
@@ -15,7 +16,7 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libsteepgs.so")
 SOURCES = ["abi.cu", "project.cu", "sort.cu", "render.cu", "gauss_bwd.cu", "densify.cu"]
-PER_FILE = {"project.cu": ["-fmad=false"]}
+PER_FILE: dict = {}
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

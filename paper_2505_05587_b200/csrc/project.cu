@@ -1,10 +1,13 @@
 // project.cu — a1: per-(view, Gaussian) projection (Eq. eqn:sigma_2D + footnote fn:Pi,
 // P:L135-139; quaternion + scale re-parameterisation P:L114).
 //
-// Compiled with -fmad=false: the decision chain (visibility, depth key, tile rect) is the exact
-// fp32 operation sequence of DESIGN.md §3.2, each line one IEEE round-to-nearest operation, with
-// exp/log evaluated in double and rounded once.  The render values (pixel mean) are computed in
-// fp64 and kept in fp64 in the splat record.
+// Decision chain (visibility, depth key, tile rect): the exact fp32 operation sequence of DESIGN.md
+// §3.2, written with explicit round-to-nearest intrinsics (__fmul_rn / __fadd_rn / __fsub_rn /
+// __fdiv_rn / __fsqrt_rn are never contracted into FMAs), exp/log evaluated in double and rounded
+// once, so the integer results match the oracle's independent evaluation bit for bit.
+// Render values: the pixel mean (kept in fp64), the conic (formed as M M^T + dil I with
+// M = P R diag(s), det from |m0 x m1|^2, rounded once), log2 o and the padded alpha-support
+// extents, written as one 64-B exp2-ready record per visible (view, Gaussian).
 //
 // One thread per Gaussian; the 14 parameter planes are read once (coalesced SoA) and the V views
 // of the call are produced from registers.  Bound: HBM (56 B read + 64 B + 16 B written per
@@ -15,9 +18,22 @@
 
 namespace sgs {
 
+#define MUL(a, b) __fmul_rn((a), (b))
+#define ADD(a, b) __fadd_rn((a), (b))
+#define SUB(a, b) __fsub_rn((a), (b))
+#define DIV(a, b) __fdiv_rn((a), (b))
+
 __device__ __forceinline__ uint32_t orderable_key(float z) {
   const uint32_t u = __float_as_uint(z);
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// 1/x in fp64 from the fp32 reciprocal and two Newton steps (|rel err| < 1e-15 for normal x).
+__device__ __forceinline__ double drcp(double x) {
+  double r = (double)__frcp_rn((float)x);
+  r = r * fma(-x, r, 2.0);
+  r = r * fma(-x, r, 2.0);
+  return r;
 }
 
 __global__ void __launch_bounds__(256) k_project(const float* __restrict__ params, int64_t ld, int64_t n,
@@ -33,101 +49,98 @@ __global__ void __launch_bounds__(256) k_project(const float* __restrict__ param
   const float logit = params[10 * ld + i];
   const float cr = params[11 * ld + i], cg = params[12 * ld + i], cb = params[13 * ld + i];
 
-  // ---- view-independent part of the chain: R(q), s, Sigma, opacity ----
-  float nq2 = qw * qw; nq2 = nq2 + qx * qx; nq2 = nq2 + qy * qy; nq2 = nq2 + qz * qz;
+  // ---- view-independent part of the decision chain: R(q), s, Sigma, opacity ----
+  const float nq2 = ADD(ADD(ADD(MUL(qw, qw), MUL(qx, qx)), MUL(qy, qy)), MUL(qz, qz));
   const bool qok = nq2 > 0.0f;
-  const float nq = sqrtf(nq2);
-  const float w = qw / nq, x = qx / nq, y = qy / nq, z = qz / nq;
+  const float nq = __fsqrt_rn(nq2);
+  const float w = DIV(qw, nq), x = DIV(qx, nq), y = DIV(qy, nq), z = DIV(qz, nq);
   float r[9];
-  r[0] = 1.0f - 2.0f * (y * y + z * z);
-  r[1] = 2.0f * (x * y - w * z);
-  r[2] = 2.0f * (x * z + w * y);
-  r[3] = 2.0f * (x * y + w * z);
-  r[4] = 1.0f - 2.0f * (x * x + z * z);
-  r[5] = 2.0f * (y * z - w * x);
-  r[6] = 2.0f * (x * z - w * y);
-  r[7] = 2.0f * (y * z + w * x);
-  r[8] = 1.0f - 2.0f * (x * x + y * y);
-  const float s[3] = {(float)exp((double)ls0), (float)exp((double)ls1), (float)exp((double)ls2)};
+  r[0] = SUB(1.0f, MUL(2.0f, ADD(MUL(y, y), MUL(z, z))));
+  r[1] = MUL(2.0f, SUB(MUL(x, y), MUL(w, z)));
+  r[2] = MUL(2.0f, ADD(MUL(x, z), MUL(w, y)));
+  r[3] = MUL(2.0f, ADD(MUL(x, y), MUL(w, z)));
+  r[4] = SUB(1.0f, MUL(2.0f, ADD(MUL(x, x), MUL(z, z))));
+  r[5] = MUL(2.0f, SUB(MUL(y, z), MUL(w, x)));
+  r[6] = MUL(2.0f, SUB(MUL(x, z), MUL(w, y)));
+  r[7] = MUL(2.0f, ADD(MUL(y, z), MUL(w, x)));
+  r[8] = SUB(1.0f, MUL(2.0f, ADD(MUL(x, x), MUL(y, y))));
+  const double ds0 = exp((double)ls0), ds1 = exp((double)ls1), ds2 = exp((double)ls2);
+  const float s[3] = {(float)ds0, (float)ds1, (float)ds2};
   float M[9];
 #pragma unroll
   for (int a = 0; a < 3; ++a)
 #pragma unroll
-    for (int k = 0; k < 3; ++k) M[3 * a + k] = r[3 * a + k] * s[k];
+    for (int k = 0; k < 3; ++k) M[3 * a + k] = MUL(r[3 * a + k], s[k]);
   float Sg[9];
 #pragma unroll
   for (int a = 0; a < 3; ++a)
 #pragma unroll
-    for (int b = 0; b < 3; ++b) {
-      float acc = M[3 * a + 0] * M[3 * b + 0];
-      acc = acc + M[3 * a + 1] * M[3 * b + 1];
-      acc = acc + M[3 * a + 2] * M[3 * b + 2];
-      Sg[3 * a + b] = acc;
-    }
+    for (int b = 0; b < 3; ++b)
+      Sg[3 * a + b] = ADD(ADD(MUL(M[3 * a + 0], M[3 * b + 0]), MUL(M[3 * a + 1], M[3 * b + 1])),
+                          MUL(M[3 * a + 2], M[3 * b + 2]));
+  const double dopac = 1.0 / (1.0 + exp(-(double)logit));
+  const float o = (float)dopac;
+  const bool ook = o > rk.alpha_min;
+  const float tau = (float)(2.0 * log((double)o / (double)rk.alpha_min));
+  const float log2o = (float)log2((double)o);
   // fp64 R(q_hat) diag(s) for the render values (columns scaled by s_k)
   double dr[9];
   {
     const double dq = sqrt((double)qw * qw + (double)qx * qx + (double)qy * qy + (double)qz * qz);
-    const double W_ = qw / dq, X = qx / dq, Y = qy / dq, Z = qz / dq;
-    const double ds0 = exp((double)ls0), ds1 = exp((double)ls1), ds2 = exp((double)ls2);
+    const double iq = 1.0 / dq;
+    const double W_ = qw * iq, X = qx * iq, Y = qy * iq, Z = qz * iq;
     dr[0] = (1.0 - 2.0 * (Y * Y + Z * Z)) * ds0; dr[1] = 2.0 * (X * Y - W_ * Z) * ds1; dr[2] = 2.0 * (X * Z + W_ * Y) * ds2;
     dr[3] = 2.0 * (X * Y + W_ * Z) * ds0; dr[4] = (1.0 - 2.0 * (X * X + Z * Z)) * ds1; dr[5] = 2.0 * (Y * Z - W_ * X) * ds2;
     dr[6] = 2.0 * (X * Z - W_ * Y) * ds0; dr[7] = 2.0 * (Y * Z + W_ * X) * ds1; dr[8] = (1.0 - 2.0 * (X * X + Y * Y)) * ds2;
   }
-  const float o = (float)(1.0 / (1.0 + exp(-(double)logit)));
-  const bool ook = o > rk.alpha_min;
-  const float tau = (float)(2.0 * log((double)o / (double)rk.alpha_min));
 
   for (int v = 0; v < V; ++v) {
     const steepgs_camera& c = cams.cam[v];
     const int64_t vi = (int64_t)v * n + i;
     const float* R = c.R;
-    float tx = R[0] * p0; tx = tx + R[1] * p1; tx = tx + R[2] * p2; tx = tx + c.t[0];
-    float ty = R[3] * p0; ty = ty + R[4] * p1; ty = ty + R[5] * p2; ty = ty + c.t[1];
-    float tz = R[6] * p0; tz = tz + R[7] * p1; tz = tz + R[8] * p2; tz = tz + c.t[2];
+    // ---- decision chain, view part ----
+    const float tx = ADD(ADD(ADD(MUL(R[0], p0), MUL(R[1], p1)), MUL(R[2], p2)), c.t[0]);
+    const float ty = ADD(ADD(ADD(MUL(R[3], p0), MUL(R[4], p1)), MUL(R[5], p2)), c.t[1]);
+    const float tz = ADD(ADD(ADD(MUL(R[6], p0), MUL(R[7], p1)), MUL(R[8], p2)), c.t[2]);
     bool vis = qok && ook;
     float mux, muy, J00, J02, J11, J12;
     if (c.model == 0) {
       vis = vis && (tz > c.znear);
-      const float xz = tx / tz, yz = ty / tz;
-      const float limx = c.guard * ((0.5f * (float)c.width) / c.fx);
-      const float limy = c.guard * ((0.5f * (float)c.height) / c.fy);
+      const float xz = DIV(tx, tz), yz = DIV(ty, tz);
+      const float limx = MUL(c.guard, DIV(MUL(0.5f, (float)c.width), c.fx));
+      const float limy = MUL(c.guard, DIV(MUL(0.5f, (float)c.height), c.fy));
       vis = vis && (fabsf(xz) <= limx) && (fabsf(yz) <= limy);
-      mux = c.fx * xz; mux = mux + c.cx;
-      muy = c.fy * yz; muy = muy + c.cy;
-      J00 = c.fx / tz; J02 = -((c.fx * xz) / tz);
-      J11 = c.fy / tz; J12 = -((c.fy * yz) / tz);
+      mux = ADD(MUL(c.fx, xz), c.cx);
+      muy = ADD(MUL(c.fy, yz), c.cy);
+      J00 = DIV(c.fx, tz); J02 = -DIV(MUL(c.fx, xz), tz);
+      J11 = DIV(c.fy, tz); J12 = -DIV(MUL(c.fy, yz), tz);
     } else {
-      mux = c.fx * tx; mux = mux + c.cx;
-      muy = c.fy * ty; muy = muy + c.cy;
+      mux = ADD(MUL(c.fx, tx), c.cx);
+      muy = ADD(MUL(c.fy, ty), c.cy);
       J00 = c.fx; J02 = 0.0f; J11 = c.fy; J12 = 0.0f;
     }
     float P[6];
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
-      float a0 = J00 * R[0 + b]; a0 = a0 + J02 * R[6 + b]; P[b] = a0;
-      float a1 = J11 * R[3 + b]; a1 = a1 + J12 * R[6 + b]; P[3 + b] = a1;
+      P[b] = ADD(MUL(J00, R[0 + b]), MUL(J02, R[6 + b]));
+      P[3 + b] = ADD(MUL(J11, R[3 + b]), MUL(J12, R[6 + b]));
     }
     float Tm[6];
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll
-      for (int b = 0; b < 3; ++b) {
-        float acc = P[3 * a + 0] * Sg[0 + b];
-        acc = acc + P[3 * a + 1] * Sg[3 + b];
-        acc = acc + P[3 * a + 2] * Sg[6 + b];
-        Tm[3 * a + b] = acc;
-      }
-    float A = Tm[0] * P[0]; A = A + Tm[1] * P[1]; A = A + Tm[2] * P[2]; A = A + rk.dilation;
-    float B = Tm[0] * P[3]; B = B + Tm[1] * P[4]; B = B + Tm[2] * P[5];
-    float C = Tm[3] * P[3]; C = C + Tm[4] * P[4]; C = C + Tm[5] * P[5]; C = C + rk.dilation;
-    const float det = A * C - B * B;
+      for (int b = 0; b < 3; ++b)
+        Tm[3 * a + b] = ADD(ADD(MUL(P[3 * a + 0], Sg[0 + b]), MUL(P[3 * a + 1], Sg[3 + b])), MUL(P[3 * a + 2], Sg[6 + b]));
+    const float A = ADD(ADD(ADD(MUL(Tm[0], P[0]), MUL(Tm[1], P[1])), MUL(Tm[2], P[2])), rk.dilation);
+    const float B = ADD(ADD(MUL(Tm[0], P[3]), MUL(Tm[1], P[4])), MUL(Tm[2], P[5]));
+    const float C = ADD(ADD(ADD(MUL(Tm[3], P[3]), MUL(Tm[4], P[4])), MUL(Tm[5], P[5])), rk.dilation);
+    const float det = SUB(MUL(A, C), MUL(B, B));
     vis = vis && (det > 0.0f);
-    const float ex = sqrtf(tau * A), ey = sqrtf(tau * C);
-    float lox = mux - ex; lox = lox - 0.5f; lox = lox - 1e-3f;
-    float hix = mux + ex; hix = hix - 0.5f; hix = hix + 1e-3f;
-    float loy = muy - ey; loy = loy - 0.5f; loy = loy - 1e-3f;
-    float hiy = muy + ey; hiy = hiy - 0.5f; hiy = hiy + 1e-3f;
+    const float ex = __fsqrt_rn(MUL(tau, A)), ey = __fsqrt_rn(MUL(tau, C));
+    const float lox = SUB(SUB(SUB(mux, ex), 0.5f), 1e-3f);
+    const float hix = ADD(SUB(ADD(mux, ex), 0.5f), 1e-3f);
+    const float loy = SUB(SUB(SUB(muy, ey), 0.5f), 1e-3f);
+    const float hiy = ADD(SUB(ADD(muy, ey), 0.5f), 1e-3f);
     vis = vis && !(lox != lox || hix != hix || loy != loy || hiy != hiy);
     const float jmin = fmaxf(ceilf(lox), 0.0f), jmax = fminf(floorf(hix), (float)(c.width - 1));
     const float kmin = fmaxf(ceilf(loy), 0.0f), kmax = fminf(floorf(hiy), (float)(c.height - 1));
@@ -144,58 +157,61 @@ __global__ void __launch_bounds__(256) k_project(const float* __restrict__ param
     depth_key[vi] = orderable_key(tz);
     tile_rect[vi] = make_uint2((uint32_t)tx0 | ((uint32_t)tx1 << 16), (uint32_t)ty0 | ((uint32_t)ty1 << 16));
 
-    // ---- render values in fp64, rounded once: the pixel mean (kept in fp64) and the conic.  fp32
-    // rounding of P alone perturbs thin, large footprints by ~1e-7 lambda_max / lambda_min, so the
-    // projected covariance is formed as Sigma2D = M M^T + dil I with M = P R diag(s) and
-    // det = |m0 x m1|^2 + dil (|m0|^2 + |m1|^2) + dil^2 (no cancellation).
-    const double dtx = ((double)R[0] * p0 + (double)R[1] * p1) + ((double)R[2] * p2 + (double)c.t[0]);
-    const double dty = ((double)R[3] * p0 + (double)R[4] * p1) + ((double)R[5] * p2 + (double)c.t[1]);
-    const double dtz = ((double)R[6] * p0 + (double)R[7] * p1) + ((double)R[8] * p2 + (double)c.t[2]);
+    // ---- render values in fp64, rounded once.  fp32 rounding of P alone would perturb thin,
+    // large footprints by ~1e-7 lambda_max / lambda_min, so Sigma2D = M M^T + dil I with
+    // M = P R diag(s) and det = |m0 x m1|^2 + dil (|m0|^2 + |m1|^2) + dil^2 (no cancellation).
+    const double dtx = fma((double)R[0], p0, fma((double)R[1], p1, fma((double)R[2], p2, (double)c.t[0])));
+    const double dty = fma((double)R[3], p0, fma((double)R[4], p1, fma((double)R[5], p2, (double)c.t[1])));
+    const double dtz = fma((double)R[6], p0, fma((double)R[7], p1, fma((double)R[8], p2, (double)c.t[2])));
     double mx, my, j00, j02, j11, j12;
     if (c.model == 0) {
-      const double iz = 1.0 / dtz;
-      mx = (double)c.fx * (dtx * iz) + (double)c.cx;
-      my = (double)c.fy * (dty * iz) + (double)c.cy;
-      j00 = (double)c.fx * iz; j02 = -(double)c.fx * dtx * iz * iz;
-      j11 = (double)c.fy * iz; j12 = -(double)c.fy * dty * iz * iz;
+      const double iz = drcp(dtz);
+      const double xz = dtx * iz, yz = dty * iz;
+      mx = fma((double)c.fx, xz, (double)c.cx);
+      my = fma((double)c.fy, yz, (double)c.cy);
+      j00 = (double)c.fx * iz; j02 = -(double)c.fx * xz * iz;
+      j11 = (double)c.fy * iz; j12 = -(double)c.fy * yz * iz;
     } else {
-      mx = (double)c.fx * dtx + (double)c.cx;
-      my = (double)c.fy * dty + (double)c.cy;
+      mx = fma((double)c.fx, dtx, (double)c.cx);
+      my = fma((double)c.fy, dty, (double)c.cy);
       j00 = c.fx; j02 = 0.0; j11 = c.fy; j12 = 0.0;
     }
     double m0[3], m1[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      // column k of R(q) diag(s) in world space, then through P = J W
+      // column k of R(q) diag(s) taken to camera space, then through J
       const double wx = dr[k], wy = dr[3 + k], wz = dr[6 + k];
-      const double cx_ = (double)R[0] * wx + (double)R[1] * wy + (double)R[2] * wz;
-      const double cy_ = (double)R[3] * wx + (double)R[4] * wy + (double)R[5] * wz;
-      const double cz_ = (double)R[6] * wx + (double)R[7] * wy + (double)R[8] * wz;
-      m0[k] = j00 * cx_ + j02 * cz_;
-      m1[k] = j11 * cy_ + j12 * cz_;
+      const double cx_ = fma((double)R[0], wx, fma((double)R[1], wy, (double)R[2] * wz));
+      const double cy_ = fma((double)R[3], wx, fma((double)R[4], wy, (double)R[5] * wz));
+      const double cz_ = fma((double)R[6], wx, fma((double)R[7], wy, (double)R[8] * wz));
+      m0[k] = fma(j00, cx_, j02 * cz_);
+      m1[k] = fma(j11, cy_, j12 * cz_);
     }
     const double dil = (double)rk.dilation;
-    const double a00 = m0[0] * m0[0] + m0[1] * m0[1] + m0[2] * m0[2];
-    const double a11 = m1[0] * m1[0] + m1[1] * m1[1] + m1[2] * m1[2];
-    const double a01 = m0[0] * m1[0] + m0[1] * m1[1] + m0[2] * m1[2];
-    const double x0 = m0[1] * m1[2] - m0[2] * m1[1], x1 = m0[2] * m1[0] - m0[0] * m1[2], x2 = m0[0] * m1[1] - m0[1] * m1[0];
-    const double ddet = (x0 * x0 + x1 * x1 + x2 * x2) + dil * (a00 + a11) + dil * dil;
-    const double idet = 1.0 / ddet;
-    // exp2-ready record: conic * log2(e)/2, log2(o), and the padded half-extents of {m <= tau}
-    const double hl2e = 0.72134752044448170;  // log2(e) / 2
-    const double dtau = (double)tau;
-    const float hx = (float)(sqrt(dtau * (a00 + dil)) * 1.001 + 0.01);
-    const float hy = (float)(sqrt(dtau * (a11 + dil)) * 1.001 + 0.01);
+    const double a00 = fma(m0[0], m0[0], fma(m0[1], m0[1], m0[2] * m0[2]));
+    const double a11 = fma(m1[0], m1[0], fma(m1[1], m1[1], m1[2] * m1[2]));
+    const double a01 = fma(m0[0], m1[0], fma(m0[1], m1[1], m0[2] * m1[2]));
+    const double x0 = fma(m0[1], m1[2], -m0[2] * m1[1]), x1 = fma(m0[2], m1[0], -m0[0] * m1[2]);
+    const double x2 = fma(m0[0], m1[1], -m0[1] * m1[0]);
+    const double ddet = fma(x0, x0, fma(x1, x1, x2 * x2)) + dil * (a00 + a11 + dil);
+    const double hl2e = 0.72134752044448170;  // log2(e) / 2: exp2-ready conic
+    const double sc = drcp(ddet) * hl2e;
+    const float hx = sqrtf(tau * (float)(a00 + dil)) * 1.001f + 0.01f;   // padded half-extents of {m <= tau}
+    const float hy = sqrtf(tau * (float)(a11 + dil)) * 1.001f + 0.01f;
     steepgs_splat* sp = splats + vi;
     double2* s0 = reinterpret_cast<double2*>(sp);
     float4* s1 = reinterpret_cast<float4*>(sp) + 1;
     *s0 = make_double2(mx, my);
-    s1[0] = make_float4((float)((a11 + dil) * idet * hl2e), (float)(-2.0 * a01 * idet * hl2e),
-                        (float)((a00 + dil) * idet * hl2e), (float)log2((double)o));
+    s1[0] = make_float4((float)((a11 + dil) * sc), (float)(-2.0 * a01 * sc), (float)((a00 + dil) * sc), log2o);
     s1[1] = make_float4(cr, cg, cb, o);
     s1[2] = make_float4(hx, hy, tau, 0.0f);
   }
 }
+
+#undef MUL
+#undef ADD
+#undef SUB
+#undef DIV
 
 cudaError_t launch_project(const float* params, int64_t ld, int64_t n, const CamPack& cams, int V,
                            const RasterK& rk, steepgs_splat* splats, uint32_t* depth_key, uint32_t* tile_rect,

@@ -271,10 +271,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_fwd(const steepgs_splat*
 constexpr int kChunk = 16;   // list entries per backward chunk (phase 1 -> phase 2)
 
 struct BwdScratch {
-  float w[kConsumers][kChunk][32];     // dL/dsigma * sigma per (entry, pixel), xor-swizzled columns
-  float at[kConsumers][kChunk][32];    // alpha * T per (entry, pixel)
+  float2 wat[kConsumers][kChunk][33];  // (dL/dsigma * sigma, alpha T) per (entry, pixel); padded rows
   uint32_t cmask[kConsumers][kChunk];  // contributing pixels of each entry (ballot)
-  float4 dl[kConsumers * 32];          // dL/dC of each pixel of the tile
+  float4 pix[kConsumers][32];          // per pixel: tile-relative centre (x, y), dL/dC_r, dL/dC_g
+  float pdl2[kConsumers][32];          // per pixel: dL/dC_b
 };
 
 __device__ __forceinline__ void red_v4(float* p, float a, float b, float c, float d) {
@@ -317,7 +317,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
     const float* dl = dL_dimage + (int64_t)view * 3 * HW;
     dl0 = dl[pix]; dl1 = dl[HW + pix]; dl2 = dl[2 * HW + pix];
   }
-  if (warp < kConsumers) sc.dl[tid] = make_float4(dl0, dl1, dl2, 0.0f);
+  if (warp < kConsumers) {
+    sc.pix[warp][lane] = make_float4((float)lx + 0.5f, (float)ly + 0.5f, dl0, dl1);
+    sc.pdl2[warp][lane] = dl2;
+  }
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&sm.full[s], 32);
@@ -354,12 +357,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
   const float lmin = __log2f(rk.alpha_min);
   const float amax = rk.alpha_max;
   float B0 = rk.bg[0], B1 = rk.bg[1], B2 = rk.bg[2];
-  float(*sw)[32] = sc.w[warp];
-  float(*sat)[32] = sc.at[warp];
+  float2(*swat)[33] = sc.wat[warp];
   uint32_t* scm = sc.cmask[warp];
-  const float4* sdl = sc.dl + warp * 32;
+  const float4* spix = sc.pix[warp];
+  const float* sdl2 = sc.pdl2[warp];
   const int e2 = lane & (kChunk - 1), half = lane >> 4;
-  const float cx0 = (float)(8 * (warp & 1)) + 0.5f, cy0 = (float)(4 * (warp >> 1)) + 0.5f;
+  const uint32_t half_mask = half ? 0xFFFF0000u : 0x0000FFFFu;
   for (int k = 0; k < nb; ++k) {
     const int s = k % kStages;
     mbar_wait(&sm.full[s], (k / kStages) & 1, 32);
@@ -390,8 +393,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
             B0 = alpha * c.x + om * B0;
             B1 = alpha * c.y + om * B1;
             B2 = alpha * c.z + om * B2;
-            sw[e][lane ^ e] = T * gsum * sigma;             // dL/dalpha * sigma (straight-through, Z3)
-            sat[e][lane ^ e] = alpha * T;
+            swat[e][lane] = make_float2(T * gsum * sigma, alpha * T);  // dL/dalpha * sigma (Z3), alpha T
           }
         }
         const uint32_t bal = __ballot_sync(0xffffffffu, contrib);
@@ -409,17 +411,17 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
       if (valid) {
         j2 = lst[t_lo + e2];
         full_bits = scm[e2];
-        uint32_t bits = half ? (full_bits >> 16) : (full_bits & 0xFFFFu);
-        const float4 g = B.geo[j2];
-        const float gx = g.x, gy = g.y;
+        uint32_t bits = full_bits & half_mask;
+        const float2 gm = *reinterpret_cast<const float2*>(&B.geo[j2]);
+        const float2* row = swat[e2];
         while (bits) {
-          const int pp = (half << 4) + __ffs(bits) - 1;
-          bits &= bits - 1u;
-          const float w = sw[e2][pp ^ e2];
-          const float at = sat[e2][pp ^ e2];
-          const float dx = (cx0 + (float)(pp & 7)) - gx;
-          const float dy = (cy0 + (float)(pp >> 3)) - gy;
-          const float4 d = sdl[pp];
+          const int pp = 31 - __clz(bits);
+          bits ^= 1u << pp;
+          const float2 wa = row[pp];
+          const float4 d = spix[pp];
+          const float dl2p = sdl2[pp];
+          const float w = wa.x, at = wa.y;
+          const float dx = d.x - gm.x, dy = d.y - gm.y;
           const float wdx = w * dx, wdy = w * dy;
           acc[0] += w;
           acc[1] += wdx;
@@ -427,9 +429,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
           acc[3] = fmaf(wdx, dx, acc[3]);
           acc[4] = fmaf(wdx, dy, acc[4]);
           acc[5] = fmaf(wdy, dy, acc[5]);
-          acc[6] = fmaf(at, d.x, acc[6]);
-          acc[7] = fmaf(at, d.y, acc[7]);
-          acc[8] = fmaf(at, d.z, acc[8]);
+          acc[6] = fmaf(at, d.z, acc[6]);
+          acc[7] = fmaf(at, d.w, acc[7]);
+          acc[8] = fmaf(at, dl2p, acc[8]);
         }
       }
 #pragma unroll

@@ -194,17 +194,22 @@ def test_render_bwd_split_parity_c1(orc, model, rp):
     assert float(rz.moments.abs().max()) == 0.0
 
 
-def test_render_windows_full_size_c2(orc):
-    """Full-size C2 (1.0M Gaussians, 980x545) in the bench's launch configuration; the oracle
-    evaluates 3 windows (images) and the gradients/S of dL restricted to those windows."""
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
+def test_render_windows_full_size(orc, name):
+    """Full-size BASELINE configs (C2 1.0M 980x545 ... C5 6M 1920x1080): the decision chain of every
+    Gaussian bit-exact; the oracle evaluates 3 windows (images) and the gradients/S of dL restricted
+    to those windows (including the ragged bottom-right corner tile)."""
     from gpu_run import run_backward, run_forward
-    cfg = synth.CONFIGS["C2"]
+    cfg = synth.CONFIGS[name]
     p = synth.scene_for(cfg)
     cams = synth.cameras_for(cfg, views=1)
     cam = cams[0]
     rz, pt = run_forward(p, cams, DEFAULT)
+    if name != "C2":
+        _cmp_decisions(orc, p, cams, DEFAULT, rz, p.shape[1])
     img = rz.image.cpu().numpy()[0]
-    windows = [(0, 0, 40, 32), (470, 250, 48, 40), (931, 500, 49, 45)]  # includes the ragged corner
+    W, H = cfg.width, cfg.height
+    windows = [(0, 0, 40, 32), (W // 2 - 24, H // 2 - 20, 48, 40), (W - 49, H - 45, 49, 45)]
     dl_full = synth.dl_dimage(1, cfg.width, cfg.height, 5)[0]
     dl = np.zeros_like(dl_full)
     dec = orc.decide(p, cam, DEFAULT)

@@ -10,6 +10,7 @@
 //                     canonical sign, C13), eps = eta sqrt(v^T Sigma v) (Z13), offspring
 //                     A = (p + eps v, o/2) in place, B = (p - eps v, o/2) appended at n + rank (Z24),
 //                     log-scale / quaternion / colour copied (Z14).
+// With capacity >= 2n (a densify can at most double n) both steps run as one fused kernel.
 // Bound: HBM (~53 B per Gaussian + 192 B per split).
 #include <math.h>
 
@@ -153,83 +154,10 @@ __device__ __forceinline__ float decide_lambda(const float* S6, float eps_split)
   return lam;
 }
 
-__global__ void __launch_bounds__(kThreads) k_densify_decide(const float* __restrict__ grad_S, int64_t ldg, int64_t n,
-                                                             float inv_denom, float eps_split,
-                                                             uint8_t* __restrict__ mask, int32_t* __restrict__ dest,
-                                                             float* __restrict__ lambda, uint64_t* status,
-                                                             int* tile_counter, int64_t* n_split) {
-  __shared__ int s_tile;
-  __shared__ uint32_t s_cnt[kItems][kThreads / 32];
-  __shared__ uint64_t s_excl;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) s_tile = atomicAdd(tile_counter, 1);
-  __syncthreads();
-  const int tile = s_tile;
-  const int64_t base = (int64_t)tile * kTileItems;
-  bool split[kItems];
-  uint32_t pos[kItems];
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const int64_t i = base + (int64_t)j * kThreads + tid;
-    split[j] = false;
-    if (i < n) {
-      float S6[6];
-      load_sbar(grad_S, ldg, i, inv_denom, S6);
-      const float lam = decide_lambda(S6, eps_split);
-      split[j] = lam < eps_split;                     // Thm 2 / Alg. 1 P:L545 (strict, Z11)
-      if (lambda) lambda[i] = lam;
-    }
-    const uint32_t b = __ballot_sync(0xffffffffu, split[j]);
-    pos[j] = __popc(b & lanemask_lt());
-    if (lane == 0) s_cnt[j][warp] = __popc(b);
-  }
-  __syncthreads();
-  if (warp == 0) {
-    const int nw = kThreads / 32;
-    uint32_t a = s_cnt[(2 * lane) / nw][(2 * lane) % nw], bb = s_cnt[(2 * lane + 1) / nw][(2 * lane + 1) % nw];
-    uint32_t sum = a + bb, inc = sum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += t;
-    }
-    const uint32_t ex = inc - sum;
-    s_cnt[(2 * lane) / nw][(2 * lane) % nw] = ex;
-    s_cnt[(2 * lane + 1) / nw][(2 * lane + 1) % nw] = ex + a;
-    const uint32_t agg = __shfl_sync(0xffffffffu, inc, 31);
-    const uint64_t excl = lookback_warp(status, tile, agg);
-    if (lane == 0) {
-      s_excl = excl;
-      if (base + kTileItems >= n) *n_split = (int64_t)(excl + agg);
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const int64_t i = base + (int64_t)j * kThreads + tid;
-    if (i >= n) continue;
-    mask[i] = split[j] ? 1 : 0;
-    dest[i] = split[j] ? (int32_t)(n + (int64_t)(s_excl + s_cnt[j][warp] + pos[j])) : -1;  // Z24
-  }
-}
-
-__global__ void __launch_bounds__(kThreads) k_densify_apply(float* __restrict__ params, int64_t ld, int64_t n,
-                                                            int64_t capacity, float* __restrict__ grad_S, int64_t ldg,
-                                                            float inv_denom, float eta, float eps_abs,
-                                                            const uint8_t* __restrict__ mask,
-                                                            const int32_t* __restrict__ dest,
-                                                            const int64_t* __restrict__ n_split,
-                                                            int32_t* __restrict__ status) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t ns = *n_split;
-  const bool ok = n + ns <= capacity;
-  if (i == 0) *status = ok ? 0 : (int32_t)STEEPGS_ERR_CAPACITY;
-  if (!ok || i >= n) return;
-  float S6[6];
-  load_sbar(grad_S, ldg, i, inv_denom, S6);
-#pragma unroll
-  for (int k = 14; k < 20; ++k) grad_S[k * ldg + i] = 0.f;
-  if (!mask[i]) return;
+// Offspring of split parent i (Thm 2 / Alg. 1): A in slot i at p + eps v, B in slot b at
+// p - eps v, both with opacity logit(o/2) (Z15), other planes copied (Z14); B's accumulators zeroed.
+__device__ __forceinline__ void spawn(float* __restrict__ params, int64_t ld, float* __restrict__ grad_S,
+                                      int64_t ldg, int64_t i, int64_t b, const float* S6, float eta, float eps_abs) {
   float v[3], lam_unused;
   eig_min_robust(S6, true, lam_unused, v);
   // parent: p, Sigma = R diag(s^2) R^T, o
@@ -254,7 +182,6 @@ __global__ void __launch_bounds__(kThreads) k_densify_apply(float* __restrict__ 
   const double o = 1.0 / (1.0 + exp(-(double)params[10 * ld + i]));
   const double h = 0.5 * o;                                   // Z15: w = 1/2 absorbed in opacity
   const float lg = (float)(log(h) - log1p(-h));
-  const int64_t b = dest[i];
 #pragma unroll
   for (int k = 3; k < 14; ++k) params[k * ld + b] = params[k * ld + i];
   params[0 * ld + b] = p0 - eps * v[0];
@@ -269,12 +196,110 @@ __global__ void __launch_bounds__(kThreads) k_densify_apply(float* __restrict__ 
   for (int k = 0; k < 20; ++k) grad_S[k * ldg + b] = 0.f;
 }
 
+// kFused (capacity >= 2n, so n + n_split <= capacity holds for any mask): the same kernel also
+// writes the offspring and clears S, one pass over the data and no second launch.
+template <bool kFused, int kIt>
+__global__ void __launch_bounds__(kThreads) k_densify_decide(float* __restrict__ params, int64_t ld,
+                                                             float* __restrict__ grad_S, int64_t ldg, int64_t n,
+                                                             float inv_denom, float eps_split, float eta, float eps_abs,
+                                                             uint8_t* __restrict__ mask, int32_t* __restrict__ dest,
+                                                             float* __restrict__ lambda, uint64_t* status,
+                                                             int* tile_counter, int64_t* n_split,
+                                                             int32_t* __restrict__ dstatus) {
+  __shared__ int s_tile;
+  __shared__ uint32_t s_cnt[kIt][kThreads / 32];
+  __shared__ uint64_t s_excl;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) s_tile = atomicAdd(tile_counter, 1);
+  __syncthreads();
+  const int tile = s_tile;
+  const int64_t base = (int64_t)tile * (kThreads * kIt);
+  bool split[kIt];
+  uint32_t pos[kIt];
+#pragma unroll
+  for (int j = 0; j < kIt; ++j) {
+    const int64_t i = base + (int64_t)j * kThreads + tid;
+    split[j] = false;
+    if (i < n) {
+      float S6[6];
+      load_sbar(grad_S, ldg, i, inv_denom, S6);
+      const float lam = decide_lambda(S6, eps_split);
+      split[j] = lam < eps_split;                     // Thm 2 / Alg. 1 P:L545 (strict, Z11)
+      if (lambda) lambda[i] = lam;
+    }
+    const uint32_t b = __ballot_sync(0xffffffffu, split[j]);
+    pos[j] = __popc(b & lanemask_lt());
+    if (lane == 0) s_cnt[j][warp] = __popc(b);
+  }
+  __syncthreads();
+  if (warp == 0) {
+    constexpr int nw = kThreads / 32, nv = kIt * nw;   // <= 64 counts, two per lane, (j, warp) order
+    uint32_t* cnt = &s_cnt[0][0];
+    const uint32_t a = 2 * lane < nv ? cnt[2 * lane] : 0u, bb = 2 * lane + 1 < nv ? cnt[2 * lane + 1] : 0u;
+    uint32_t sum = a + bb, inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    const uint32_t ex = inc - sum;
+    if (2 * lane < nv) cnt[2 * lane] = ex;
+    if (2 * lane + 1 < nv) cnt[2 * lane + 1] = ex + a;
+    const uint32_t agg = __shfl_sync(0xffffffffu, inc, 31);
+    const uint64_t excl = lookback_warp(status, tile, agg);
+    if (lane == 0) {
+      s_excl = excl;
+      if (base + kThreads * kIt >= n) *n_split = (int64_t)(excl + agg);
+    }
+  }
+  __syncthreads();
+  if (kFused && tile == 0 && tid == 0) *dstatus = 0;
+#pragma unroll
+  for (int j = 0; j < kIt; ++j) {
+    const int64_t i = base + (int64_t)j * kThreads + tid;
+    if (i >= n) continue;
+    const int64_t b = n + (int64_t)(s_excl + s_cnt[j][warp] + pos[j]);
+    mask[i] = split[j] ? 1 : 0;
+    dest[i] = split[j] ? (int32_t)b : -1;  // Z24
+    if (kFused) {
+      float S6[6];
+      if (split[j]) load_sbar(grad_S, ldg, i, inv_denom, S6);
+#pragma unroll
+      for (int k = 14; k < 20; ++k) grad_S[k * ldg + i] = 0.f;   // Z23
+      if (split[j]) spawn(params, ld, grad_S, ldg, i, b, S6, eta, eps_abs);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_densify_apply(float* __restrict__ params, int64_t ld, int64_t n,
+                                                            int64_t capacity, float* __restrict__ grad_S, int64_t ldg,
+                                                            float inv_denom, float eta, float eps_abs,
+                                                            const uint8_t* __restrict__ mask,
+                                                            const int32_t* __restrict__ dest,
+                                                            const int64_t* __restrict__ n_split,
+                                                            int32_t* __restrict__ status) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t ns = *n_split;
+  const bool ok = n + ns <= capacity;
+  if (i == 0) *status = ok ? 0 : (int32_t)STEEPGS_ERR_CAPACITY;
+  if (!ok || i >= n) return;
+  float S6[6];
+  load_sbar(grad_S, ldg, i, inv_denom, S6);
+#pragma unroll
+  for (int k = 14; k < 20; ++k) grad_S[k * ldg + i] = 0.f;
+  if (!mask[i]) return;
+  spawn(params, ld, grad_S, ldg, i, dest[i], S6, eta, eps_abs);
+}
+
+
 inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 }  // namespace
 
+constexpr int kItemsFused = 1;   // one Gaussian per thread when the offspring are written too
+
 size_t densify_ws_bytes(int64_t n) {
-  const int64_t tiles = (n + kTileItems - 1) / kTileItems;
+  const int64_t tiles = (n + kThreads * kItemsFused - 1) / (kThreads * kItemsFused);
   return align_up(8 * (size_t)(tiles > 0 ? tiles : 1)) + 256;
 }
 
@@ -282,7 +307,9 @@ cudaError_t launch_densify(float* params, int64_t ld, int64_t n, int64_t capacit
                            const steepgs_densify_params& dp, uint8_t* mask, int32_t* dest, float* lambda,
                            int64_t* n_split, int32_t* status, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (ws_bytes < densify_ws_bytes(n)) return cudaErrorInvalidValue;
-  const int64_t tiles = (n + kTileItems - 1) / kTileItems;
+  const bool fused = capacity >= 2 * n;
+  const int64_t tiles = fused ? (n + kThreads * kItemsFused - 1) / (kThreads * kItemsFused)
+                              : (n + kTileItems - 1) / kTileItems;
   char* w = static_cast<char*>(ws);
   uint64_t* sstatus = reinterpret_cast<uint64_t*>(w);
   int* counter = reinterpret_cast<int*>(w + align_up(8 * (size_t)(tiles > 0 ? tiles : 1)));
@@ -291,9 +318,17 @@ cudaError_t launch_densify(float* params, int64_t ld, int64_t n, int64_t capacit
   e = cudaMemsetAsync(n_split, 0, sizeof(int64_t), st);
   if (e != cudaSuccess) return e;
   const float inv_denom = 1.0f / dp.denom;
+  if (n > 0 && fused) {
+    k_densify_decide<true, kItemsFused><<<(unsigned)tiles, kThreads, 0, st>>>(params, ld, grad_S, ldg, n, inv_denom, dp.eps_split,
+                                                                 dp.eta, dp.eps_abs, mask, dest, lambda, sstatus,
+                                                                 counter, n_split, status);
+    note_launch();
+    return check_launch("k_densify_decide<fused>");
+  }
   if (n > 0) {
-    k_densify_decide<<<(unsigned)tiles, kThreads, 0, st>>>(grad_S, ldg, n, inv_denom, dp.eps_split, mask, dest, lambda,
-                                                           sstatus, counter, n_split);
+    k_densify_decide<false, kItems><<<(unsigned)tiles, kThreads, 0, st>>>(params, ld, grad_S, ldg, n, inv_denom, dp.eps_split,
+                                                                  dp.eta, dp.eps_abs, mask, dest, lambda, sstatus,
+                                                                  counter, n_split, status);
     note_launch();
     if ((e = check_launch("k_densify_decide")) != cudaSuccess) return e;
   }

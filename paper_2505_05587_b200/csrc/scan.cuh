@@ -23,14 +23,16 @@ __device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
 __device__ __forceinline__ void st_volatile(uint64_t* p, uint64_t v) { *reinterpret_cast<volatile uint64_t*>(p) = v; }
 __device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v) { *reinterpret_cast<volatile uint32_t*>(p) = v; }
 
-// Warp-parallel decoupled look-back (one warp).  Returns the exclusive prefix of `tile`.
-__device__ __forceinline__ uint64_t lookback_warp(uint64_t* status, int tile, uint64_t aggregate) {
+// Publish a tile's aggregate (tile 0 publishes its inclusive prefix directly).  One lane.
+__device__ __forceinline__ void publish_aggregate(uint64_t* status, int tile, uint64_t aggregate) {
+  st_volatile(&status[tile], (tile == 0 ? kScanFlagPre : kScanFlagAgg) | aggregate);
+}
+
+// Warp-parallel decoupled look-back (one warp) for a tile whose aggregate is already published.
+// Returns the exclusive prefix of `tile` and publishes its inclusive prefix.
+__device__ __forceinline__ uint64_t lookback_published(uint64_t* status, int tile, uint64_t aggregate) {
   const int lane = threadIdx.x & 31;
-  if (tile == 0) {
-    if (lane == 0) st_volatile(&status[0], kScanFlagPre | aggregate);
-    return 0;
-  }
-  if (lane == 0) st_volatile(&status[tile], kScanFlagAgg | aggregate);
+  if (tile == 0) return 0;
   uint64_t excl = 0;
   int pred = tile - 1;
   while (true) {
@@ -50,6 +52,12 @@ __device__ __forceinline__ uint64_t lookback_warp(uint64_t* status, int tile, ui
   }
   if (lane == 0) st_volatile(&status[tile], kScanFlagPre | (excl + aggregate));
   return excl;
+}
+
+// Publish + look back in one go (one warp).  Returns the exclusive prefix of `tile`.
+__device__ __forceinline__ uint64_t lookback_warp(uint64_t* status, int tile, uint64_t aggregate) {
+  if ((threadIdx.x & 31) == 0) publish_aggregate(status, tile, aggregate);
+  return lookback_published(status, tile, aggregate);
 }
 
 

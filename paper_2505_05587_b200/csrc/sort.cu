@@ -64,7 +64,9 @@ __global__ void __launch_bounds__(kScanThreads) k_compact(const uint32_t* __rest
     if (lane == 0) s_cnt[j][warp] = __popc(b);
   }
   __syncthreads();
-  // exclusive scan of the 64 warp counts in (j, warp) order by warp 0
+  // exclusive scan of the 64 warp counts in (j, warp) order by warp 0; the aggregate is published
+  // before the visible items' records are gathered, so the look-back overlaps those loads
+  __shared__ uint32_t s_agg;
   if (warp == 0) {
     const int nw = kScanThreads / 32;
     uint32_t a = s_cnt[(2 * lane) / nw][(2 * lane) % nw], b = s_cnt[(2 * lane + 1) / nw][(2 * lane + 1) % nw];
@@ -78,7 +80,19 @@ __global__ void __launch_bounds__(kScanThreads) k_compact(const uint32_t* __rest
     s_cnt[(2 * lane) / nw][(2 * lane) % nw] = ex;
     s_cnt[(2 * lane + 1) / nw][(2 * lane + 1) % nw] = ex + a;
     const uint32_t agg = __shfl_sync(0xffffffffu, inc, 31);
-    const uint64_t excl = lookback_warp(status, tile, agg);
+    if (lane == 0) { publish_aggregate(status, tile, agg); s_agg = agg; }
+  }
+  uint32_t key[kScanItems];
+  uint2 rect[kScanItems];
+  int32_t tt[kScanItems];
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    const int64_t idx = base + (int64_t)j * kScanThreads + tid;
+    if (flag[j]) { key[j] = depth_key[idx]; rect[j] = tile_rect[idx]; tt[j] = tiles_touched[idx]; }
+  }
+  if (warp == 0) {
+    const uint32_t agg = __shfl_sync(0xffffffffu, s_agg, 0);
+    const uint64_t excl = lookback_published(status, tile, agg);
     if (lane == 0) {
       s_excl = excl;
       if ((base + kScanTile >= total)) *n_visible = (int64_t)(excl + agg);  // last tile
@@ -91,14 +105,12 @@ __global__ void __launch_bounds__(kScanThreads) k_compact(const uint32_t* __rest
     if (!flag[j]) continue;
     const int64_t idx = base + (int64_t)j * kScanThreads + tid;
     const uint64_t pos = bex + s_cnt[j][warp] + pos_in_warp[j];
-    const uint32_t key = depth_key[idx];
-    keys_out[pos] = key;
+    keys_out[pos] = key[j];
     vals_out[pos] = (uint32_t)pos;
-    const uint2 r = tile_rect[idx];
     const uint32_t v = (uint32_t)(idx / n), i = (uint32_t)(idx - (int64_t)v * n);
-    recs[pos] = make_uint4(r.x, r.y, i, (v << 24) | (uint32_t)tiles_touched[idx]);
+    recs[pos] = make_uint4(rect[j].x, rect[j].y, i, (v << 24) | (uint32_t)tt[j]);
 #pragma unroll
-    for (int p = 0; p < 4; ++p) atomicAdd(&s_hist[p][(key >> (8 * p)) & 255u], 1u);
+    for (int p = 0; p < 4; ++p) atomicAdd(&s_hist[p][(key[j] >> (8 * p)) & 255u], 1u);
   }
   __syncthreads();
   for (int k = tid; k < 4 * 256; k += kScanThreads) {
@@ -240,7 +252,7 @@ __global__ void __launch_bounds__(kScanThreads) k_duplicate(const uint32_t* __re
                                                             uint32_t* __restrict__ inst_keys,
                                                             uint32_t* __restrict__ inst_ids, uint64_t* status,
                                                             int* tile_counter, uint32_t* hist2, int64_t* n_inst,
-                                                            int32_t* overflow) {
+                                                            int32_t* overflow, int tile_passes) {
   __shared__ int s_tile;
   __shared__ uint32_t s_cnt[kScanItems][kScanThreads / 32];
   __shared__ uint32_t s_hist[3][256];
@@ -310,8 +322,8 @@ __global__ void __launch_bounds__(kScanThreads) k_duplicate(const uint32_t* __re
         inst_keys[pos] = key;
         inst_ids[pos] = rec[j].z;
         atomicAdd(&s_hist[0][key & 255u], 1u);
-        atomicAdd(&s_hist[1][(key >> 8) & 255u], 1u);
-        atomicAdd(&s_hist[2][(key >> 16) & 255u], 1u);
+        if (tile_passes > 1) atomicAdd(&s_hist[1][(key >> 8) & 255u], 1u);
+        if (tile_passes > 2) atomicAdd(&s_hist[2][(key >> 16) & 255u], 1u);
       }
   }
   __syncthreads();
@@ -446,13 +458,13 @@ cudaError_t launch_bin_sort(const uint32_t* depth_key, const uint32_t* tile_rect
     t = vi; vi = vo; vo = t;
   }
   // sorted slots now in vi (== valsA)
+  const int tile_passes = tiles_total <= 256 ? 1 : (tiles_total <= 65536 ? 2 : 3);
   k_duplicate<<<L.compact_tiles, kScanThreads, 0, st>>>(vi, recs, n_visible, tiles_x, tiles_per_view,
                                                         max_instances, keysC, valsC, st_dup, counters + 5,
-                                                        hist + 4 * 256, n_inst, overflow);
+                                                        hist + 4 * 256, n_inst, overflow, tile_passes);
   note_launch();
   if ((e = check_launch("k_duplicate")) != cudaSuccess) return e;
   // tile sort: one 8-bit pass per byte of the largest tile key (C -> D -> C ...)
-  const int tile_passes = tiles_total <= 256 ? 1 : (tiles_total <= 65536 ? 2 : 3);
   uint32_t *tki = keysC, *tvi = valsC, *tko = keysD, *tvo = valsD;
   for (int p = 0; p < tile_passes; ++p) {
     k_radix_pass<<<L.inst_tiles > 0 ? L.inst_tiles : 1, kRadixThreads, 0, st>>>(

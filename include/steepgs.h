@@ -38,7 +38,7 @@ typedef enum {
   STEEPGS_OK = 0,
   STEEPGS_ERR_INVALID_ARGUMENT = 1,    /* null/misaligned pointer, n < 0, V outside [1, 64],
                                           width/height <= 0 or differing across views, ld < n,
-                                          tile != 16, denom <= 0 */
+                                          tile != 16, denom <= 0, gate not 0/1 */
   STEEPGS_ERR_WORKSPACE_TOO_SMALL = 2, /* ws_bytes < steepgs_bin_sort_workspace_size(...) */
   STEEPGS_ERR_CAPACITY = 3,            /* densify: n + n_split > capacity (host-count variant) */
   STEEPGS_ERR_UNSUPPORTED_DEVICE = 5,  /* no CUDA device of compute capability 10.x */
@@ -67,11 +67,16 @@ typedef struct {
 
 /* Densify parameters (Thm 2, Alg. 1).  eps_split default -1e-6; eta >= 0:
  * eps = eta sqrt(v^T Sigma v) (default 0.5, Z13), eta < 0: eps = eps_abs; denom = number of
- * accumulated views/steps (S_bar = S / denom), must be > 0.  gate must be 0 (the
- * compactest gate of P:L578 is reserved, NEXT f2); eps_grad is ignored. */
+ * accumulated views/steps (S_bar = S / denom), must be > 0.
+ * gate = 1: the "compactest" variant (App. A.2): a Gaussian is split only if also
+ *   ||G_p / denom||_2 <= eps_grad, G_p = the accumulated position-gradient planes 0-2 (Z12, Z21).
+ * budget >= 0: "densification with increment budget" (App. A.2): of the Gaussians
+ *   that pass the rule, split at most `budget`, those with the least lambda_min (ties: lower
+ *   index first); budget < 0: unlimited. */
 typedef struct {
   float eps_split, eta, eps_abs, eps_grad, denom;
   int32_t gate;
+  int64_t budget;
 } steepgs_densify_params;
 
 /* Projected splat (a1 output), 64 B.  mean Pi(p) in pixels kept in fp64 so that per-pair offsets

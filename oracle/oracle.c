@@ -691,22 +691,47 @@ int orc_eig_sym3(const double* A6, double* lam, double* V) {
  * ------------------------------------------------------------------------------------------ */
 int64_t orc_densify(double* params, int64_t ld, int64_t n, int64_t capacity, double* acc,
                     int64_t ldg, double denom, double eps_split, double eta, double eps_abs,
+                    int32_t gate, double eps_grad, int64_t budget,
                     uint8_t* mask, int32_t* dest, double* lambda) {
   int64_t nsplit = 0;
   double* vmin = (double*)malloc(sizeof(double) * 3 * (size_t)(n > 0 ? n : 1));
-  if (!vmin) return -2;
+  double* lam0 = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+  if (!vmin || !lam0) { free(vmin); free(lam0); return -2; }
+  int64_t ncand = 0;
   for (int64_t i = 0; i < n; ++i) {
     double Sbar[6];
     for (int k = 0; k < 6; ++k) Sbar[k] = acc[(14 + k) * ldg + i] / denom;
     double lam[3], V[9];
     orc_eig_sym3(Sbar, lam, V);
     if (lambda) lambda[i] = lam[0];
+    lam0[i] = lam[0];
     for (int k = 0; k < 3; ++k) vmin[3 * i + k] = V[3 * k + 0];
-    const int split = lam[0] < eps_split;                                      /* P:L545, Z11 */
+    int split = lam[0] < eps_split;                                            /* P:L545, Z11 */
+    if (split && gate) {
+      double g2 = 0;
+      for (int k = 0; k < 3; ++k) { const double g = acc[k * ldg + i] / denom; g2 += g * g; }
+      split = sqrt(g2) <= eps_grad;
+    }
     mask[i] = (uint8_t)split;
-    dest[i] = split ? (int32_t)(n + nsplit) : -1;                              /* Z24 */
-    nsplit += split;
+    ncand += split;
   }
+  if (budget >= 0 && ncand > budget) {
+    /* keep the `budget` least lambda_min (ties: lower index) — selection by repeated minimum */
+    uint8_t* keep = (uint8_t*)calloc((size_t)(n > 0 ? n : 1), 1);
+    for (int64_t r = 0; r < budget; ++r) {
+      int64_t best = -1;
+      for (int64_t i = 0; i < n; ++i)
+        if (mask[i] && !keep[i] && (best < 0 || lam0[i] < lam0[best])) best = i;
+      keep[best] = 1;
+    }
+    for (int64_t i = 0; i < n; ++i) mask[i] = keep[i];
+    free(keep);
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    dest[i] = mask[i] ? (int32_t)(n + nsplit) : -1;                            /* Z24 */
+    nsplit += mask[i];
+  }
+  free(lam0);
   if (n + nsplit > capacity) { free(vmin); return -1; }                        /* C16 */
   for (int64_t i = 0; i < n; ++i) {
     if (!mask[i]) continue;

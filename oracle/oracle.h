@@ -88,13 +88,17 @@ int64_t orc_render_view(const double* params, int64_t ld, int64_t n, const orc_c
  * (p < 1e-12 (1+|q|)): lam = q, V = I.  Returns the number of sweeps. */
 int orc_eig_sym3(const double* A, double* lam, double* V);
 
-/* SDC densify (Thm 2, Alg. 1) on fp64 planes, in place.  S planes are read from
+/* SDC densify (Thm 2, Alg. 1) on fp64 planes, in place.  Variants of App. A.2:
+ * gate = 1 also requires ||acc[0..2] / denom||_2 <= eps_grad (compactest); budget >= 0
+ * keeps at most `budget` splits, those with the least lambda_min, ties by index.
+ * S planes are read from
  * acc[14..19][ld].  Offspring A in slot i (p + eps v), B in slot n + rank (p - eps v), both with
  * opacity o/2 (stored as logit), eps = eta sqrt(v^T Sigma v) (eta >= 0) or eps_abs.  S planes are
  * zeroed for [0, n').  mask[n], dest[n] (-1 if kept), lambda[n] (may be NULL).
  * Returns n_split, or -1 if n + n_split > capacity (then nothing but mask/dest/lambda written). */
 int64_t orc_densify(double* params, int64_t ld, int64_t n, int64_t capacity, double* acc,
                     int64_t ldg, double denom, double eps_split, double eta, double eps_abs,
+                    int32_t gate, double eps_grad, int64_t budget,
                     uint8_t* mask, int32_t* dest, double* lambda);
 
 int orc_num_threads(void);

@@ -35,7 +35,7 @@ class RasterParams(C.Structure):
 
 class DensifyParams(C.Structure):
     _fields_ = [("eps_split", C.c_float), ("eta", C.c_float), ("eps_abs", C.c_float),
-                ("eps_grad", C.c_float), ("denom", C.c_float), ("gate", C.c_int32)]
+                ("eps_grad", C.c_float), ("denom", C.c_float), ("gate", C.c_int32), ("budget", C.c_int64)]
 
 
 class Binning(C.Structure):
@@ -118,9 +118,11 @@ def raster_params(alpha_min=1.0 / 255.0, alpha_max=0.99, t_min=1e-4, dilation=0.
     return r
 
 
-def densify_params(eps_split=-1e-6, eta=0.5, eps_abs=0.0, denom=1.0):
+def densify_params(eps_split=-1e-6, eta=0.5, eps_abs=0.0, denom=1.0, eps_grad=None, budget=None):
     d = DensifyParams()
-    d.eps_split, d.eta, d.eps_abs, d.eps_grad, d.denom, d.gate = eps_split, eta, eps_abs, 0.0, denom, 0
+    d.eps_split, d.eta, d.eps_abs, d.denom = eps_split, eta, eps_abs, denom
+    d.gate, d.eps_grad = (0, 0.0) if eps_grad is None else (1, float(eps_grad))
+    d.budget = -1 if budget is None else int(budget)
     return d
 
 

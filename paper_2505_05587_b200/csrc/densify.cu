@@ -196,12 +196,98 @@ __device__ __forceinline__ void spawn(float* __restrict__ params, int64_t ld, fl
   for (int k = 0; k < 20; ++k) grad_S[k * ldg + b] = 0.f;
 }
 
+// Compactest gate (App. A.2): ||G_p / denom||_2 <= eps_grad on the position gradient.
+__device__ __forceinline__ bool gate_ok(const float* __restrict__ grad_S, int64_t ldg, int64_t i, float inv_denom,
+                                        float eps_grad) {
+  const float g0 = grad_S[0 * ldg + i] * inv_denom, g1 = grad_S[1 * ldg + i] * inv_denom;
+  const float g2 = grad_S[2 * ldg + i] * inv_denom;
+  return sqrtf(g0 * g0 + g1 * g1 + g2 * g2) <= eps_grad;
+}
+
+__device__ __forceinline__ uint32_t orderable(float f) {
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// ---- increment budget (App. A.2): keep the `budget` least lambda_min among the
+// candidates, ties by index.  Radix select of the threshold key over 4 byte-passes on the device. --
+struct SelState {
+  uint32_t hist[256];
+  uint32_t prefix, pmask, remaining, count;
+};
+
+__global__ void __launch_bounds__(kThreads) k_budget_keys(const float* __restrict__ grad_S, int64_t ldg, int64_t n,
+                                                          float inv_denom, float eps_split, int gate, float eps_grad,
+                                                          uint32_t* __restrict__ keys, float* __restrict__ lambda,
+                                                          SelState* st) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool cand = false;
+  if (i < n) {
+    float S6[6];
+    load_sbar(grad_S, ldg, i, inv_denom, S6);
+    const float lam = decide_lambda(S6, eps_split);
+    if (lambda) lambda[i] = lam;
+    cand = lam < eps_split && (!gate || gate_ok(grad_S, ldg, i, inv_denom, eps_grad));
+    keys[i] = cand ? orderable(lam) : 0xFFFFFFFFu;
+  }
+  const uint32_t b = __ballot_sync(0xffffffffu, cand);
+  if ((threadIdx.x & 31) == 0 && b) atomicAdd(&st->count, (uint32_t)__popc(b));
+}
+
+__global__ void __launch_bounds__(kThreads) k_select_hist(const uint32_t* __restrict__ keys, int64_t n, int shift,
+                                                          int64_t budget, SelState* st) {
+  if ((int64_t)st->count <= budget) return;  // every candidate is kept: nothing to select
+  __shared__ uint32_t h[256];
+  h[threadIdx.x] = 0u;
+  __syncthreads();
+  const uint32_t prefix = st->prefix, pmask = st->pmask;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = keys[i];
+    if (k != 0xFFFFFFFFu && (k & pmask) == prefix) atomicAdd(&h[(k >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  if (h[threadIdx.x]) atomicAdd(&st->hist[threadIdx.x], h[threadIdx.x]);
+}
+
+__global__ void __launch_bounds__(256) k_select_pick(int shift, int64_t budget, SelState* st) {
+  if ((int64_t)st->count <= budget) return;
+  __shared__ uint32_t s_warp[8];
+  const int d = threadIdx.x, lane = d & 31, warp = d >> 5;
+  const uint32_t c = st->hist[d];
+  uint32_t inc = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) s_warp[warp] = inc;
+  __syncthreads();
+  uint32_t wpre = 0;
+  for (int w = 0; w < warp; ++w) wpre += s_warp[w];
+  const uint32_t excl = wpre + inc - c;
+  const uint32_t rem = shift == 24 ? (uint32_t)budget : st->remaining;
+  __syncthreads();
+  if (rem == 0u) {                       // budget 0: select nothing
+    if (d == 0) { st->prefix = 0u; st->pmask = 0xFFFFFFFFu; st->remaining = 0u; }
+  } else if (excl < rem && rem <= excl + c) {
+    st->prefix |= (uint32_t)d << shift;
+    st->pmask |= 0xFFu << shift;
+    st->remaining = rem - excl;
+  }
+  st->hist[d] = 0u;
+}
+
 // kFused (capacity >= 2n, so n + n_split <= capacity holds for any mask): the same kernel also
 // writes the offspring and clears S, one pass over the data and no second launch.
-template <bool kFused, int kIt>
+// kSel: the split set was already chosen (budget path): split = candidate key < threshold, or
+// == threshold within the first `remaining` ties in index order (tie ranks by this kernel's scan of
+// the ties would need a second look-back; ties are resolved by k_budget_ties first).
+template <bool kFused, int kIt, bool kSel>
 __global__ void __launch_bounds__(kThreads) k_densify_decide(float* __restrict__ params, int64_t ld,
                                                              float* __restrict__ grad_S, int64_t ldg, int64_t n,
                                                              float inv_denom, float eps_split, float eta, float eps_abs,
+                                                             int gate, float eps_grad,
+                                                             const uint8_t* __restrict__ sel,
                                                              uint8_t* __restrict__ mask, int32_t* __restrict__ dest,
                                                              float* __restrict__ lambda, uint64_t* status,
                                                              int* tile_counter, int64_t* n_split,
@@ -221,11 +307,16 @@ __global__ void __launch_bounds__(kThreads) k_densify_decide(float* __restrict__
     const int64_t i = base + (int64_t)j * kThreads + tid;
     split[j] = false;
     if (i < n) {
-      float S6[6];
-      load_sbar(grad_S, ldg, i, inv_denom, S6);
-      const float lam = decide_lambda(S6, eps_split);
-      split[j] = lam < eps_split;                     // Thm 2 / Alg. 1 P:L545 (strict, Z11)
-      if (lambda) lambda[i] = lam;
+      if (kSel) {
+        split[j] = sel[i] != 0;
+      } else {
+        float S6[6];
+        load_sbar(grad_S, ldg, i, inv_denom, S6);
+        const float lam = decide_lambda(S6, eps_split);
+        split[j] = lam < eps_split;                   // Thm 2 / Alg. 1 P:L545 (strict, Z11)
+        if (gate && split[j]) split[j] = gate_ok(grad_S, ldg, i, inv_denom, eps_grad);
+        if (lambda) lambda[i] = lam;
+      }
     }
     const uint32_t b = __ballot_sync(0xffffffffu, split[j]);
     pos[j] = __popc(b & lanemask_lt());
@@ -271,6 +362,66 @@ __global__ void __launch_bounds__(kThreads) k_densify_decide(float* __restrict__
   }
 }
 
+// Budget path, final selection: sel = key < t, or key == t and among the first `remaining` ties of t in
+// index order (decoupled look-back scan of the tie flags).  With count <= budget every candidate is kept.
+__global__ void __launch_bounds__(kThreads) k_budget_ties(const uint32_t* __restrict__ keys, int64_t n, int64_t budget,
+                                                          const SelState* st, uint8_t* __restrict__ sel,
+                                                          uint64_t* status, int* tile_counter) {
+  __shared__ int s_tile;
+  __shared__ uint32_t s_cnt[kItems][kThreads / 32];
+  __shared__ uint64_t s_excl;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) s_tile = atomicAdd(tile_counter, 1);
+  __syncthreads();
+  const int tile = s_tile;
+  const int64_t base = (int64_t)tile * kTileItems;
+  const bool all = (int64_t)st->count <= budget;
+  const uint32_t t = st->prefix, rem = st->remaining;
+  bool tie[kItems];
+  uint32_t key[kItems], pos[kItems];
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const int64_t i = base + (int64_t)j * kThreads + tid;
+    key[j] = i < n ? keys[i] : 0xFFFFFFFFu;
+    tie[j] = !all && key[j] != 0xFFFFFFFFu && key[j] == t;
+    const uint32_t b = __ballot_sync(0xffffffffu, tie[j]);
+    pos[j] = __popc(b & lanemask_lt());
+    if (lane == 0) s_cnt[j][warp] = __popc(b);
+  }
+  __syncthreads();
+  if (warp == 0) {
+    constexpr int nw = kThreads / 32;
+    uint32_t* cnt = &s_cnt[0][0];
+    const uint32_t a = cnt[2 * lane], bb = cnt[2 * lane + 1];
+    uint32_t sum = a + bb, inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += u;
+    }
+    const uint32_t ex = inc - sum;
+    cnt[2 * lane] = ex;
+    cnt[2 * lane + 1] = ex + a;
+    const uint32_t agg = __shfl_sync(0xffffffffu, inc, 31);
+    const uint64_t excl = lookback_warp(status, tile, agg);
+    if (lane == 0) s_excl = excl;
+    (void)nw;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const int64_t i = base + (int64_t)j * kThreads + tid;
+    if (i >= n) continue;
+    bool s = false;
+    if (key[j] != 0xFFFFFFFFu) {
+      if (all) s = true;
+      else if (key[j] < t) s = true;
+      else if (tie[j]) s = (s_excl + s_cnt[j][warp] + pos[j]) < rem;
+    }
+    sel[i] = s ? 1 : 0;
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) k_densify_apply(float* __restrict__ params, int64_t ld, int64_t n,
                                                             int64_t capacity, float* __restrict__ grad_S, int64_t ldg,
                                                             float inv_denom, float eta, float eps_abs,
@@ -298,43 +449,84 @@ inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 constexpr int kItemsFused = 1;   // one Gaussian per thread when the offspring are written too
 
-size_t densify_ws_bytes(int64_t n) {
-  const int64_t tiles = (n + kThreads * kItemsFused - 1) / (kThreads * kItemsFused);
-  return align_up(8 * (size_t)(tiles > 0 ? tiles : 1)) + 256;
+namespace {
+struct DensWs {
+  size_t st_decide, st_ties, counters, sel_state, keys, sel, end;
+};
+DensWs dens_layout(int64_t n) {
+  DensWs L;
+  const int64_t tiles1 = (n + kThreads * kItemsFused - 1) / (kThreads * kItemsFused);
+  const int64_t tiles8 = (n + kTileItems - 1) / kTileItems;
+  size_t o = 0;
+  auto take = [&](size_t b) { const size_t at = o; o = align_up(o + b); return at; };
+  L.st_decide = take(8 * (size_t)(tiles1 > 0 ? tiles1 : 1));
+  L.st_ties = take(8 * (size_t)(tiles8 > 0 ? tiles8 : 1));
+  L.counters = take(16 * sizeof(int));
+  L.sel_state = take(sizeof(SelState));
+  L.keys = take(4 * (size_t)(n > 0 ? n : 1));
+  L.sel = take((size_t)(n > 0 ? n : 1));
+  L.end = o;
+  return L;
 }
+}  // namespace
+
+size_t densify_ws_bytes(int64_t n) { return dens_layout(n).end; }
 
 cudaError_t launch_densify(float* params, int64_t ld, int64_t n, int64_t capacity, float* grad_S, int64_t ldg,
                            const steepgs_densify_params& dp, uint8_t* mask, int32_t* dest, float* lambda,
                            int64_t* n_split, int32_t* status, void* ws, size_t ws_bytes, cudaStream_t st) {
-  if (ws_bytes < densify_ws_bytes(n)) return cudaErrorInvalidValue;
+  const DensWs L = dens_layout(n);
+  if (ws_bytes < L.end) return cudaErrorInvalidValue;
   const bool fused = capacity >= 2 * n;
-  const int64_t tiles = fused ? (n + kThreads * kItemsFused - 1) / (kThreads * kItemsFused)
-                              : (n + kTileItems - 1) / kTileItems;
+  const bool budget = dp.budget >= 0;
   char* w = static_cast<char*>(ws);
-  uint64_t* sstatus = reinterpret_cast<uint64_t*>(w);
-  int* counter = reinterpret_cast<int*>(w + align_up(8 * (size_t)(tiles > 0 ? tiles : 1)));
-  cudaError_t e = cudaMemsetAsync(ws, 0, densify_ws_bytes(n), st);
+  uint64_t* st_decide = reinterpret_cast<uint64_t*>(w + L.st_decide);
+  uint64_t* st_ties = reinterpret_cast<uint64_t*>(w + L.st_ties);
+  int* counter = reinterpret_cast<int*>(w + L.counters);
+  SelState* sst = reinterpret_cast<SelState*>(w + L.sel_state);
+  uint32_t* keys = reinterpret_cast<uint32_t*>(w + L.keys);
+  uint8_t* sel = reinterpret_cast<uint8_t*>(w + L.sel);
+  cudaError_t e = cudaMemsetAsync(ws, 0, L.keys, st);   // scan states, counters, selection state
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(n_split, 0, sizeof(int64_t), st);
   if (e != cudaSuccess) return e;
   const float inv_denom = 1.0f / dp.denom;
-  if (n > 0 && fused) {
-    k_densify_decide<true, kItemsFused><<<(unsigned)tiles, kThreads, 0, st>>>(params, ld, grad_S, ldg, n, inv_denom, dp.eps_split,
-                                                                 dp.eta, dp.eps_abs, mask, dest, lambda, sstatus,
-                                                                 counter, n_split, status);
+  const unsigned b1 = (unsigned)((n + kThreads - 1) / kThreads);
+  if (n > 0 && budget) {
+    k_budget_keys<<<b1, kThreads, 0, st>>>(grad_S, ldg, n, inv_denom, dp.eps_split, dp.gate, dp.eps_grad, keys, lambda,
+                                           sst);
     note_launch();
-    return check_launch("k_densify_decide<fused>");
+    if ((e = check_launch("k_budget_keys")) != cudaSuccess) return e;
+    unsigned hb = b1 < 148 * 8 ? b1 : 148 * 8;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      k_select_hist<<<hb, kThreads, 0, st>>>(keys, n, shift, dp.budget, sst);
+      k_select_pick<<<1, 256, 0, st>>>(shift, dp.budget, sst);
+      note_launch(2);
+      if ((e = check_launch("k_select")) != cudaSuccess) return e;
+    }
+    const unsigned bt = (unsigned)((n + kTileItems - 1) / kTileItems);
+    k_budget_ties<<<bt, kThreads, 0, st>>>(keys, n, dp.budget, sst, sel, st_ties, counter + 1);
+    note_launch();
+    if ((e = check_launch("k_budget_ties")) != cudaSuccess) return e;
   }
+  const int64_t tiles = fused ? (n + kThreads * kItemsFused - 1) / (kThreads * kItemsFused)
+                              : (n + kTileItems - 1) / kTileItems;
   if (n > 0) {
-    k_densify_decide<false, kItems><<<(unsigned)tiles, kThreads, 0, st>>>(params, ld, grad_S, ldg, n, inv_denom, dp.eps_split,
-                                                                  dp.eta, dp.eps_abs, mask, dest, lambda, sstatus,
-                                                                  counter, n_split, status);
+#define SGS_DECIDE(F, IT, SEL)                                                                              \
+  k_densify_decide<F, IT, SEL><<<(unsigned)tiles, kThreads, 0, st>>>(                                      \
+      params, ld, grad_S, ldg, n, inv_denom, dp.eps_split, dp.eta, dp.eps_abs, dp.gate, dp.eps_grad, sel,  \
+      mask, dest, budget ? nullptr : lambda, st_decide, counter, n_split, status)
+    if (fused && budget) SGS_DECIDE(true, kItemsFused, true);
+    else if (fused) SGS_DECIDE(true, kItemsFused, false);
+    else if (budget) SGS_DECIDE(false, kItems, true);
+    else SGS_DECIDE(false, kItems, false);
+#undef SGS_DECIDE
     note_launch();
     if ((e = check_launch("k_densify_decide")) != cudaSuccess) return e;
+    if (fused) return cudaSuccess;
   }
-  const unsigned blocks = (unsigned)((n + kThreads - 1) / kThreads);
-  k_densify_apply<<<blocks > 0 ? blocks : 1, kThreads, 0, st>>>(params, ld, n, capacity, grad_S, ldg, inv_denom, dp.eta,
-                                                                dp.eps_abs, mask, dest, n_split, status);
+  k_densify_apply<<<b1 > 0 ? b1 : 1, kThreads, 0, st>>>(params, ld, n, capacity, grad_S, ldg, inv_denom, dp.eta,
+                                                        dp.eps_abs, mask, dest, n_split, status);
   note_launch();
   return check_launch("k_densify_apply");
 }

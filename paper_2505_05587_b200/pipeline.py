@@ -116,8 +116,9 @@ class Rasterizer:
 
     # ---- a8 ----
     def densify(self, params: torch.Tensor, grad_S: torch.Tensor, n: int, capacity: int, eps_split=-1e-6, eta=0.5,
-                eps_abs=0.0, denom=1.0, want_lambda=True):
-        dp = _lib.densify_params(eps_split, eta, eps_abs, denom)
+                eps_abs=0.0, denom=1.0, want_lambda=True, eps_grad=None, budget=None):
+        """SDC densify (Thm 2).  eps_grad: compactest gate (App. A.2); budget: split at most this many."""
+        dp = _lib.densify_params(eps_split, eta, eps_abs, denom, eps_grad, budget)
         _lib.densify(params, params.shape[1], n, capacity, grad_S, grad_S.shape[1], dp, self.split_mask,
                      self.dest_index, self.lambda_min if want_lambda else None, self.n_split, self.dens_status,
                      self.dens_ws)

@@ -395,3 +395,70 @@ def test_densify_full_size_c4(orc):
     assert ns == int(mask.sum())
     dest = rz.dest_index[:n].cpu().numpy()
     assert np.array_equal(dest[mask == 1], n + np.arange(ns))
+
+
+def _gpu_densify_g(p, S, G, n, cap, **kw):
+    from gpu_run import to_dev
+    from paper_2505_05587_b200.pipeline import Rasterizer
+    P = torch.zeros(14, cap, dtype=torch.float32, device="cuda")
+    P[:, :n] = to_dev(p)
+    A = torch.zeros(20, cap, dtype=torch.float32, device="cuda")
+    A[14:20, :n] = to_dev(S)
+    A[0:3, :n] = to_dev(G)
+    rz = Rasterizer(cap, 1, 16, 16)
+    rz.densify(P, A, n, cap, **kw)
+    torch.cuda.synchronize()
+    return rz, P, A
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_densify_budget_and_gate_parity(orc, fused):
+    """App. A.2 variants: increment budget (least lambda_min first, ties by index) and the compactest
+    gate; inputs keep lambda_min away from eps_split, |G| away from eps_grad, and the budget cut
+    away from near-equal lambda values (oracle-decided)."""
+    n, denom = 5000, 2.0
+    cap = 2 * n if fused else n + n // 2 + 64
+    p, S = _densify_inputs(orc, n, 31, denom=denom)
+    rng = np.random.default_rng(32)
+    G = (rng.lognormal(0.0, 1.0, size=(3, n)) * 1e-3 * rng.choice([-1.0, 1.0], size=(3, n))).astype(np.float32)
+    gn = np.linalg.norm(G.astype(np.float64) / denom, axis=0)
+    eps_grad = float(np.median(gn))
+    G[:, np.abs(gn - eps_grad) <= 1e-4 * eps_grad] *= 1.5
+    lam = np.array([orc.eig_sym3(S[:, i].astype(np.float64) / denom)[0][0] for i in range(n)])
+    cand = np.flatnonzero(lam < -1e-6)
+    K = len(cand) // 3
+    srt = np.sort(lam[cand])
+    while abs(srt[K] - srt[K - 1]) <= 1e-4 * np.abs(srt).max():    # a clear cut between kept / dropped
+        K += 1
+    accd = np.zeros((20, cap)); pd = np.zeros((14, cap)); pd[:, :n] = p
+    for kw in (dict(budget=K), dict(eps_grad=eps_grad), dict(budget=K // 2, eps_grad=eps_grad)):
+        accd[:] = 0.0
+        accd[14:20, :n] = S
+        accd[0:3, :n] = G
+        r = orc.densify(pd, accd, n, cap, denom=denom, **kw)
+        rz, P, A = _gpu_densify_g(p, S, G, n, cap, denom=denom, **kw)
+        assert int(rz.dens_status.item()) == 0
+        assert int(rz.n_split.item()) == r["n_split"] > 0, kw
+        assert np.array_equal(rz.split_mask[:n].cpu().numpy(), r["mask"]), kw
+        assert np.array_equal(rz.dest_index[:n].cpu().numpy(), r["dest"]), kw
+        if "budget" in kw:
+            assert r["n_split"] <= kw["budget"]
+
+
+def test_densify_budget_exact_ties(orc):
+    n = 40
+    p = synth.blob_scene(n, 3)
+    S = np.zeros((6, n), np.float32)
+    S[[0, 3, 5]] = 1.0
+    for i in (3, 7, 8, 20, 21, 33):
+        S[:, i] = [-2.0, 0.1, 0.0, 1.0, 0.0, 1.0]          # identical indefinite matrices: exact ties
+    S[:, 30] = [-5.0, 0.0, 0.0, 1.0, 0.0, 1.0]             # strictly smallest
+    G = np.zeros((3, n), np.float32)
+    for K in (0, 1, 3, 7, 100):
+        accd = np.zeros((20, 2 * n)); accd[14:20, :n] = S
+        pd = np.zeros((14, 2 * n)); pd[:, :n] = p
+        r = orc.densify(pd, accd, n, 2 * n, budget=K)
+        rz, _, _ = _gpu_densify_g(p, S, G, n, 2 * n, budget=K)
+        assert np.array_equal(rz.split_mask[:n].cpu().numpy(), r["mask"]), K
+        assert np.array_equal(rz.dest_index[:n].cpu().numpy(), r["dest"]), K
+    assert list(np.flatnonzero(r["mask"])) == [3, 7, 8, 20, 21, 30, 33]

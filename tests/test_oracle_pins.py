@@ -392,3 +392,30 @@ def test_theorem1_merged_slot_second_order(orc):
     ratios = [errs[k] / errs[k + 1] for k in range(3)]
     assert all(2.5 <= r <= 5.5 for r in ratios), (errs, ratios)
     assert abs(errs[-1]) < 0.05 * abs(lam[0] / 2)
+
+
+def test_budget_and_gate_variants_spec_examples(orc):
+    """App. A.2: increment budget keeps the least lambda_min (lambda = (-3,-1,-2), K = 2
+    keeps -3 and -2; K = 0 keeps none), ties by index; the compactest gate also requires a small
+    accumulated position gradient."""
+    mats = [np.diag([-3.0, 1, 2]), np.diag([-1.0, 1, 2]), np.diag([-2.0, 1, 2]), np.eye(3)]
+    p = np.zeros((14, 16))
+    p[:, :4] = params_from(np.zeros((4, 3)), [0.1, 0.1, 0.1])
+    r = orc.densify(p, _acc_from_S(mats, 4, 16), 4, 16, budget=2)
+    assert list(r["mask"]) == [1, 0, 1, 0] and list(r["dest"]) == [4, -1, 5, -1]
+    r = orc.densify(p, _acc_from_S(mats, 4, 16), 4, 16, budget=0)
+    assert list(r["mask"]) == [0, 0, 0, 0] and r["n_split"] == 0
+    r = orc.densify(p, _acc_from_S(mats, 4, 16), 4, 16, budget=5)
+    assert list(r["mask"]) == [1, 1, 1, 0]
+    ties = [np.diag([-1.0, 1, 2])] * 5
+    r = orc.densify(p, _acc_from_S(ties, 5, 16), 5, 16, budget=3)
+    assert list(r["mask"]) == [1, 1, 1, 0, 0]
+    acc = _acc_from_S(mats, 4, 16)
+    acc[0:3, 0] = [3.0, 0.0, 4.0]          # |G| = 5
+    acc[0:3, 2] = [0.1, 0.0, 0.0]          # |G| = 0.1
+    r = orc.densify(p, acc, 4, 16, eps_grad=1.0)
+    assert list(r["mask"]) == [0, 1, 1, 0]
+    acc10 = acc.copy()
+    acc10[14:20] *= 10.0                    # same S_bar with denom = 10; |G / denom| = 0.5 for index 0
+    r = orc.densify(p, acc10, 4, 16, eps_grad=1.0, denom=10.0)
+    assert list(r["mask"]) == [1, 1, 1, 0]

@@ -151,7 +151,8 @@ steepgs_status steepgs_l1_grad(const float* image, const float* target, int32_t 
  * P:L537-538).  Replays each pixel back to front, accumulates per (view, Gaussian) 9 moments of
  * w = dL/dsigma * sigma (sum w, sum w d, sum w d d^T, sum alpha T dL/dC) into moments_ws, then per
  * Gaussian chains them to dL/dparams and S_view = P^T (Q M Q - m0 Q) P, summed over the V views.
- * grad_S: if accumulate != 0 grad_S += result, else grad_S = result (columns [0, n)).
+ * grad_S (columns [0, n)): accumulate = 0: grad_S = result; 1: grad_S += result; 2: gradient planes
+ * 0-13 = result, S planes 14-19 += result (Alg. 1: per-step gradients, S summed over T_split steps).
  * moments_ws [V][n][12] fp32 must be all-zero on first use; the call leaves it all-zero. */
 steepgs_status steepgs_render_bwd_split(const float* params, int64_t ld, int64_t n,
                                         const steepgs_splat* splats, const steepgs_binning* b,
@@ -193,6 +194,25 @@ steepgs_status steepgs_densify_host_count(float* params, int64_t ld, int64_t n, 
                                           uint8_t* split_mask, int32_t* dest_index, float* lambda_min,
                                           int64_t* n_split, int32_t* status, void* workspace,
                                           size_t ws_bytes, int64_t* n_split_host, void* stream);
+
+/* ---- Algorithm 1 optimiser step (NEXT f1; "update each Gaussian's parameters via standard
+ * gradient descent", 3DGS default Adam).  One fused pass over the 14 parameter planes:
+ * m = b1 m + (1-b1) g, v = b2 v + (1-b2) g^2, p -= lr_group * (m / (1-b1^t)) / (sqrt(v / (1-b2^t)) + eps),
+ * g = grad_S planes 0-13 (columns [0, n)); lr groups: mean, log-scale, quaternion, opacity logit, rgb.
+ * step t >= 1 (number of optimiser steps taken, including this one; bias corrections 1 - beta^t).
+ * gacc [3][ldm] or NULL: the position-gradient accumulator G of Alg. 1 (read by the compactest
+ * gate): gacc = g (gacc_accumulate = 0, first step of a densification window) or gacc += g (1). */
+typedef struct {              /* hyper-parameters in fp64; the kernel rounds lr, beta, 1 - beta, eps to fp32 */
+  double lr[5];
+  double beta1, beta2, eps;
+} steepgs_adam_params;
+steepgs_status steepgs_adam_step(float* params, int64_t ld, int64_t n, const float* grad_S, int64_t ldg,
+                                 float* adam_m, float* adam_v, int64_t ldm, const steepgs_adam_params* ap,
+                                 int64_t step, float* gacc, int32_t gacc_accumulate, void* stream);
+/* After a densify: zero the Adam moments (14 planes of m and v) of split parents (split_mask[i]) and
+ * of the appended offspring [n, n + *n_split) — both offspring are new Gaussians (Alg. 1). */
+steepgs_status steepgs_reset_moments(float* adam_m, float* adam_v, int64_t ldm, int64_t n,
+                                     const uint8_t* split_mask, const int64_t* n_split, void* stream);
 
 /* Copy planes [first, first + count) of a planar [*][ld] fp32 array, columns [0, n), device to
  * device (cudaMemcpy2DAsync; no kernel).  Used to checkpoint / restore Gaussian sets. */

@@ -1,0 +1,106 @@
+"""Algorithm 1 (SteepGS training loop) on the CPU oracle.  TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs may import
+this module.  It composes the fp64 oracle (render + densify from liboracle.so) with a textbook Adam
+written out in numpy fp64; it shares nothing with the CUDA product.
+
+Readings (C17-C20):
+  C17  "update each Gaussian parameters via standard gradient descent" = the optimiser
+       3DGS trains with: Adam (Kingma & Ba 2015, Alg. 1), one lr per parameter group (mean,
+       log-scale, quaternion, opacity logit, rgb), bias corrections with the global step count t.
+  C18  Schedule: a step t is a densify step iff t >= t_start and (t - t_start) % T_split
+       == 0; such a step takes no gradient step (Alg. 1's if/else).  Every other step renders its
+       batch, takes one Adam step and accumulates G (position gradient) and S.
+  C19  Accumulation windows: G and S restart after step t_start - T_split and after every densify
+       step, so each densify sees the T_split - 1 gradient steps since the last one and divides by
+       T_split as written.
+  C20  Split parents and both offspring restart with zero Adam moments (they are new Gaussians,
+       P:L547); the step count t is global.
+The per-step loss is the batch mean of the per-view L1 (Eq. eqn:loss with lambda = 0):
+dL/dimage = sign(image - target) / (3 H W V).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import densify as _densify
+from . import render as _render
+
+# plane -> parameter group (mean, log-scale, quaternion, opacity logit, rgb)
+PLANE_GROUP = np.array([0, 0, 0, 1, 1, 1, 2, 2, 2, 2, 3, 4, 4, 4])
+
+
+def adam_step(p, g, m, v, lr, beta1, beta2, eps, t):
+    """Kingma & Ba 2015, Algorithm 1, one step on [14][n] fp64 arrays (in place).  lr: 5 group lrs."""
+    lr_plane = np.asarray(lr, dtype=np.float64)[PLANE_GROUP][:, None]
+    m *= beta1
+    m += (1.0 - beta1) * g
+    v *= beta2
+    v += (1.0 - beta2) * g * g
+    m_hat = m / (1.0 - beta1 ** t)
+    v_hat = v / (1.0 - beta2 ** t)
+    p -= lr_plane * m_hat / (np.sqrt(v_hat) + eps)
+
+
+def is_densify_step(t: int, t_start: int, t_split: int) -> bool:
+    return t >= t_start and (t - t_start) % t_split == 0
+
+
+def window_restarts_after(t: int, t_start: int, t_split: int) -> bool:
+    return t == t_start - t_split or is_densify_step(t, t_start, t_split)
+
+
+def train(params0, n0: int, capacity: int, batches, T: int, t_start: int, t_split: int, lr, beta1=0.9,
+          beta2=0.999, eps=1e-15, rp=None, eps_split=-1e-6, eta=0.5, eps_grad=None, budget=None):
+    """Run steps t = 1..T.  batches(t) -> (cams, targets [V][3][H][W]) for gradient steps.
+    Returns dict(params [14][n], n, n_split, lambda_min [n] and ||G / T_split|| [n] per densify step, loss per gradient step)."""
+    P = np.zeros((14, capacity))
+    P[:, :n0] = np.asarray(params0, dtype=np.float64)[:, :n0]
+    m = np.zeros((14, capacity))
+    v = np.zeros((14, capacity))
+    G = np.zeros((3, capacity))
+    S = np.zeros((6, capacity))
+    n = n0
+    opt_t = 0
+    splits, losses, lams, gnorms = [], [], [], []
+    for t in range(1, T + 1):
+        if is_densify_step(t, t_start, t_split):
+            acc = np.zeros((20, capacity))
+            acc[0:3] = G
+            acc[14:20] = S
+            d = _densify(P, acc, n, capacity, denom=float(t_split), eps_split=eps_split, eta=eta,
+                         eps_grad=eps_grad, budget=budget)
+            if d["n_split"] < 0:
+                raise RuntimeError("capacity exceeded")
+            lams.append(d["lambda_min"].copy())
+            gnorms.append(np.linalg.norm(G[:, :n], axis=0) / t_split)
+            P = d["params"]
+            ns = d["n_split"]
+            reset = np.zeros(capacity, bool)
+            reset[:n] = d["mask"] != 0
+            reset[n:n + ns] = True
+            m[:, reset] = 0.0
+            v[:, reset] = 0.0
+            n += ns
+            splits.append(ns)
+        else:
+            cams, targets = batches(t)
+            V = len(cams)
+            grad = np.zeros((20, n))
+            loss = 0.0
+            for k, cam in enumerate(cams):
+                img = _render(P[:, :n], cam, rp)["image"]
+                H, W = img.shape[1:]
+                r = img - np.asarray(targets[k], dtype=np.float64)
+                scale = 1.0 / (3.0 * H * W * V)
+                loss += scale * np.abs(r).sum()
+                grad += _render(P[:, :n], cam, rp, dl_dimage=np.sign(r) * scale)["grad"]
+            losses.append(loss)
+            opt_t += 1
+            adam_step(P[:, :n], grad[:14], m[:, :n], v[:, :n], lr, beta1, beta2, eps, opt_t)
+            G[:, :n] += grad[0:3]
+            S[:, :n] += grad[14:20]
+        if window_restarts_after(t, t_start, t_split):
+            G[:] = 0.0
+            S[:] = 0.0
+    return dict(params=P[:, :n].copy(), n=n, n_split=splits, loss=losses, lambda_min=lams, g_norm=gnorms)

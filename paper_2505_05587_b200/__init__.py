@@ -5,6 +5,6 @@ this package is the thin Python binding (`_lib`), the host-side orchestration (`
 multi-GPU view sharding (`parallel`).  No CPU fallback exists.
 """
 from . import _lib  # noqa: F401
-from .pipeline import SMOOTH, Raster, Rasterizer, require_cuda  # noqa: F401
+from .pipeline import SMOOTH, Adam, Raster, Rasterizer, Schedule, Trainer, require_cuda  # noqa: F401
 
-__all__ = ["Rasterizer", "Raster", "SMOOTH", "require_cuda"]
+__all__ = ["Rasterizer", "Raster", "SMOOTH", "Trainer", "Adam", "Schedule", "require_cuda"]

@@ -38,6 +38,10 @@ class DensifyParams(C.Structure):
                 ("eps_grad", C.c_float), ("denom", C.c_float), ("gate", C.c_int32), ("budget", C.c_int64)]
 
 
+class AdamParams(C.Structure):
+    _fields_ = [("lr", C.c_double * 5), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double)]
+
+
 class Binning(C.Structure):
     _fields_ = [("ids", C.c_void_p), ("ranges", C.c_void_p), ("n_instances", C.c_void_p),
                 ("n_visible", C.c_void_p), ("overflow", C.c_void_p), ("max_instances", C.c_int64),
@@ -69,6 +73,8 @@ def lib():
             "steepgs_densify_workspace_size": [I64, P],
             "steepgs_densify": [P, I64, I64, I64, P, I64, P, P, P, P, P, P, P, C.c_size_t, P],
             "steepgs_densify_host_count": [P, I64, I64, I64, P, I64, P, P, P, P, P, P, P, C.c_size_t, P, P],
+            "steepgs_adam_step": [P, I64, I64, P, I64, P, P, I64, P, I64, P, I32, P],
+            "steepgs_reset_moments": [P, P, I64, I64, P, P, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -193,6 +199,24 @@ def densify(params, ld, n, capacity, grad_S, ldg, dp, mask, dest, lam, n_split, 
     _check("steepgs_densify", lib().steepgs_densify(ptr(params), ld, n, capacity, ptr(grad_S), ldg, C.byref(dp),
                                                     ptr(mask), ptr(dest), ptr(lam), ptr(n_split), ptr(status),
                                                     ptr(ws), ws.numel() * ws.element_size(), stream_ptr(stream)))
+
+
+def adam_params(lr, beta1=0.9, beta2=0.999, eps=1e-15):
+    a = AdamParams()
+    a.lr[:] = [float(x) for x in lr]
+    a.beta1, a.beta2, a.eps = float(beta1), float(beta2), float(eps)
+    return a
+
+
+def adam_step(params, n, grad_S, m, v, ap, step, gacc=None, gacc_accumulate=True, stream=None):
+    _check("steepgs_adam_step", lib().steepgs_adam_step(ptr(params), params.shape[1], n, ptr(grad_S), grad_S.shape[1],
+                                                        ptr(m), ptr(v), m.shape[1], C.byref(ap), int(step), ptr(gacc),
+                                                        int(bool(gacc_accumulate)), stream_ptr(stream)))
+
+
+def reset_moments(m, v, n, split_mask, n_split, stream=None):
+    _check("steepgs_reset_moments", lib().steepgs_reset_moments(ptr(m), ptr(v), m.shape[1], n, ptr(split_mask),
+                                                                ptr(n_split), stream_ptr(stream)))
 
 
 def launch_count() -> int:

@@ -182,6 +182,7 @@ steepgs_status steepgs_render_bwd_split(const float* params, int64_t ld, int64_t
   if ((s = check_raster(rp)) != STEEPGS_OK) return s;
   if ((s = check_binning(b, V, cams)) != STEEPGS_OK) return s;
   if (n < 0 || ld < n || ldg < n) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "need 0 <= n <= ld, ldg");
+  if (accumulate < 0 || accumulate > 2) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "accumulate must be 0, 1 or 2");
   if (n > 0 && (!params || !splats || !final_T || !n_contrib || !dL_dimage || !moments_ws || !grad_S))
     return fail(STEEPGS_ERR_INVALID_ARGUMENT, "null pointer");
   if (!aligned(moments_ws, 16)) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "moments_ws must be 16-byte aligned");
@@ -220,11 +221,36 @@ steepgs_status steepgs_gauss_bwd_split(const float* params, int64_t ld, int64_t 
   if ((s = check_views(cams, V, &pack)) != STEEPGS_OK) return s;
   if ((s = check_raster(rp)) != STEEPGS_OK) return s;
   if (n < 0 || ld < n || ldg < n) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "need 0 <= n <= ld, ldg");
+  if (accumulate < 0 || accumulate > 2) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "accumulate must be 0, 1 or 2");
   if (n > 0 && (!params || !moments_ws || !grad_S)) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "null pointer");
   if (!aligned(moments_ws, 16)) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "moments_ws must be 16-byte aligned");
   const cudaError_t e = launch_gauss_bwd(params, ld, n, pack, V, raster_k(rp), moments_ws, grad_S, ldg, accumulate,
                                          (cudaStream_t)stream);
   return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_gauss_bwd_split");
+}
+
+steepgs_status steepgs_adam_step(float* params, int64_t ld, int64_t n, const float* grad_S, int64_t ldg,
+                                 float* adam_m, float* adam_v, int64_t ldm, const steepgs_adam_params* ap,
+                                 int64_t step, float* gacc, int32_t gacc_accumulate, void* stream) {
+  steepgs_status s;
+  if ((s = device_ok()) != STEEPGS_OK) return s;
+  if (!ap || step < 1 || n < 0 || ld < n || ldg < n || ldm < n || !(ap->beta1 >= 0.0 && ap->beta1 < 1.0) ||
+      !(ap->beta2 >= 0.0 && ap->beta2 < 1.0) || !(ap->eps > 0.0) || (gacc_accumulate & ~1))
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "bad adam arguments");
+  if (n > 0 && (!params || !grad_S || !adam_m || !adam_v)) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "null pointer");
+  const cudaError_t e = launch_adam(params, ld, n, grad_S, ldg, adam_m, adam_v, ldm, *ap, step, gacc,
+                                    gacc_accumulate, (cudaStream_t)stream);
+  return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_adam_step");
+}
+
+steepgs_status steepgs_reset_moments(float* adam_m, float* adam_v, int64_t ldm, int64_t n,
+                                     const uint8_t* split_mask, const int64_t* n_split, void* stream) {
+  steepgs_status s;
+  if ((s = device_ok()) != STEEPGS_OK) return s;
+  if (!adam_m || !adam_v || !n_split || n < 0 || ldm < n || (n > 0 && !split_mask))
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "bad reset_moments arguments");
+  const cudaError_t e = launch_reset_moments(adam_m, adam_v, ldm, n, split_mask, n_split, ldm, (cudaStream_t)stream);
+  return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_reset_moments");
 }
 
 steepgs_status steepgs_copy_planes(float* dst, int64_t ld_dst, const float* src, int64_t ld_src, int64_t n,

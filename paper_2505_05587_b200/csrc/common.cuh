@@ -58,4 +58,10 @@ cudaError_t launch_densify(float* params, int64_t ld, int64_t n, int64_t capacit
                            const steepgs_densify_params& dp, uint8_t* mask, int32_t* dest, float* lambda,
                            int64_t* n_split, int32_t* status, void* ws, size_t ws_bytes, cudaStream_t st);
 
+cudaError_t launch_adam(float* params, int64_t ld, int64_t n, const float* grad, int64_t ldg, float* m, float* v,
+                        int64_t ldm, const steepgs_adam_params& ap, int64_t step, float* gacc, int gacc_accumulate,
+                        cudaStream_t st);
+cudaError_t launch_reset_moments(float* m, float* v, int64_t ldm, int64_t n, const uint8_t* mask,
+                                 const int64_t* n_split, int64_t capacity, cudaStream_t st);
+
 }  // namespace sgs

@@ -192,13 +192,13 @@ __global__ void __launch_bounds__(128) k_gauss_bwd(const float* __restrict__ par
   out[11] = gc[0]; out[12] = gc[1]; out[13] = gc[2];
 #pragma unroll
   for (int k = 0; k < 6; ++k) out[14 + k] = S6[k];
-  if (accumulate) {
+  // accumulate: 0 = overwrite all 20 planes, 1 = += all, 2 = overwrite the 14 gradient planes and
+  // += the 6 S planes (Alg. 1: per-step gradients for the optimizer, S summed over T_split steps)
+  const bool acc_g = accumulate == 1, acc_s = accumulate != 0;
 #pragma unroll
-    for (int k = 0; k < 20; ++k) grad_S[k * ldg + i] += out[k];
-  } else {
+  for (int k = 0; k < 14; ++k) grad_S[k * ldg + i] = acc_g ? grad_S[k * ldg + i] + out[k] : out[k];
 #pragma unroll
-    for (int k = 0; k < 20; ++k) grad_S[k * ldg + i] = out[k];
-  }
+  for (int k = 14; k < 20; ++k) grad_S[k * ldg + i] = acc_s ? grad_S[k * ldg + i] + out[k] : out[k];
 }
 
 }  // namespace

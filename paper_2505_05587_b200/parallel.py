@@ -35,6 +35,16 @@ def allreduce_accumulators(acc: torch.Tensor, group=None, n: int | None = None) 
     return acc
 
 
+def allreduce_planes(acc: torch.Tensor, first: int, count: int, n: int, group=None) -> torch.Tensor:
+    """Sum planes [first, first + count), columns [0, n) of a planar accumulator over ranks, in place."""
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return acc
+    blk = acc[first:first + count, :n].contiguous()
+    dist.all_reduce(blk, op=dist.ReduceOp.SUM, group=group)
+    acc[first:first + count, :n].copy_(blk)
+    return acc
+
+
 def params_checksum(params: torch.Tensor, n: int) -> float:
     """Debug aid: identical on every rank after densify (replicated parameters)."""
     return float(params[:, :n].double().sum().item())

@@ -147,3 +147,121 @@ class Rasterizer:
         ids = view(b.ids, 4 * min(I, self.max_instances), torch.int32).cpu()
         ranges = view(b.ranges, 8 * tiles, torch.int32).view(tiles, 2).cpu()
         return dict(ids=ids, ranges=ranges, n_instances=I, overflow=ovf, n_visible=nv)
+
+
+# ---------------------------------------------------------------------------------------------
+# NEXT f1: the Algorithm-1 loop with the paper's schedule.
+# Readings C17-C20: Adam per parameter group; densify steps take no gradient step;
+# G and S windows restart after step t_start - T_split and after each densify (denominator T_split);
+# split parents and offspring restart with zero Adam moments, the step count is global.
+# ---------------------------------------------------------------------------------------------
+@dataclasses.dataclass
+class Adam:
+    lr: tuple = (1.6e-4, 5e-3, 1e-3, 5e-2, 2.5e-3)   # mean, log-scale, quaternion, opacity logit, rgb (3DGS)
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-15
+
+
+@dataclasses.dataclass
+class Schedule:
+    t_start: int = 500          # "density control for every 100 steps starting from the 500th step"
+    t_split: int = 100
+    eps_split: float = -1e-6
+    eta: float = 0.5
+    eps_grad: float | None = None   # compactest gate (App. A.2)
+    budget: int | None = None       # increment budget (App. A.2)
+
+    def densify_at(self, t: int) -> bool:
+        return t >= self.t_start and (t - self.t_start) % self.t_split == 0
+
+    def window_restarts_after(self, t: int) -> bool:
+        return t == self.t_start - self.t_split or self.densify_at(t)
+
+
+class Trainer:
+    """Algorithm 1 on one GPU (or view-sharded over a process group: the 14 gradient planes are
+    allreduced every step so the Adam update stays replicated, the 6 S planes only before densify).
+
+    Device state, all [plane][capacity] fp32: params (14), grad_S (20: per-step gradients + the
+    window's S), adam m/v (14 each), gacc (3: the window's position-gradient sum G).  One host sync
+    per densify step (the new Gaussian count)."""
+
+    def __init__(self, params0: torch.Tensor, n: int, capacity: int, V: int, width: int, height: int,
+                 raster: Raster | None = None, adam: Adam | None = None, schedule: Schedule | None = None,
+                 max_instances: int | None = None, group=None):
+        require_cuda()
+        self.cap, self.n = int(capacity), int(n)
+        if self.n > self.cap:
+            raise ValueError("n > capacity")
+        self.rz = Rasterizer(self.cap, V, width, height, raster, max_instances)
+        d = self.rz.device
+        self.params = torch.zeros(N_PLANES, self.cap, dtype=torch.float32, device=d)
+        self.params[:, :self.n].copy_(params0[:, :self.n])
+        self.grad_S = torch.zeros(N_ACC, self.cap, dtype=torch.float32, device=d)
+        self.m = torch.zeros(N_PLANES, self.cap, dtype=torch.float32, device=d)
+        self.v = torch.zeros(N_PLANES, self.cap, dtype=torch.float32, device=d)
+        self.gacc = torch.zeros(3, self.cap, dtype=torch.float32, device=d)
+        self.adam = adam or Adam()
+        self.ap = _lib.adam_params(self.adam.lr, self.adam.beta1, self.adam.beta2, self.adam.eps)
+        self.sched = schedule or Schedule()
+        self.group = group
+        self.t = 0              # training steps done
+        self.opt_steps = 0      # Adam steps done
+        self.fresh = True       # the next gradient step opens an accumulation window
+        self.history: list[dict] = []
+
+    def _world(self) -> int:
+        import torch.distributed as dist
+        return dist.get_world_size(self.group) if dist.is_available() and dist.is_initialized() else 1
+
+    def _allreduce_planes(self, first: int, count: int):
+        if self._world() > 1:
+            from .parallel import allreduce_planes
+            allreduce_planes(self.grad_S, first, count, self.n, self.group)
+
+    def step(self, cams: list[dict] | None = None, targets: torch.Tensor | None = None) -> dict:
+        """Training step t = self.t + 1: a densify step (cams/targets ignored) or a gradient step on
+        the batch (len(cams) == V views, targets [V][3][H][W] on the device)."""
+        t = self.t + 1
+        if self.sched.densify_at(t):
+            info = self._densify(t)
+        else:
+            rz = self.rz
+            rz.project(self.params, self.n, cams)
+            rz.bin_sort()
+            rz.render_fwd()
+            count = 3 * rz._HW
+            _lib.l1_grad(rz.image, targets, rz.V, count, 1.0 / (count * rz.V * self._world()), rz.dL, rz.loss)
+            rz.render_bwd_moments()
+            rz.gauss_bwd(self.params, self.grad_S, accumulate=0 if self.fresh else 2)
+            self._allreduce_planes(0, N_PLANES)
+            self.opt_steps += 1
+            _lib.adam_step(self.params, self.n, self.grad_S, self.m, self.v, self.ap, self.opt_steps, self.gacc,
+                           gacc_accumulate=not self.fresh)
+            self.fresh = False
+            info = dict(t=t, kind="grad")
+        if self.sched.window_restarts_after(t):
+            self.fresh = True
+        self.t = t
+        return info
+
+    def _densify(self, t: int) -> dict:
+        rz, s = self.rz, self.sched
+        n = self.n
+        _lib.copy_planes(self.grad_S, self.gacc, n, 0, 3)           # G -> accumulator planes 0-2 (gate)
+        self._allreduce_planes(14, 6)
+        rz.densify(self.params, self.grad_S, n, self.cap, eps_split=s.eps_split, eta=s.eta,
+                   denom=float(s.t_split), eps_grad=s.eps_grad, budget=s.budget)
+        ns, st = int(rz.n_split.item()), int(rz.dens_status.item())
+        if st != 0:
+            raise _lib.SteepGSError("steepgs_densify", 3, f"capacity {self.cap} < {n} + {ns}")
+        _lib.reset_moments(self.m, self.v, n, rz.split_mask, rz.n_split)
+        self.n = n + ns
+        info = dict(t=t, kind="densify", n_before=n, n_split=ns)
+        self.history.append(info)
+        return info
+
+    def loss(self) -> torch.Tensor:
+        """Per-view losses of the last gradient step ([V], device)."""
+        return self.rz.loss

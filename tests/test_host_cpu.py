@@ -49,16 +49,16 @@ def test_host_only_entry_points(libsteepgs):
     from paper_2505_05587_b200 import _lib
     assert ctypes.sizeof(_lib.Camera) == 84 and ctypes.sizeof(_lib.RasterParams) == 32
     # the ctypes mirrors must match the C layouts of include/steepgs.h (checked with the C compiler)
-    src = ('#include <stdio.h>\n#include "steepgs.h"\nint main(void){printf("%zu %zu %zu %zu %zu\\n",'
+    src = ('#include <stdio.h>\n#include "steepgs.h"\nint main(void){printf("%zu %zu %zu %zu %zu %zu\\n",'
            'sizeof(steepgs_camera), sizeof(steepgs_raster_params), sizeof(steepgs_densify_params),'
-           'sizeof(steepgs_binning), sizeof(steepgs_splat));return 0;}')
+           'sizeof(steepgs_binning), sizeof(steepgs_splat), sizeof(steepgs_adam_params));return 0;}')
     import tempfile
     with tempfile.TemporaryDirectory() as d:
         open(os.path.join(d, "s.c"), "w").write(src)
         subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", os.path.join(d, "s"), os.path.join(d, "s.c")])
         sizes = [int(x) for x in subprocess.check_output([os.path.join(d, "s")]).split()]
     assert sizes == [ctypes.sizeof(_lib.Camera), ctypes.sizeof(_lib.RasterParams), ctypes.sizeof(_lib.DensifyParams),
-                     ctypes.sizeof(_lib.Binning), _lib.SPLAT_BYTES]
+                     ctypes.sizeof(_lib.Binning), _lib.SPLAT_BYTES, ctypes.sizeof(_lib.AdamParams)]
     assert _lib.version().startswith("steepgs-b200")
     assert _lib.bin_sort_workspace_size(1000, 2, 64, 48, 10000) > 0
     assert _lib.densify_workspace_size(5000) >= 8

@@ -104,6 +104,9 @@ typedef struct {
   const int64_t* n_instances;   /* device scalar I */
   const int64_t* n_visible;     /* device scalar: visible (view, Gaussian) pairs */
   const int32_t* overflow;      /* device flag: 1 if I > max_instances (results then invalid) */
+  uint32_t* tile_last;          /* [V * tiles_x * tiles_y]: zeroed by bin_sort; render_fwd stores the
+                                   tile's composited list prefix (max over its pixels of n_contrib),
+                                   which render_bwd reads: the backward needs the forward's binning */
   int64_t max_instances;
   int32_t tiles_x, tiles_y, V;
 } steepgs_binning;
@@ -153,14 +156,18 @@ steepgs_status steepgs_l1_grad(const float* image, const float* target, int32_t 
  * Gaussian chains them to dL/dparams and S_view = P^T (Q M Q - m0 Q) P, summed over the V views.
  * grad_S (columns [0, n)): accumulate = 0: grad_S = result; 1: grad_S += result; 2: gradient planes
  * 0-13 = result, S planes 14-19 += result (Alg. 1: per-step gradients, S summed over T_split steps).
- * moments_ws [V][n][12] fp32 must be all-zero on first use; the call leaves it all-zero. */
+ * moments_ws [V][n][12] fp32 must be all-zero on first use; the call leaves it all-zero.
+ * view_grad_stats [2][ldg] fp32 or NULL (NEXT f4, the ADC statistic of P:L154): plane 0 gets the sum
+ * over this call's views v with tiles_touched[v][i] > 0 of ||dL/dPi(p_i)||_2 (pixel units), plane 1
+ * the number of such views; written (accumulate = 0) or added (1, 2) like the S planes.
+ * tiles_touched ([V][n], from steepgs_project) is read only then. */
 steepgs_status steepgs_render_bwd_split(const float* params, int64_t ld, int64_t n,
                                         const steepgs_splat* splats, const steepgs_binning* b,
                                         const steepgs_camera* cams, int32_t V,
                                         const steepgs_raster_params* rp, const float* final_T,
                                         const int32_t* n_contrib, const float* dL_dimage,
                                         float* moments_ws, float* grad_S, int64_t ldg, int32_t accumulate,
-                                        void* stream);
+                                        const int32_t* tiles_touched, float* view_grad_stats, void* stream);
 
 /* The two halves of steepgs_render_bwd_split, exported separately so each kernel can be timed:
  * a5 (per-pixel replay -> moments_ws) and a6 (moments -> grad_S, S; clears moments_ws). */
@@ -171,7 +178,7 @@ steepgs_status steepgs_render_bwd_moments(const steepgs_splat* splats, int64_t n
 steepgs_status steepgs_gauss_bwd_split(const float* params, int64_t ld, int64_t n, const steepgs_camera* cams,
                                        int32_t V, const steepgs_raster_params* rp,
                                        float* moments_ws, float* grad_S, int64_t ldg, int32_t accumulate,
-                                       void* stream);
+                                       const int32_t* tiles_touched, float* view_grad_stats, void* stream);
 
 /* ---- a8: steepest density control (Thm 2; Alg. 1; eigen App. A.3
  * P:L584-604).  Per Gaussian: S_bar = S / denom; lambda_min by the trigonometric roots (fp32,
@@ -195,6 +202,31 @@ steepgs_status steepgs_densify_host_count(float* params, int64_t ld, int64_t n, 
                                           int64_t* n_split, int32_t* status, void* workspace,
                                           size_t ws_bytes, int64_t* n_split_host, void* stream);
 
+/* ---- NEXT f4: 3DGS Adaptive Density Control baseline.  Per Gaussian:
+ * g = view_grad_stats[0][i] / view_grad_stats[1][i] (0 if never visible); selected iff g >= eps_adc;
+ * clone iff ||Sigma||_2 = max_k s_k^2 <= tau_adc, else split.  Rank by exclusive scan, dest = n + rank.
+ * Clone: parent unchanged, copy appended at p - clone_step * G / denom (G = grad_S planes 0-2, the
+ * accumulated position gradient).  Split: both offspring at p + R(q) diag(s) z_j (z_0 = normals
+ * planes 0-2, z_1 = planes 3-5, column i; caller-drawn N(0, I)), log-scale + ln(scale_factor)
+ * (0.8: Sigma_j = 0.64 Sigma); A in slot i, B appended; opacity, quaternion, colour copied.
+ * view_grad_stats and all 20 grad_S planes are zeroed on [0, n + n_new).  Outputs: kind [n] u8
+ * (0 keep, 1 clone, 2 split), dest_index [n] i32, n_new [1] int64 and status [1] int32 device
+ * scalars (3 = capacity exceeded: params untouched). */
+typedef struct {
+  float eps_adc;       /* mean view-space gradient-norm threshold */
+  float tau_adc;       /* clone / split boundary on ||Sigma||_2 */
+  float clone_step;    /* clone displacement along -G / denom */
+  float scale_factor;  /* split offspring scale factor (> 0) */
+  float denom;         /* accumulated steps for G (> 0) */
+  int32_t reserved;
+} steepgs_adc_params;
+steepgs_status steepgs_adc_workspace_size(int64_t n, size_t* bytes /*[host]*/);
+steepgs_status steepgs_densify_adc(float* params, int64_t ld, int64_t n, int64_t capacity, float* grad_S,
+                                   int64_t ldg, float* view_grad_stats, const float* normals, int64_t ldz,
+                                   const steepgs_adc_params* ap, uint8_t* kind, int32_t* dest_index,
+                                   int64_t* n_new, int32_t* status, void* workspace, size_t ws_bytes,
+                                   void* stream);
+
 /* ---- Algorithm 1 optimiser step (NEXT f1; "update each Gaussian's parameters via standard
  * gradient descent", 3DGS default Adam).  One fused pass over the 14 parameter planes:
  * m = b1 m + (1-b1) g, v = b2 v + (1-b2) g^2, p -= lr_group * (m / (1-b1^t)) / (sqrt(v / (1-b2^t)) + eps),
@@ -209,10 +241,12 @@ typedef struct {              /* hyper-parameters in fp64; the kernel rounds lr,
 steepgs_status steepgs_adam_step(float* params, int64_t ld, int64_t n, const float* grad_S, int64_t ldg,
                                  float* adam_m, float* adam_v, int64_t ldm, const steepgs_adam_params* ap,
                                  int64_t step, float* gacc, int32_t gacc_accumulate, void* stream);
-/* After a densify: zero the Adam moments (14 planes of m and v) of split parents (split_mask[i]) and
- * of the appended offspring [n, n + *n_split) — both offspring are new Gaussians (Alg. 1). */
+/* After a densify: zero the Adam moments (14 planes of m and v) of the replaced parents
+ * (split_mask[i] == mask_value: 1 for steepgs_densify's mask, 2 for ADC splits in steepgs_densify_adc's
+ * kind) and of the appended offspring [n, n + *n_split) — new Gaussians (Alg. 1, C20). */
 steepgs_status steepgs_reset_moments(float* adam_m, float* adam_v, int64_t ldm, int64_t n,
-                                     const uint8_t* split_mask, const int64_t* n_split, void* stream);
+                                     const uint8_t* split_mask, const int64_t* n_split, int32_t mask_value,
+                                     void* stream);
 
 /* Copy planes [first, first + count) of a planar [*][ld] fp32 array, columns [0, n), device to
  * device (cudaMemcpy2DAsync; no kernel).  Used to checkpoint / restore Gaussian sets. */

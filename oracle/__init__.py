@@ -66,7 +66,7 @@ def lib():
         L.orc_position_hessian.argtypes = [P, C.c_int64, C.c_int64, P, P, C.c_double, C.c_double, P]
         L.orc_render_view.restype = C.c_int64
         L.orc_render_view.argtypes = [P, C.c_int64, C.c_int64, P, P, P, P, C.c_int32, C.c_int32, C.c_int32,
-                                      C.c_int32, C.c_int32, P, P, P, P, P, P, P, P, P]
+                                      C.c_int32, C.c_int32, P, P, P, P, P, P, P, P, P, P]
         L.orc_eig_sym3.restype = C.c_int
         L.orc_eig_sym3.argtypes = [P, P, P]
         L.orc_densify.restype = C.c_int64
@@ -144,7 +144,7 @@ def render(params, cam: dict, rp: dict | None = None, window=None, brute_force: 
            dl_dimage=None, split: dict | None = None, decision: dict | None = None) -> dict:
     """One view: image/T/n_comp/ambiguity over `window` = (x0, y0, w, h) (default: full image);
     with dl_dimage ([3][h][w] over the window) also grad[20][n] (14 param grads + 6 S planes),
-    absg[20][n] and amb_g[n]."""
+    absg[20][n], amb_g[n] and grad_mu[2][n] (dL/dPi(p), the ADC statistic's per-view gradient)."""
     p = f64(params)
     n = p.shape[1]
     if window is None:
@@ -152,10 +152,10 @@ def render(params, cam: dict, rp: dict | None = None, window=None, brute_force: 
     x0, y0, w, h = (int(v) for v in window)
     d = decision if decision is not None else decide(params, cam, rp)
     img = np.zeros((3, h, w)); T = np.zeros((h, w)); nc = np.zeros((h, w), np.int32); amb = np.zeros((h, w), np.uint8)
-    grad = absg = ambg = dl = None
+    grad = absg = ambg = dl = gmu = None
     if dl_dimage is not None:
         dl = np.ascontiguousarray(np.asarray(dl_dimage, dtype=np.float64).reshape(3, h, w))
-        grad = np.zeros((20, n)); absg = np.zeros((20, n)); ambg = np.zeros(n, np.uint8)
+        grad = np.zeros((20, n)); absg = np.zeros((20, n)); ambg = np.zeros(n, np.uint8); gmu = np.zeros((2, n))
     sp = None
     if split is not None:
         sp = Split()
@@ -166,11 +166,12 @@ def render(params, cam: dict, rp: dict | None = None, window=None, brute_force: 
     c, r = camera(cam), raster(rp)
     pairs = lib().orc_render_view(_ptr(p), n, n, C.byref(c), C.byref(r), _ptr(d["visible"]), _ptr(d["key"]),
                                   x0, y0, w, h, int(brute_force), C.byref(sp) if sp is not None else None,
-                                  _ptr(dl), _ptr(img), _ptr(T), _ptr(nc), _ptr(amb), _ptr(grad), _ptr(absg), _ptr(ambg))
+                                  _ptr(dl), _ptr(img), _ptr(T), _ptr(nc), _ptr(amb), _ptr(grad), _ptr(absg), _ptr(ambg),
+                                  _ptr(gmu))
     if pairs < 0:
         raise MemoryError("oracle render failed")
-    return dict(image=img, final_T=T, n_comp=nc, amb_px=amb, grad=grad, absg=absg, amb_g=ambg, pairs=int(pairs),
-                decision=d)
+    return dict(image=img, final_T=T, n_comp=nc, amb_px=amb, grad=grad, absg=absg, amb_g=ambg, grad_mu=gmu,
+                pairs=int(pairs), decision=d)
 
 
 def eig_sym3(A) -> tuple[np.ndarray, np.ndarray]:

@@ -417,12 +417,14 @@ static double slot_sigma(const cand_t* cd, const orc_split* split, const double*
   return sigma_at(&cd->g, x, y, d);
 }
 
+#define ACCW 42
+
 int64_t orc_render_view(const double* params, int64_t ld, int64_t n, const orc_camera* cam,
                         const orc_raster* rp, const uint8_t* visible, const uint32_t* depth_key,
                         int32_t x0, int32_t y0, int32_t w, int32_t h, int32_t brute_force,
                         const orc_split* split, const double* dL_dimage,
                         double* image, double* final_T, int32_t* n_comp, uint8_t* amb_px,
-                        double* grad, double* absg, uint8_t* amb_g) {
+                        double* grad, double* absg, uint8_t* amb_g, double* grad_mu) {
   const int want_bwd = dL_dimage != NULL;
   /* Candidates: visible Gaussians (fp32 decision) whose alpha support can reach the window. */
   int64_t ncand = 0, cap = 1024;
@@ -508,10 +510,10 @@ int64_t orc_render_view(const double* params, int64_t ld, int64_t n, const orc_c
   }
 
   const int nthr = orc_num_threads();
-  double* tacc = NULL;   /* per-thread [ncand][40] accumulators (grad 20 + abs 20) */
+  double* tacc = NULL;   /* per-thread [ncand][ACCW] accumulators (grad 20 + abs 20 + dL/dmu 2) */
   uint8_t* tamb = NULL;
   if (want_bwd) {
-    tacc = (double*)calloc((size_t)nthr * (size_t)(ncand > 0 ? ncand : 1) * 40, sizeof(double));
+    tacc = (double*)calloc((size_t)nthr * (size_t)(ncand > 0 ? ncand : 1) * ACCW, sizeof(double));
     tamb = (uint8_t*)calloc((size_t)(ncand > 0 ? ncand : 1), 1);
     if (!tacc || !tamb) { free(cand); free(start); free(list); free(tacc); free(tamb); return -1; }
   }
@@ -525,7 +527,7 @@ int64_t orc_render_view(const double* params, int64_t ld, int64_t n, const orc_c
 #else
     const int tid = 0;
 #endif
-    double* acc = want_bwd ? tacc + (size_t)tid * (size_t)ncand * 40 : NULL;
+    double* acc = want_bwd ? tacc + (size_t)tid * (size_t)ncand * ACCW : NULL;
     rec_t* recs = (rec_t*)malloc(sizeof(rec_t) * (size_t)(ncand > 0 ? ncand : 1));
 #pragma omp for schedule(static)
     for (int32_t ky = 0; ky < h; ++ky) {
@@ -595,8 +597,10 @@ int64_t orc_render_view(const double* params, int64_t ld, int64_t n, const orc_c
           hessian_pair(g, sg, d, H);
           contrib[14] = ga * H[0]; contrib[15] = ga * H[1]; contrib[16] = ga * H[2];
           contrib[17] = ga * H[4]; contrib[18] = ga * H[5]; contrib[19] = ga * H[8];
-          double* a = acc + (size_t)rc->c * 40;
+          double* a = acc + (size_t)rc->c * ACCW;
           for (int k = 0; k < 20; ++k) { a[k] += contrib[k]; a[20 + k] += fabs(contrib[k]); }
+          a[40] += ga * dsdmu[0];                               /* dL/dPi(p) (ADC statistic) */
+          a[41] += ga * dsdmu[1];
         }
       }
     }
@@ -606,11 +610,12 @@ int64_t orc_render_view(const double* params, int64_t ld, int64_t n, const orc_c
     for (int64_t c = 0; c < ncand; ++c) {
       const int64_t gi = cand[c].gid;
       for (int t = 0; t < nthr; ++t) {
-        const double* a = tacc + ((size_t)t * (size_t)ncand + (size_t)c) * 40;
+        const double* a = tacc + ((size_t)t * (size_t)ncand + (size_t)c) * ACCW;
         for (int k = 0; k < 20; ++k) {
           if (grad) grad[k * ld + gi] += a[k];
           if (absg) absg[k * ld + gi] += a[20 + k];
         }
+        if (grad_mu) { grad_mu[gi] += a[40]; grad_mu[ld + gi] += a[41]; }
       }
       if (amb_g && tamb[c]) amb_g[gi] = 1;
     }

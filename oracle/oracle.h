@@ -73,14 +73,15 @@ void orc_position_hessian(const double* params, int64_t ld, int64_t i, const orc
  * contributions|, amb_g[n] |= 1 for Gaussians in an ambiguous pixel's candidate list.
  * brute_force = 1: candidates = every visible Gaussian; 0: per-Gaussian fp64 AABB scatter.
  * amb_px[h][w] = 1 where some candidate sits within a rounding band of a threshold
- * (DESIGN.md §3.4).  split != NULL renders the merged-slot model (fwd only).
+ * (DESIGN.md §3.4).  split != NULL renders the merged-slot model (fwd only).  grad_mu (optional,
+ * [2][ld]) += dL/dPi(p) of this view, the 2D-mean gradient ADC thresholds.
  * Returns the number of composited pairs, or -1 on allocation failure. */
 int64_t orc_render_view(const double* params, int64_t ld, int64_t n, const orc_camera* cam,
                         const orc_raster* rp, const uint8_t* visible, const uint32_t* depth_key,
                         int32_t x0, int32_t y0, int32_t w, int32_t h, int32_t brute_force,
                         const orc_split* split, const double* dL_dimage,
                         double* image, double* final_T, int32_t* n_comp, uint8_t* amb_px,
-                        double* grad, double* absg, uint8_t* amb_g);
+                        double* grad, double* absg, uint8_t* amb_g, double* grad_mu);
 
 /* Symmetric 3x3 eigen-decomposition by cyclic Jacobi.  A = (xx,xy,xz,yy,yz,zz).
  * lam ascending; V columns are unit eigenvectors (V[3*r + c] = component r of vector c), each

@@ -25,6 +25,7 @@ import numpy as np
 
 from . import densify as _densify
 from . import render as _render
+from .adc import adc_densify
 
 # plane -> parameter group (mean, log-scale, quaternion, opacity logit, rgb)
 PLANE_GROUP = np.array([0, 0, 0, 1, 1, 1, 2, 2, 2, 2, 3, 4, 4, 4])
@@ -51,20 +52,44 @@ def window_restarts_after(t: int, t_start: int, t_split: int) -> bool:
 
 
 def train(params0, n0: int, capacity: int, batches, T: int, t_start: int, t_split: int, lr, beta1=0.9,
-          beta2=0.999, eps=1e-15, rp=None, eps_split=-1e-6, eta=0.5, eps_grad=None, budget=None):
+          beta2=0.999, eps=1e-15, rp=None, eps_split=-1e-6, eta=0.5, eps_grad=None, budget=None,
+          density="sdc", adc=None, normals=None):
     """Run steps t = 1..T.  batches(t) -> (cams, targets [V][3][H][W]) for gradient steps.
-    Returns dict(params [14][n], n, n_split, lambda_min [n] and ||G / T_split|| [n] per densify step, loss per gradient step)."""
+    density = "adc": the 3DGS baseline (oracle/adc.py) with adc = dict(eps_adc, tau_adc, clone_step,
+    scale_factor) and normals(t) -> [6][>=n] standard normals for that densify step.
+    Returns dict(params [14][n], n, n_split, lambda_min [n] and ||G / T_split|| [n] per densify step, loss per
+    gradient step); for "adc" lambda_min holds the mean view-gradient statistic and g_norm ||Sigma||_2."""
     P = np.zeros((14, capacity))
     P[:, :n0] = np.asarray(params0, dtype=np.float64)[:, :n0]
     m = np.zeros((14, capacity))
     v = np.zeros((14, capacity))
     G = np.zeros((3, capacity))
     S = np.zeros((6, capacity))
+    st_sum = np.zeros(capacity)        # ADC statistic (P:L154): sum of ||dL/dPi(p)|| over visible views
+    st_cnt = np.zeros(capacity)
     n = n0
     opt_t = 0
     splits, losses, lams, gnorms = [], [], [], []
     for t in range(1, T + 1):
-        if is_densify_step(t, t_start, t_split):
+        if is_densify_step(t, t_start, t_split) and density == "adc":
+            d = adc_densify(P, G, st_sum, st_cnt, n, capacity, adc["eps_adc"], adc["tau_adc"], adc["clone_step"],
+                            adc["scale_factor"], float(t_split), normals(t))
+            if d["n_new"] < 0:
+                raise RuntimeError("capacity exceeded")
+            with np.errstate(invalid="ignore", divide="ignore"):
+                lams.append(np.where(st_cnt[:n] > 0, st_sum[:n] / st_cnt[:n], 0.0))
+            gnorms.append(np.exp(2.0 * P[3:6, :n]).max(0))
+            ns = d["n_new"]
+            P = np.zeros((14, capacity))
+            P[:, :n + ns] = d["params"]
+            reset = np.zeros(capacity, bool)
+            reset[:n] = d["kind"] == 2
+            reset[n:n + ns] = True
+            m[:, reset] = 0.0
+            v[:, reset] = 0.0
+            n += ns
+            splits.append(ns)
+        elif is_densify_step(t, t_start, t_split):
             acc = np.zeros((20, capacity))
             acc[0:3] = G
             acc[14:20] = S
@@ -89,12 +114,17 @@ def train(params0, n0: int, capacity: int, batches, T: int, t_start: int, t_spli
             grad = np.zeros((20, n))
             loss = 0.0
             for k, cam in enumerate(cams):
-                img = _render(P[:, :n], cam, rp)["image"]
+                fw = _render(P[:, :n], cam, rp)
+                img = fw["image"]
                 H, W = img.shape[1:]
                 r = img - np.asarray(targets[k], dtype=np.float64)
                 scale = 1.0 / (3.0 * H * W * V)
                 loss += scale * np.abs(r).sum()
-                grad += _render(P[:, :n], cam, rp, dl_dimage=np.sign(r) * scale)["grad"]
+                bw = _render(P[:, :n], cam, rp, dl_dimage=np.sign(r) * scale, decision=fw["decision"])
+                grad += bw["grad"]
+                vis = fw["decision"]["visible"] != 0
+                st_sum[:n] += np.where(vis, np.hypot(bw["grad_mu"][0], bw["grad_mu"][1]), 0.0)
+                st_cnt[:n] += vis
             losses.append(loss)
             opt_t += 1
             adam_step(P[:, :n], grad[:14], m[:, :n], v[:, :n], lr, beta1, beta2, eps, opt_t)
@@ -103,4 +133,6 @@ def train(params0, n0: int, capacity: int, batches, T: int, t_start: int, t_spli
         if window_restarts_after(t, t_start, t_split):
             G[:] = 0.0
             S[:] = 0.0
+            st_sum[:] = 0.0
+            st_cnt[:] = 0.0
     return dict(params=P[:, :n].copy(), n=n, n_split=splits, loss=losses, lambda_min=lams, g_norm=gnorms)

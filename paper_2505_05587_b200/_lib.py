@@ -38,13 +38,19 @@ class DensifyParams(C.Structure):
                 ("eps_grad", C.c_float), ("denom", C.c_float), ("gate", C.c_int32), ("budget", C.c_int64)]
 
 
+class AdcParams(C.Structure):
+    _fields_ = [("eps_adc", C.c_float), ("tau_adc", C.c_float), ("clone_step", C.c_float),
+                ("scale_factor", C.c_float), ("denom", C.c_float), ("reserved", C.c_int32)]
+
+
 class AdamParams(C.Structure):
     _fields_ = [("lr", C.c_double * 5), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double)]
 
 
 class Binning(C.Structure):
     _fields_ = [("ids", C.c_void_p), ("ranges", C.c_void_p), ("n_instances", C.c_void_p),
-                ("n_visible", C.c_void_p), ("overflow", C.c_void_p), ("max_instances", C.c_int64),
+                ("n_visible", C.c_void_p), ("overflow", C.c_void_p), ("tile_last", C.c_void_p),
+                ("max_instances", C.c_int64),
                 ("tiles_x", C.c_int32), ("tiles_y", C.c_int32), ("V", C.c_int32)]
 
 
@@ -66,15 +72,17 @@ def lib():
             "steepgs_bin_sort": [P, P, P, I64, P, I32, P, P, C.c_size_t, I64, P, P],
             "steepgs_render_fwd": [P, I64, P, P, I32, P, P, P, P, P, P],
             "steepgs_render_bwd_moments": [P, I64, P, P, I32, P, P, P, P, P, P],
-            "steepgs_gauss_bwd_split": [P, I64, I64, P, I32, P, P, P, I64, I32, P],
+            "steepgs_gauss_bwd_split": [P, I64, I64, P, I32, P, P, P, I64, I32, P, P, P],
             "steepgs_copy_planes": [P, I64, P, I64, I64, I32, I32, P],
             "steepgs_l1_grad": [P, P, I32, I64, F, P, P, P],
-            "steepgs_render_bwd_split": [P, I64, I64, P, P, P, I32, P, P, P, P, P, P, I64, I32, P],
+            "steepgs_render_bwd_split": [P, I64, I64, P, P, P, I32, P, P, P, P, P, P, I64, I32, P, P, P],
             "steepgs_densify_workspace_size": [I64, P],
             "steepgs_densify": [P, I64, I64, I64, P, I64, P, P, P, P, P, P, P, C.c_size_t, P],
             "steepgs_densify_host_count": [P, I64, I64, I64, P, I64, P, P, P, P, P, P, P, C.c_size_t, P, P],
+            "steepgs_adc_workspace_size": [I64, P],
+            "steepgs_densify_adc": [P, I64, I64, I64, P, I64, P, P, I64, P, P, P, P, P, P, C.c_size_t, P],
             "steepgs_adam_step": [P, I64, I64, P, I64, P, P, I64, P, I64, P, I32, P],
-            "steepgs_reset_moments": [P, P, I64, I64, P, P, P],
+            "steepgs_reset_moments": [P, P, I64, I64, P, P, I32, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -165,10 +173,12 @@ def render_bwd_moments(splats, n, binning, cams_arr, V, rp, final_T, n_contrib, 
                                             ptr(n_contrib), ptr(dL), ptr(moments), stream_ptr(stream)))
 
 
-def gauss_bwd_split(params, ld, n, cams_arr, V, rp, moments, grad_S, ldg, accumulate, stream=None):
+def gauss_bwd_split(params, ld, n, cams_arr, V, rp, moments, grad_S, ldg, accumulate, tiles_touched=None,
+                    view_grad_stats=None, stream=None):
     _check("steepgs_gauss_bwd_split",
            lib().steepgs_gauss_bwd_split(ptr(params), ld, n, cams_arr, V, C.byref(rp),
-                                         ptr(moments), ptr(grad_S), ldg, int(accumulate), stream_ptr(stream)))
+                                         ptr(moments), ptr(grad_S), ldg, int(accumulate), ptr(tiles_touched),
+                                         ptr(view_grad_stats), stream_ptr(stream)))
 
 
 def copy_planes(dst, src, n, first, count, stream=None):
@@ -182,11 +192,12 @@ def l1_grad(image, target, V, count, scale, dL, loss=None, stream=None):
 
 
 def render_bwd_split(params, ld, n, splats, binning, cams_arr, V, rp, final_T, n_contrib, dL,
-                     moments, grad_S, ldg, accumulate, stream=None):
+                     moments, grad_S, ldg, accumulate, tiles_touched=None, view_grad_stats=None, stream=None):
     _check("steepgs_render_bwd_split",
            lib().steepgs_render_bwd_split(ptr(params), ld, n, ptr(splats), C.byref(binning),
                                           cams_arr, V, C.byref(rp), ptr(final_T), ptr(n_contrib), ptr(dL),
-                                          ptr(moments), ptr(grad_S), ldg, int(accumulate), stream_ptr(stream)))
+                                          ptr(moments), ptr(grad_S), ldg, int(accumulate), ptr(tiles_touched),
+                                          ptr(view_grad_stats), stream_ptr(stream)))
 
 
 def densify_workspace_size(n) -> int:
@@ -199,6 +210,28 @@ def densify(params, ld, n, capacity, grad_S, ldg, dp, mask, dest, lam, n_split, 
     _check("steepgs_densify", lib().steepgs_densify(ptr(params), ld, n, capacity, ptr(grad_S), ldg, C.byref(dp),
                                                     ptr(mask), ptr(dest), ptr(lam), ptr(n_split), ptr(status),
                                                     ptr(ws), ws.numel() * ws.element_size(), stream_ptr(stream)))
+
+
+def adc_params(eps_adc, tau_adc, clone_step=0.0, scale_factor=0.8, denom=1.0):
+    a = AdcParams()
+    a.eps_adc, a.tau_adc, a.clone_step, a.scale_factor, a.denom = (float(eps_adc), float(tau_adc), float(clone_step),
+                                                                   float(scale_factor), float(denom))
+    return a
+
+
+def adc_workspace_size(n) -> int:
+    out = C.c_size_t(0)
+    _check("steepgs_adc_workspace_size", lib().steepgs_adc_workspace_size(n, C.byref(out)))
+    return int(out.value)
+
+
+def densify_adc(params, n, capacity, grad_S, stats, normals, ap, kind, dest, n_new, status, ws, stream=None):
+    assert stats.shape[1] == grad_S.shape[1]
+    _check("steepgs_densify_adc",
+           lib().steepgs_densify_adc(ptr(params), params.shape[1], n, capacity, ptr(grad_S), grad_S.shape[1],
+                                     ptr(stats), ptr(normals), normals.shape[1], C.byref(ap), ptr(kind), ptr(dest),
+                                     ptr(n_new), ptr(status), ptr(ws), ws.numel() * ws.element_size(),
+                                     stream_ptr(stream)))
 
 
 def adam_params(lr, beta1=0.9, beta2=0.999, eps=1e-15):
@@ -214,9 +247,9 @@ def adam_step(params, n, grad_S, m, v, ap, step, gacc=None, gacc_accumulate=True
                                                         int(bool(gacc_accumulate)), stream_ptr(stream)))
 
 
-def reset_moments(m, v, n, split_mask, n_split, stream=None):
+def reset_moments(m, v, n, split_mask, n_split, mask_value=1, stream=None):
     _check("steepgs_reset_moments", lib().steepgs_reset_moments(ptr(m), ptr(v), m.shape[1], n, ptr(split_mask),
-                                                                ptr(n_split), stream_ptr(stream)))
+                                                                ptr(n_split), int(mask_value), stream_ptr(stream)))
 
 
 def launch_count() -> int:

@@ -174,7 +174,7 @@ steepgs_status steepgs_render_bwd_split(const float* params, int64_t ld, int64_t
                                         const steepgs_raster_params* rp,
                                         const float* final_T, const int32_t* n_contrib, const float* dL_dimage,
                                         float* moments_ws, float* grad_S, int64_t ldg, int32_t accumulate,
-                                        void* stream) {
+                                        const int32_t* tiles_touched, float* view_grad_stats, void* stream) {
   steepgs_status s;
   if ((s = device_ok()) != STEEPGS_OK) return s;
   CamPack pack;
@@ -183,6 +183,8 @@ steepgs_status steepgs_render_bwd_split(const float* params, int64_t ld, int64_t
   if ((s = check_binning(b, V, cams)) != STEEPGS_OK) return s;
   if (n < 0 || ld < n || ldg < n) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "need 0 <= n <= ld, ldg");
   if (accumulate < 0 || accumulate > 2) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "accumulate must be 0, 1 or 2");
+  if (view_grad_stats && n > 0 && !tiles_touched)
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "view_grad_stats needs tiles_touched");
   if (n > 0 && (!params || !splats || !final_T || !n_contrib || !dL_dimage || !moments_ws || !grad_S))
     return fail(STEEPGS_ERR_INVALID_ARGUMENT, "null pointer");
   if (!aligned(moments_ws, 16)) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "moments_ws must be 16-byte aligned");
@@ -190,7 +192,8 @@ steepgs_status steepgs_render_bwd_split(const float* params, int64_t ld, int64_t
   cudaError_t e = launch_render_bwd(splats, *b, cams[0].width, cams[0].height, rk, final_T, n_contrib, dL_dimage, n,
                                     moments_ws, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "steepgs_render_bwd_split");
-  e = launch_gauss_bwd(params, ld, n, pack, V, rk, moments_ws, grad_S, ldg, accumulate, (cudaStream_t)stream);
+  e = launch_gauss_bwd(params, ld, n, pack, V, rk, moments_ws, grad_S, ldg, accumulate, tiles_touched, view_grad_stats,
+                       (cudaStream_t)stream);
   return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_render_bwd_split");
 }
 
@@ -214,7 +217,7 @@ steepgs_status steepgs_render_bwd_moments(const steepgs_splat* splats, int64_t n
 steepgs_status steepgs_gauss_bwd_split(const float* params, int64_t ld, int64_t n, const steepgs_camera* cams,
                                        int32_t V, const steepgs_raster_params* rp,
                                        float* moments_ws, float* grad_S, int64_t ldg, int32_t accumulate,
-                                       void* stream) {
+                                       const int32_t* tiles_touched, float* view_grad_stats, void* stream) {
   steepgs_status s;
   if ((s = device_ok()) != STEEPGS_OK) return s;
   CamPack pack;
@@ -222,11 +225,38 @@ steepgs_status steepgs_gauss_bwd_split(const float* params, int64_t ld, int64_t 
   if ((s = check_raster(rp)) != STEEPGS_OK) return s;
   if (n < 0 || ld < n || ldg < n) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "need 0 <= n <= ld, ldg");
   if (accumulate < 0 || accumulate > 2) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "accumulate must be 0, 1 or 2");
+  if (view_grad_stats && n > 0 && !tiles_touched)
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "view_grad_stats needs tiles_touched");
   if (n > 0 && (!params || !moments_ws || !grad_S)) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "null pointer");
   if (!aligned(moments_ws, 16)) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "moments_ws must be 16-byte aligned");
   const cudaError_t e = launch_gauss_bwd(params, ld, n, pack, V, raster_k(rp), moments_ws, grad_S, ldg, accumulate,
-                                         (cudaStream_t)stream);
+                                         tiles_touched, view_grad_stats, (cudaStream_t)stream);
   return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_gauss_bwd_split");
+}
+
+steepgs_status steepgs_adc_workspace_size(int64_t n, size_t* bytes) {
+  if (!bytes || n < 0) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "bad arguments");
+  *bytes = adc_ws_bytes(n);
+  return STEEPGS_OK;
+}
+
+steepgs_status steepgs_densify_adc(float* params, int64_t ld, int64_t n, int64_t capacity, float* grad_S,
+                                   int64_t ldg, float* view_grad_stats, const float* normals, int64_t ldz,
+                                   const steepgs_adc_params* ap, uint8_t* kind, int32_t* dest_index,
+                                   int64_t* n_new, int32_t* status, void* workspace, size_t ws_bytes,
+                                   void* stream) {
+  steepgs_status s;
+  if ((s = device_ok()) != STEEPGS_OK) return s;
+  if (!ap || n < 0 || capacity < n || ld < capacity || ldg < capacity || ldz < n || capacity > INT32_MAX ||
+      !(ap->scale_factor > 0.f) || !(ap->denom > 0.f))
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "bad adc arguments (need n <= capacity <= ld, ldg; ldz >= n)");
+  if (!n_new || !status || !workspace || (n > 0 && (!params || !grad_S || !view_grad_stats || !normals || !kind ||
+                                                    !dest_index)))
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "null pointer");
+  const cudaError_t e = launch_adc(params, ld, n, capacity, grad_S, ldg, view_grad_stats, ldg, normals, ldz, *ap, kind,
+                                   dest_index, n_new, status, workspace, ws_bytes, (cudaStream_t)stream);
+  if (e == cudaErrorInvalidValue) return fail(STEEPGS_ERR_WORKSPACE_TOO_SMALL, "workspace too small");
+  return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_densify_adc");
 }
 
 steepgs_status steepgs_adam_step(float* params, int64_t ld, int64_t n, const float* grad_S, int64_t ldg,
@@ -244,12 +274,15 @@ steepgs_status steepgs_adam_step(float* params, int64_t ld, int64_t n, const flo
 }
 
 steepgs_status steepgs_reset_moments(float* adam_m, float* adam_v, int64_t ldm, int64_t n,
-                                     const uint8_t* split_mask, const int64_t* n_split, void* stream) {
+                                     const uint8_t* split_mask, const int64_t* n_split, int32_t mask_value,
+                                     void* stream) {
   steepgs_status s;
   if ((s = device_ok()) != STEEPGS_OK) return s;
-  if (!adam_m || !adam_v || !n_split || n < 0 || ldm < n || (n > 0 && !split_mask))
+  if (!adam_m || !adam_v || !n_split || n < 0 || ldm < n || (n > 0 && !split_mask) || mask_value < 1 ||
+      mask_value > 255)
     return fail(STEEPGS_ERR_INVALID_ARGUMENT, "bad reset_moments arguments");
-  const cudaError_t e = launch_reset_moments(adam_m, adam_v, ldm, n, split_mask, n_split, ldm, (cudaStream_t)stream);
+  const cudaError_t e = launch_reset_moments(adam_m, adam_v, ldm, n, split_mask, n_split, mask_value, ldm,
+                                            (cudaStream_t)stream);
   return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_reset_moments");
 }
 

@@ -51,7 +51,7 @@ cudaError_t launch_render_bwd(const steepgs_splat* splats, const steepgs_binning
                               const float* dL_dimage, int64_t n, float* moments, cudaStream_t st);
 cudaError_t launch_gauss_bwd(const float* params, int64_t ld, int64_t n, const CamPack& cams, int V,
                              const RasterK& rk, float* moments, float* grad_S, int64_t ldg, int accumulate,
-                             cudaStream_t st);
+                             const int32_t* tiles_touched, float* view_grad_stats, cudaStream_t st);
 
 size_t densify_ws_bytes(int64_t n);
 cudaError_t launch_densify(float* params, int64_t ld, int64_t n, int64_t capacity, float* grad_S, int64_t ldg,
@@ -62,6 +62,12 @@ cudaError_t launch_adam(float* params, int64_t ld, int64_t n, const float* grad,
                         int64_t ldm, const steepgs_adam_params& ap, int64_t step, float* gacc, int gacc_accumulate,
                         cudaStream_t st);
 cudaError_t launch_reset_moments(float* m, float* v, int64_t ldm, int64_t n, const uint8_t* mask,
-                                 const int64_t* n_split, int64_t capacity, cudaStream_t st);
+                                 const int64_t* n_split, int mask_value, int64_t capacity, cudaStream_t st);
+
+size_t adc_ws_bytes(int64_t n);
+cudaError_t launch_adc(float* params, int64_t ld, int64_t n, int64_t capacity, float* grad_S, int64_t ldg,
+                       float* stats, int64_t lds, const float* normals, int64_t ldz, const steepgs_adc_params& ap,
+                       uint8_t* kind, int32_t* dest, int64_t* n_new, int32_t* status, void* ws, size_t ws_bytes,
+                       cudaStream_t st);
 
 }  // namespace sgs

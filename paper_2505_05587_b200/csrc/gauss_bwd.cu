@@ -22,7 +22,9 @@ namespace {
 __global__ void __launch_bounds__(128) k_gauss_bwd(const float* __restrict__ params, int64_t ld, int64_t n,
                                                    const CamPack cams, int V, const RasterK rk,
                                                    float* __restrict__ moments, float* __restrict__ grad_S,
-                                                   int64_t ldg, int accumulate) {
+                                                   int64_t ldg, int accumulate,
+                                                   const int32_t* __restrict__ tiles_touched,
+                                                   float* __restrict__ vstats) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const float p0 = params[0 * ld + i], p1 = params[1 * ld + i], p2 = params[2 * ld + i];
@@ -47,6 +49,7 @@ __global__ void __launch_bounds__(128) k_gauss_bwd(const float* __restrict__ par
   float G3[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // dL/dSigma_3D (symmetric, full)
   float glogit = 0.f, gc[3] = {0.f, 0.f, 0.f};
   float S6[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  float vsum = 0.f, vcnt = 0.f;   // ADC statistics (f4): sum of ||dL/dPi(p)|| over visible views, count
 
   // Moments of view v + 1 are loaded (unconditionally: never-touched entries are zero) while view
   // v is processed, so each thread keeps one 48-B load in flight behind the arithmetic.
@@ -61,6 +64,8 @@ __global__ void __launch_bounds__(128) k_gauss_bwd(const float* __restrict__ par
     }
     const float m0 = ma.x, m1x = ma.y, m1y = ma.z, Mxx = ma.w, Mxy = mb.x, Myy = mb.y;
     const float cg0 = mb.z, cg1 = mb.w, cg2 = mc.x;
+    const bool vis = vstats != nullptr && __ldg(tiles_touched + (int64_t)v * n + i) > 0;
+    if (vis) vcnt += 1.f;
     if (m0 == 0.f && m1x == 0.f && m1y == 0.f && Mxx == 0.f && Mxy == 0.f && Myy == 0.f && cg0 == 0.f &&
         cg1 == 0.f && cg2 == 0.f)
       continue;
@@ -113,6 +118,7 @@ __global__ void __launch_bounds__(128) k_gauss_bwd(const float* __restrict__ par
     const float Qa = C * idet, Qb = -B * idet, Qc = A * idet;
     // dL/dmu = Q m1
     const float gmx = Qa * m1x + Qb * m1y, gmy = Qb * m1x + Qc * m1y;
+    if (vis) vsum += sqrtf(gmx * gmx + gmy * gmy);
     // K = Q M Q (2x2 sym)
     const float QM00 = Qa * Mxx + Qb * Mxy, QM01 = Qa * Mxy + Qb * Myy;
     const float QM10 = Qb * Mxx + Qc * Mxy, QM11 = Qb * Mxy + Qc * Myy;
@@ -199,16 +205,21 @@ __global__ void __launch_bounds__(128) k_gauss_bwd(const float* __restrict__ par
   for (int k = 0; k < 14; ++k) grad_S[k * ldg + i] = acc_g ? grad_S[k * ldg + i] + out[k] : out[k];
 #pragma unroll
   for (int k = 14; k < 20; ++k) grad_S[k * ldg + i] = acc_s ? grad_S[k * ldg + i] + out[k] : out[k];
+  if (vstats) {   // same window semantics as S: accumulate = 0 opens a new window
+    vstats[i] = accumulate ? vstats[i] + vsum : vsum;
+    vstats[ldg + i] = accumulate ? vstats[ldg + i] + vcnt : vcnt;
+  }
 }
 
 }  // namespace
 
 cudaError_t launch_gauss_bwd(const float* params, int64_t ld, int64_t n, const CamPack& cams, int V,
                              const RasterK& rk, float* moments, float* grad_S, int64_t ldg, int accumulate,
-                             cudaStream_t st) {
+                             const int32_t* tiles_touched, float* view_grad_stats, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   const unsigned blocks = (unsigned)((n + 127) / 128);
-  k_gauss_bwd<<<blocks, 128, 0, st>>>(params, ld, n, cams, V, rk, moments, grad_S, ldg, accumulate);
+  k_gauss_bwd<<<blocks, 128, 0, st>>>(params, ld, n, cams, V, rk, moments, grad_S, ldg, accumulate, tiles_touched,
+                                      view_grad_stats);
   note_launch();
   return check_launch("k_gauss_bwd");
 }

@@ -51,9 +51,9 @@ struct Buffer {
 
 struct Smem {
   Buffer buf[kStages];
+  uint4 raw[4][kBatch];          // producer staging: the next batch's 64-B records (cp.async), SoA by 16 B
   unsigned long long full[kStages], empty[kStages];
   int done_warps;
-  int maxlast;
 };
 
 __device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -100,44 +100,100 @@ __device__ __forceinline__ float pair_e(float dx, float dy, const float4 g, cons
   return __fsub_rn(p.y, m);
 }
 
-// Producer: stage splats [first, first + cnt) of the tile list into `B` (lane-strided) with the
-// 8-bit sub-block mask of each.  The record is exp2-ready (pre-scaled conic, log2 o, padded extents
-// from a1), so staging is a gather, two fp64 subtractions and eight interval tests.
-__device__ __forceinline__ void produce(Buffer& B, const uint32_t* __restrict__ ids, const steepgs_splat* __restrict__ vs,
-                                        uint32_t first, int cnt, double ox, double oy, float* mom_view, int lane) {
-  uint32_t gid[kBatch / 32];
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Producer (one warp): batch k covers tile-list positions [first + rel(k), + cnt(k)).  The records
+// of batch k + 1 are copied with cp.async (16 x 16 B in flight per lane) and the ids of batch k + 2
+// loaded while the warp waits for a free stage, so a batch costs the producer no exposed memory
+// round trip once it runs ahead.  Staging a record is then two fp64 subtractions and eight
+// interval tests of the padded extents against the 8x4 sub-blocks.
+// kFwd: stop early once every consumer warp has terminated (forward early exit).
+template <bool kFwd, class BatchOf>
+__device__ __forceinline__ void run_producer(Smem& sm, const uint32_t* __restrict__ ids,
+                                             const steepgs_splat* __restrict__ vs, uint32_t first, int nb,
+                                             BatchOf batch_of, double ox, double oy, float* mom_view, int lane) {
+  uint32_t gcur[kBatch / 32], gnext[kBatch / 32];
+  auto load_ids = [&](int k, uint32_t* g) {
+    int rel = 0, cnt = 0;
+    if (k < nb) batch_of(k, rel, cnt);
 #pragma unroll
-  for (int q = 0; q < kBatch / 32; ++q) {
-    const int k = q * 32 + lane;
-    gid[q] = k < cnt ? __ldg(ids + first + k) : 0u;
+    for (int q = 0; q < kBatch / 32; ++q) {
+      const int kk = q * 32 + lane;
+      g[q] = kk < cnt ? __ldg(ids + first + rel + kk) : 0u;
+    }
+  };
+  auto issue = [&](int k, const uint32_t* g) {
+    if (k < nb) {
+      int rel, cnt;
+      batch_of(k, rel, cnt);
+#pragma unroll
+      for (int q = 0; q < kBatch / 32; ++q) {
+        const int kk = q * 32 + lane;
+        if (kk < cnt) {
+          const uint4* src = reinterpret_cast<const uint4*>(vs + g[q]);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) cp_async16(&sm.raw[j][kk], src + j);
+        }
+      }
+    }
+    cp_async_commit();
+  };
+  load_ids(0, gcur);
+  issue(0, gcur);
+  load_ids(1, gnext);
+  for (int k = 0; k < nb; ++k) {
+    const int s = k % kStages;
+    if (k >= kStages) mbar_wait(&sm.empty[s], ((k / kStages) & 1) ^ 1, 256);
+    Buffer& B = sm.buf[s];
+    const int stop = kFwd ? (*reinterpret_cast<volatile int*>(&sm.done_warps) == kConsumers) : 0;
+    int rel, cnt;
+    batch_of(k, rel, cnt);
+    cp_async_wait_all();
+    if (!stop) {
+#pragma unroll
+      for (int q = 0; q < kBatch / 32; ++q) {
+        const int kk = q * 32 + lane;
+        if (kk >= cnt) { B.mask[kk] = 0u; continue; }
+        const double2 mean = *reinterpret_cast<const double2*>(&sm.raw[0][kk]);
+        const float4 a = *reinterpret_cast<const float4*>(&sm.raw[1][kk]);   // conic', log2 o
+        const float4 b = *reinterpret_cast<const float4*>(&sm.raw[2][kk]);   // rgb, o
+        const float4 c = *reinterpret_cast<const float4*>(&sm.raw[3][kk]);   // extents, tau
+        const float gx = (float)(mean.x - ox), gy = (float)(mean.y - oy);
+        B.geo[kk] = make_float4(gx, gy, a.x, a.y);
+        B.par[kk] = make_float4(a.z, a.w, 0.0f, 0.0f);
+        B.col[kk] = make_float4(b.x, b.y, b.z, 0.0f);
+        if (mom_view) B.mptr[kk] = mom_view + (size_t)gcur[q] * 12;
+        uint32_t xb = 0u, yb = 0u;
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+          if (gx - c.x <= 8.0f * t + 7.5f && gx + c.x >= 8.0f * t + 0.5f) xb |= 1u << t;
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          if (gy - c.y <= 4.0f * t + 3.5f && gy + c.y >= 4.0f * t + 0.5f) yb |= 1u << t;
+        uint32_t m = 0u;
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          if (yb & (1u << t)) m |= xb << (2 * t);
+        B.mask[kk] = m;
+      }
+    }
+    if (lane == 0) {
+      B.base = rel;
+      B.stop = stop;
+    }
+    __syncwarp();
+    mbar_arrive(&sm.full[s]);
+    if (stop) break;
+#pragma unroll
+    for (int q = 0; q < kBatch / 32; ++q) gcur[q] = gnext[q];
+    issue(k + 1, gcur);
+    load_ids(k + 2, gnext);
   }
-#pragma unroll
-  for (int q = 0; q < kBatch / 32; ++q) {
-    const int k = q * 32 + lane;
-    if (k >= cnt) { B.mask[k] = 0u; continue; }
-    const steepgs_splat* sp = vs + gid[q];
-    const double2 mean = __ldg(reinterpret_cast<const double2*>(sp));
-    const float4 a = __ldg(reinterpret_cast<const float4*>(sp) + 1);   // conic', log2 o
-    const float4 b = __ldg(reinterpret_cast<const float4*>(sp) + 2);   // rgb, o
-    const float4 c = __ldg(reinterpret_cast<const float4*>(sp) + 3);   // extents, tau
-    const float gx = (float)(mean.x - ox), gy = (float)(mean.y - oy);
-    B.geo[k] = make_float4(gx, gy, a.x, a.y);
-    B.par[k] = make_float4(a.z, a.w, 0.0f, 0.0f);
-    B.col[k] = make_float4(b.x, b.y, b.z, 0.0f);
-    if (mom_view) B.mptr[k] = mom_view + (size_t)gid[q] * 12;
-    uint32_t xb = 0u, yb = 0u;
-#pragma unroll
-    for (int s = 0; s < 2; ++s)
-      if (gx - c.x <= 8.0f * s + 7.5f && gx + c.x >= 8.0f * s + 0.5f) xb |= 1u << s;
-#pragma unroll
-    for (int s = 0; s < 4; ++s)
-      if (gy - c.y <= 4.0f * s + 3.5f && gy + c.y >= 4.0f * s + 0.5f) yb |= 1u << s;
-    uint32_t m = 0u;
-#pragma unroll
-    for (int s = 0; s < 4; ++s)
-      if (yb & (1u << s)) m |= xb << (2 * s);
-    B.mask[k] = m;
-  }
+  cp_async_wait_all();
 }
 
 // Consumer: compact the staged batch to the splats whose mask has bit `w` (ascending order) into
@@ -162,6 +218,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_fwd(const steepgs_splat*
                                                          int tiles_x, int tiles_per_view, const RasterK rk,
                                                          float* __restrict__ image, float* __restrict__ final_T,
                                                          int32_t* __restrict__ n_contrib,
+                                                         uint32_t* __restrict__ tile_last,
                                                          unsigned long long* __restrict__ pair_counts) {
   __shared__ Smem sm;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -180,21 +237,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_fwd(const steepgs_splat*
   __syncthreads();
 
   if (warp == kConsumers) {  // ---------------- producer ----------------
-    const steepgs_splat* vs = splats + (int64_t)view * n;
-    for (int k = 0; k < nb; ++k) {
-      const int s = k % kStages;
-      if (k >= kStages) mbar_wait(&sm.empty[s], ((k / kStages) & 1) ^ 1, 256);
-      Buffer& B = sm.buf[s];
-      const int stop = *reinterpret_cast<volatile int*>(&sm.done_warps) == kConsumers;
-      if (!stop) {
-        const uint32_t first = rg.x + (uint32_t)k * kBatch;
-        produce(B, ids, vs, first, min((int)(rg.y - first), kBatch), ox, oy, nullptr, lane);
-      }
-      if (lane == 0) { B.base = k * kBatch; B.stop = stop; }
-      __syncwarp();
-      mbar_arrive(&sm.full[s]);
-      if (stop) break;
-    }
+    const int len = (int)(rg.y - rg.x);
+    run_producer<true>(sm, ids, splats + (int64_t)view * n, rg.x, nb,
+                       [len](int k, int& rel, int& cnt) { rel = k * kBatch; cnt = min(len - rel, kBatch); }, ox, oy,
+                       nullptr, lane);
     return;
   }
 
@@ -254,6 +300,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_fwd(const steepgs_splat*
     final_T[(int64_t)view * HW + pix] = T;
     n_contrib[(int64_t)view * HW + pix] = last;
   }
+  {
+    const int wl = __reduce_max_sync(0xffffffffu, last);   // the tile's composited prefix, for the backward
+    if (lane == 0 && wl > 0) atomicMax(tile_last + (int64_t)view * tiles_per_view + tile, (uint32_t)wl);
+  }
   if (pair_counts) {
     unsigned long long c = (unsigned long long)ncomp, e = (unsigned long long)neval;
 #pragma unroll
@@ -285,7 +335,7 @@ __device__ __forceinline__ void red_v4(float* p, float a, float b, float c, floa
 //   phase 1 (pixel-parallel): each lane runs its pixel's recursion over the chunk and leaves
 //     w = dL/dsigma * sigma and alpha T in shared memory, plus a ballot of contributing pixels;
 //   phase 2 (splat-parallel): lanes e and e + 16 own entry e and sum its 9 moments over the
-//     contributing pixels (each half over 16 pixels), combine with one xor-16 shuffle per value, and
+//     contributing pixels (even / odd columns), combine with one xor-16 shuffle per value, and
 //     add them with two 16-B + one 4-B vector REDs.
 // No per-(warp, splat) cross-lane reduction tree: the reduction costs O(contributing pairs).
 __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat* __restrict__ splats,
@@ -295,6 +345,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
                                                          const float* __restrict__ final_T,
                                                          const int32_t* __restrict__ n_contrib,
                                                          const float* __restrict__ dL_dimage,
+                                                         const uint32_t* __restrict__ tile_last,
                                                          float* __restrict__ moments) {
   extern __shared__ __align__(16) unsigned char dsmem[];
   Smem& sm = *reinterpret_cast<Smem*>(dsmem);
@@ -321,34 +372,26 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
     sc.pix[warp][lane] = make_float4((float)lx + 0.5f, (float)ly + 0.5f, dl0, dl1);
     sc.pdl2[warp][lane] = dl2;
   }
+  // list prefix any pixel of the tile composited (stored by the forward), so the producer starts at
+  // once instead of after a block-wide reduction of n_contrib
+  const int L = (int)__ldg(tile_last + (int64_t)view * tiles_per_view + tile);
+  const int nb = (L + kBatch - 1) / kBatch;
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&sm.full[s], 32);
       mbar_init(&sm.empty[s], 32 * kConsumers);
     }
-    sm.maxlast = 0;
   }
   __syncthreads();
   const int wmax = __reduce_max_sync(0xffffffffu, last);
-  if (lane == 0 && wmax > 0) atomicMax(&sm.maxlast, wmax);
-  __syncthreads();
-  const int L = sm.maxlast;              // list prefix any pixel of the tile composited
-  const int nb = (L + kBatch - 1) / kBatch;
 
   if (warp == kConsumers) {  // ---------------- producer: batches from the back ----------------
-    const steepgs_splat* vs = splats + (int64_t)view * n;
-    float* mom_view = moments + (int64_t)view * n * 12;
-    for (int k = 0; k < nb; ++k) {
-      const int s = k % kStages;
-      if (k >= kStages) mbar_wait(&sm.empty[s], ((k / kStages) & 1) ^ 1, 256);
-      Buffer& B = sm.buf[s];
-      const int bb = nb - 1 - k;
-      const uint32_t first = rg.x + (uint32_t)bb * kBatch;
-      produce(B, ids, vs, first, min(L - bb * kBatch, kBatch), ox, oy, mom_view, lane);
-      if (lane == 0) B.base = bb * kBatch;
-      __syncwarp();
-      mbar_arrive(&sm.full[s]);
-    }
+    run_producer<false>(sm, ids, splats + (int64_t)view * n, rg.x, nb,
+                        [nb, L](int k, int& rel, int& cnt) {
+                          rel = (nb - 1 - k) * kBatch;
+                          cnt = min(L - rel, kBatch);
+                        },
+                        ox, oy, moments + (int64_t)view * n * 12, lane);
     return;
   }
 
@@ -362,7 +405,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
   const float4* spix = sc.pix[warp];
   const float* sdl2 = sc.pdl2[warp];
   const int e2 = lane & (kChunk - 1), half = lane >> 4;
-  const uint32_t half_mask = half ? 0xFFFF0000u : 0x0000FFFFu;
+  const uint32_t half_mask = half ? 0xAAAAAAAAu : 0x55555555u;   // alternate columns: balanced halves
   for (int k = 0; k < nb; ++k) {
     const int s = k % kStages;
     mbar_wait(&sm.full[s], (k / kStages) & 1, 32);
@@ -483,7 +526,7 @@ cudaError_t launch_render_fwd(const steepgs_splat* splats, int64_t n, const stee
   const int tpv = b.tiles_x * b.tiles_y;
   dim3 grid(tpv, b.V);
   k_render_fwd<<<grid, kThreads, 0, st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
-                                          b.tiles_x, tpv, rk, image, final_T, n_contrib,
+                                          b.tiles_x, tpv, rk, image, final_T, n_contrib, b.tile_last,
                                           reinterpret_cast<unsigned long long*>(pair_counts));
   note_launch();
   return check_launch("k_render_fwd");
@@ -517,7 +560,7 @@ cudaError_t launch_render_bwd(const steepgs_splat* splats, const steepgs_binning
     attr_set = true;
   }
   k_render_bwd<<<grid, kThreads, smem, st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
-                                          b.tiles_x, tpv, rk, final_T, n_contrib, dL_dimage, moments);
+                                          b.tiles_x, tpv, rk, final_T, n_contrib, dL_dimage, b.tile_last, moments);
   note_launch();
   return check_launch("k_render_bwd");
 }

@@ -99,20 +99,24 @@ class Rasterizer:
 
     # ---- a5 + a6 ----
     def render_bwd(self, params: torch.Tensor, grad_S: torch.Tensor, dL: torch.Tensor | None = None,
-                   accumulate: bool = False):
+                   accumulate: int = 0, view_grad_stats: torch.Tensor | None = None):
         dl = self.dL if dL is None else dL
-        _lib.render_bwd_split(params, params.shape[1], self.n, self.splats, self.binning, self.cams_arr, self.V, self.rp, self.final_T, self.n_contrib, dl, self.moments, grad_S,
-                              grad_S.shape[1], accumulate)
+        _lib.render_bwd_split(params, params.shape[1], self.n, self.splats, self.binning, self.cams_arr, self.V,
+                              self.rp, self.final_T, self.n_contrib, dl, self.moments, grad_S, grad_S.shape[1],
+                              accumulate, self.tiles_touched if view_grad_stats is not None else None,
+                              view_grad_stats)
 
     def render_bwd_moments(self, dL: torch.Tensor | None = None):
         """a5 only (per-pixel replay -> moments)."""
         _lib.render_bwd_moments(self.splats, self.n, self.binning, self.cams_arr, self.V, self.rp, self.final_T,
                                 self.n_contrib, self.dL if dL is None else dL, self.moments)
 
-    def gauss_bwd(self, params: torch.Tensor, grad_S: torch.Tensor, accumulate: bool = False):
-        """a6 only (moments -> dL/dparams and S)."""
+    def gauss_bwd(self, params: torch.Tensor, grad_S: torch.Tensor, accumulate: int = 0,
+                  view_grad_stats: torch.Tensor | None = None):
+        """a6 only (moments -> dL/dparams and S; optionally the ADC view-gradient statistics, f4)."""
         _lib.gauss_bwd_split(params, params.shape[1], self.n, self.cams_arr, self.V, self.rp,
-                             self.moments, grad_S, grad_S.shape[1], accumulate)
+                             self.moments, grad_S, grad_S.shape[1], accumulate,
+                             self.tiles_touched if view_grad_stats is not None else None, view_grad_stats)
 
     # ---- a8 ----
     def densify(self, params: torch.Tensor, grad_S: torch.Tensor, n: int, capacity: int, eps_split=-1e-6, eta=0.5,
@@ -122,6 +126,18 @@ class Rasterizer:
         _lib.densify(params, params.shape[1], n, capacity, grad_S, grad_S.shape[1], dp, self.split_mask,
                      self.dest_index, self.lambda_min if want_lambda else None, self.n_split, self.dens_status,
                      self.dens_ws)
+
+    # ---- f4 ----
+    def densify_adc(self, params: torch.Tensor, grad_S: torch.Tensor, stats: torch.Tensor, normals: torch.Tensor,
+                    n: int, capacity: int, eps_adc: float, tau_adc: float, clone_step: float = 0.0,
+                    scale_factor: float = 0.8, denom: float = 1.0):
+        """3DGS ADC baseline: clone / split by the mean view-space gradient norm."""
+        if not hasattr(self, "adc_ws"):
+            self.adc_ws = torch.empty(_lib.adc_workspace_size(self.cap), dtype=torch.uint8, device=self.device)
+            self.adc_kind = torch.empty(self.cap, dtype=torch.uint8, device=self.device)
+        ap = _lib.adc_params(eps_adc, tau_adc, clone_step, scale_factor, denom)
+        _lib.densify_adc(params, n, capacity, grad_S, stats, normals, ap, self.adc_kind, self.dest_index, self.n_split,
+                         self.dens_status, self.adc_ws)
 
     def forward_backward(self, params, n, cams, targets=None, grad_S=None, dL=None, accumulate=False):
         """a1..a6 for the V views of this call (no host sync)."""
@@ -171,6 +187,12 @@ class Schedule:
     eta: float = 0.5
     eps_grad: float | None = None   # compactest gate (App. A.2)
     budget: int | None = None       # increment budget (App. A.2)
+    density: str = "sdc"            # "sdc" (Alg. 1) or "adc" (3DGS baseline, f4)
+    eps_adc: float | None = None    # ADC threshold on the mean ||dL/dPi(p)|| in pixel units; None: 3DGS's
+                                    # 0.0002 in NDC units = 0.0004 / W (C22)
+    tau_adc: float = 2e-3           # ADC clone/split boundary on ||Sigma||_2 = (0.01 x scene extent ~4.4)^2
+    clone_step: float = 0.0         # ADC clone displacement along -G / T_split
+    scale_factor: float = 0.8       # ADC split offspring scale
 
     def densify_at(self, t: int) -> bool:
         return t >= self.t_start and (t - self.t_start) % self.t_split == 0
@@ -189,7 +211,7 @@ class Trainer:
 
     def __init__(self, params0: torch.Tensor, n: int, capacity: int, V: int, width: int, height: int,
                  raster: Raster | None = None, adam: Adam | None = None, schedule: Schedule | None = None,
-                 max_instances: int | None = None, group=None):
+                 max_instances: int | None = None, group=None, seed: int = 0, normals_fn=None):
         require_cuda()
         self.cap, self.n = int(capacity), int(n)
         if self.n > self.cap:
@@ -202,6 +224,12 @@ class Trainer:
         self.m = torch.zeros(N_PLANES, self.cap, dtype=torch.float32, device=d)
         self.v = torch.zeros(N_PLANES, self.cap, dtype=torch.float32, device=d)
         self.gacc = torch.zeros(3, self.cap, dtype=torch.float32, device=d)
+        self.vstats = torch.zeros(2, self.cap, dtype=torch.float32, device=d) if (schedule or Schedule()).density == "adc" \
+            else None
+        self.normals = None
+        self.normals_fn = normals_fn     # ADC: t -> [6][>= n] device normals; default: drawn on the device
+        self.generator = torch.Generator(device=d)
+        self.generator.manual_seed(seed)
         self.adam = adam or Adam()
         self.ap = _lib.adam_params(self.adam.lr, self.adam.beta1, self.adam.beta2, self.adam.eps)
         self.sched = schedule or Schedule()
@@ -220,6 +248,11 @@ class Trainer:
             from .parallel import allreduce_planes
             allreduce_planes(self.grad_S, first, count, self.n, self.group)
 
+    def _allreduce_stats(self):
+        if self._world() > 1:
+            from .parallel import allreduce_planes
+            allreduce_planes(self.vstats, 0, 2, self.n, self.group)
+
     def step(self, cams: list[dict] | None = None, targets: torch.Tensor | None = None) -> dict:
         """Training step t = self.t + 1: a densify step (cams/targets ignored) or a gradient step on
         the batch (len(cams) == V views, targets [V][3][H][W] on the device)."""
@@ -234,7 +267,7 @@ class Trainer:
             count = 3 * rz._HW
             _lib.l1_grad(rz.image, targets, rz.V, count, 1.0 / (count * rz.V * self._world()), rz.dL, rz.loss)
             rz.render_bwd_moments()
-            rz.gauss_bwd(self.params, self.grad_S, accumulate=0 if self.fresh else 2)
+            rz.gauss_bwd(self.params, self.grad_S, accumulate=0 if self.fresh else 2, view_grad_stats=self.vstats)
             self._allreduce_planes(0, N_PLANES)
             self.opt_steps += 1
             _lib.adam_step(self.params, self.n, self.grad_S, self.m, self.v, self.ap, self.opt_steps, self.gacc,
@@ -249,14 +282,28 @@ class Trainer:
     def _densify(self, t: int) -> dict:
         rz, s = self.rz, self.sched
         n = self.n
-        _lib.copy_planes(self.grad_S, self.gacc, n, 0, 3)           # G -> accumulator planes 0-2 (gate)
-        self._allreduce_planes(14, 6)
-        rz.densify(self.params, self.grad_S, n, self.cap, eps_split=s.eps_split, eta=s.eta,
-                   denom=float(s.t_split), eps_grad=s.eps_grad, budget=s.budget)
+        _lib.copy_planes(self.grad_S, self.gacc, n, 0, 3)           # G -> accumulator planes 0-2 (gate / clone)
+        if s.density == "adc":
+            self._allreduce_stats()
+            if self.normals_fn is not None:
+                self.normals = self.normals_fn(t)
+            else:                                                      # z ~ N(0, I): an input of the method
+                if self.normals is None:
+                    self.normals = torch.empty(6, self.cap, dtype=torch.float32, device=rz.device)
+                self.normals.normal_(generator=self.generator)
+            eps_adc = s.eps_adc if s.eps_adc is not None else 0.0004 / rz.W
+            rz.densify_adc(self.params, self.grad_S, self.vstats, self.normals, n, self.cap, eps_adc, s.tau_adc,
+                           s.clone_step, s.scale_factor, float(s.t_split))
+            reset_mask, reset_value = rz.adc_kind, 2                   # clone parents keep their Adam state
+        else:
+            self._allreduce_planes(14, 6)
+            rz.densify(self.params, self.grad_S, n, self.cap, eps_split=s.eps_split, eta=s.eta,
+                       denom=float(s.t_split), eps_grad=s.eps_grad, budget=s.budget)
+            reset_mask, reset_value = rz.split_mask, 1
         ns, st = int(rz.n_split.item()), int(rz.dens_status.item())
         if st != 0:
             raise _lib.SteepGSError("steepgs_densify", 3, f"capacity {self.cap} < {n} + {ns}")
-        _lib.reset_moments(self.m, self.v, n, rz.split_mask, rz.n_split)
+        _lib.reset_moments(self.m, self.v, n, reset_mask, rz.n_split, reset_value)
         self.n = n + ns
         info = dict(t=t, kind="densify", n_before=n, n_split=ns)
         self.history.append(info)

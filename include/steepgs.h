@@ -122,6 +122,16 @@ steepgs_status steepgs_project(const float* params, int64_t ld, int64_t n, const
                                uint32_t* depth_key, uint32_t* tile_rect, int32_t* tiles_touched,
                                void* stream);
 
+/* ---- NEXT f3: view-dependent colour from real spherical harmonics (3DGS ordering and
+ * constants, degree 0..3, K = (degree + 1)^2).  colour = max(0, sum_k Y_k(dir) f_k + 1/2) per
+ * (view, Gaussian), dir = (p - o)/|p - o| with o = -R^T t (pinhole) or R^T e_z (affine).  The DC
+ * coefficients f_0 are parameter planes 11-13; sh_rest [3 (K - 1)][ld_sh] holds f_k, plane
+ * 3 (k - 1) + ch.  Same outputs as steepgs_project; the splat record carries the view's colour. */
+steepgs_status steepgs_project_sh(const float* params, int64_t ld, int64_t n, const float* sh_rest, int64_t ld_sh,
+                                  int32_t sh_degree, const steepgs_camera* cams, int32_t V,
+                                  const steepgs_raster_params* rp, steepgs_splat* splats, uint32_t* depth_key,
+                                  uint32_t* tile_rect, int32_t* tiles_touched, void* stream);
+
 /* ---- a2: bin & sort ("sorts points according to view-dependent depth"; C7).
  * Stable depth sort of visible (view, Gaussian) pairs, duplication per touched tile, stable sort
  * by (view, tile), tile ranges.  Result order within a tile: ascending (depth key, index) —
@@ -156,6 +166,7 @@ steepgs_status steepgs_l1_grad(const float* image, const float* target, int32_t 
  * Gaussian chains them to dL/dparams and S_view = P^T (Q M Q - m0 Q) P, summed over the V views.
  * grad_S (columns [0, n)): accumulate = 0: grad_S = result; 1: grad_S += result; 2: gradient planes
  * 0-13 = result, S planes 14-19 += result (Alg. 1: per-step gradients, S summed over T_split steps).
+ * accumulate | 4 (SH colour, after steepgs_sh_bwd): planes 0-2 are added to, planes 11-13 untouched.
  * moments_ws [V][n][12] fp32 must be all-zero on first use; the call leaves it all-zero.
  * view_grad_stats [2][ldg] fp32 or NULL (NEXT f4, the ADC statistic of P:L154): plane 0 gets the sum
  * over this call's views v with tiles_touched[v][i] > 0 of ||dL/dPi(p_i)||_2 (pixel units), plane 1
@@ -179,6 +190,16 @@ steepgs_status steepgs_gauss_bwd_split(const float* params, int64_t ld, int64_t 
                                        int32_t V, const steepgs_raster_params* rp,
                                        float* moments_ws, float* grad_S, int64_t ldg, int32_t accumulate,
                                        const int32_t* tiles_touched, float* view_grad_stats, void* stream);
+
+/* NEXT f3 backward: call after steepgs_render_bwd_moments and before steepgs_gauss_bwd_split (which
+ * then takes accumulate | 4).  From the per-(view, Gaussian) colour gradient in moments_ws (left in
+ * place) through the clamp and the SH expansion: grad_S planes 11-13 = dL/d(DC coefficients), planes
+ * 0-2 = the view-direction part of dL/dp (pinhole), grad_sh [3 (K - 1)][ldg_sh] = dL/d(rest);
+ * written (accumulate 0, 2) or added (1) like the gradient planes of steepgs_gauss_bwd_split. */
+steepgs_status steepgs_sh_bwd(const float* params, int64_t ld, int64_t n, const float* sh_rest, int64_t ld_sh,
+                              int32_t sh_degree, const steepgs_camera* cams, int32_t V, const float* moments_ws,
+                              float* grad_S, int64_t ldg, float* grad_sh, int64_t ldg_sh, int32_t accumulate,
+                              void* stream);
 
 /* ---- a8: steepest density control (Thm 2; Alg. 1; eigen App. A.3
  * P:L584-604).  Per Gaussian: S_bar = S / denom; lambda_min by the trigonometric roots (fp32,
@@ -241,12 +262,23 @@ typedef struct {              /* hyper-parameters in fp64; the kernel rounds lr,
 steepgs_status steepgs_adam_step(float* params, int64_t ld, int64_t n, const float* grad_S, int64_t ldg,
                                  float* adam_m, float* adam_v, int64_t ldm, const steepgs_adam_params* ap,
                                  int64_t step, float* gacc, int32_t gacc_accumulate, void* stream);
-/* After a densify: zero the Adam moments (14 planes of m and v) of the replaced parents
+/* After a densify: zero the Adam moments (`planes` planes of m and v: 14 for the parameter planes,
+ * 3 (K - 1) for SH rest coefficients) of the replaced parents
  * (split_mask[i] == mask_value: 1 for steepgs_densify's mask, 2 for ADC splits in steepgs_densify_adc's
  * kind) and of the appended offspring [n, n + *n_split) — new Gaussians (Alg. 1, C20). */
 steepgs_status steepgs_reset_moments(float* adam_m, float* adam_v, int64_t ldm, int64_t n,
                                      const uint8_t* split_mask, const int64_t* n_split, int32_t mask_value,
-                                     void* stream);
+                                     int32_t planes, void* stream);
+
+/* Adam over `planes` dense planes with the single learning rate ap->lr[0] (SH rest coefficients,
+ * f3; 3DGS uses feature_lr / 20), same update and bias corrections as steepgs_adam_step. */
+steepgs_status steepgs_adam_step_planes(float* params, int64_t ld, int32_t planes, int64_t n, const float* grad,
+                                        int64_t ldg, float* adam_m, float* adam_v, int64_t ldm,
+                                        const steepgs_adam_params* ap, int64_t step, void* stream);
+/* After a densify: arr[:, dest_index[i]] = arr[:, i] for every parent with dest_index[i] >= 0 (extra
+ * per-Gaussian planes such as SH rest coefficients follow their parent into the appended slot). */
+steepgs_status steepgs_copy_offspring(float* arr, int64_t ld, int32_t planes, int64_t n, const int32_t* dest_index,
+                                      void* stream);
 
 /* Copy planes [first, first + count) of a planar [*][ld] fp32 array, columns [0, n), device to
  * device (cudaMemcpy2DAsync; no kernel).  Used to checkpoint / restore Gaussian sets. */

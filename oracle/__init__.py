@@ -43,6 +43,10 @@ class Raster(C.Structure):
                 ("dilation", C.c_double), ("bg", C.c_double * 3), ("tile", C.c_int32)]
 
 
+class SH(C.Structure):
+    _fields_ = [("rest", C.c_void_p), ("ld", C.c_int64), ("degree", C.c_int32)]
+
+
 class Split(C.Structure):
     _fields_ = [("index", C.c_int64), ("m", C.c_int32), ("w", C.c_double * 4), ("delta", (C.c_double * 3) * 4)]
 
@@ -66,7 +70,9 @@ def lib():
         L.orc_position_hessian.argtypes = [P, C.c_int64, C.c_int64, P, P, C.c_double, C.c_double, P]
         L.orc_render_view.restype = C.c_int64
         L.orc_render_view.argtypes = [P, C.c_int64, C.c_int64, P, P, P, P, C.c_int32, C.c_int32, C.c_int32,
-                                      C.c_int32, C.c_int32, P, P, P, P, P, P, P, P, P, P]
+                                      C.c_int32, C.c_int32, P, P, P, P, P, P, P, P, P, P, P, P]
+        L.orc_sh_basis.restype = None
+        L.orc_sh_basis.argtypes = [P, C.c_int32, P, P]
         L.orc_eig_sym3.restype = C.c_int
         L.orc_eig_sym3.argtypes = [P, P, P]
         L.orc_densify.restype = C.c_int64
@@ -141,10 +147,13 @@ def position_hessian(params, i: int, cam: dict, x: float, y: float, rp: dict | N
 
 
 def render(params, cam: dict, rp: dict | None = None, window=None, brute_force: bool = False,
-           dl_dimage=None, split: dict | None = None, decision: dict | None = None) -> dict:
+           dl_dimage=None, split: dict | None = None, decision: dict | None = None, sh_rest=None,
+           sh_degree: int | None = None) -> dict:
     """One view: image/T/n_comp/ambiguity over `window` = (x0, y0, w, h) (default: full image);
     with dl_dimage ([3][h][w] over the window) also grad[20][n] (14 param grads + 6 S planes),
-    absg[20][n], amb_g[n] and grad_mu[2][n] (dL/dPi(p), the ADC statistic's per-view gradient)."""
+    absg[20][n], amb_g[n] and grad_mu[2][n] (dL/dPi(p), the ADC statistic's per-view gradient).
+    sh_degree (0..3) with sh_rest [3 ((deg + 1)^2 - 1)][n]: SH colours (f3; DC = planes 11-13), and
+    with dl_dimage also grad_sh [3 ((deg + 1)^2 - 1)][n]."""
     p = f64(params)
     n = p.shape[1]
     if window is None:
@@ -163,15 +172,35 @@ def render(params, cam: dict, rp: dict | None = None, window=None, brute_force: 
         for j, (wj, dj) in enumerate(zip(split["w"], split["delta"])):
             sp.w[j] = float(wj)
             sp.delta[j][:] = [float(v) for v in dj]
+    shs = None
+    gsh = None
+    if sh_degree is not None:
+        K = (int(sh_degree) + 1) ** 2
+        rest = np.ascontiguousarray(np.zeros((max(3 * (K - 1), 1), n)) if sh_rest is None or K == 1
+                                    else np.asarray(sh_rest, dtype=np.float64)[:3 * (K - 1), :n])
+        shs = SH()
+        shs.rest, shs.ld, shs.degree = rest.ctypes.data, n, int(sh_degree)
+        if dl_dimage is not None:
+            gsh = np.zeros((max(3 * (K - 1), 1), n))
     c, r = camera(cam), raster(rp)
     pairs = lib().orc_render_view(_ptr(p), n, n, C.byref(c), C.byref(r), _ptr(d["visible"]), _ptr(d["key"]),
                                   x0, y0, w, h, int(brute_force), C.byref(sp) if sp is not None else None,
                                   _ptr(dl), _ptr(img), _ptr(T), _ptr(nc), _ptr(amb), _ptr(grad), _ptr(absg), _ptr(ambg),
-                                  _ptr(gmu))
+                                  _ptr(gmu), C.byref(shs) if shs is not None else None, _ptr(gsh))
     if pairs < 0:
         raise MemoryError("oracle render failed")
+    if gsh is not None and sh_degree == 0:
+        gsh = np.zeros((0, n))
     return dict(image=img, final_T=T, n_comp=nc, amb_px=amb, grad=grad, absg=absg, amb_g=ambg, grad_mu=gmu,
-                pairs=int(pairs), decision=d)
+                grad_sh=gsh, pairs=int(pairs), decision=d)
+
+
+def sh_basis(direction, degree: int = 3):
+    """(Y[16], dY[16][3]) of the real SH basis (3DGS ordering) at a unit direction."""
+    v = np.ascontiguousarray(np.asarray(direction, dtype=np.float64))
+    Y = np.zeros(16); dY = np.zeros(48)
+    lib().orc_sh_basis(_ptr(v), int(degree), _ptr(Y), _ptr(dY))
+    return Y, dY.reshape(16, 3)
 
 
 def eig_sym3(A) -> tuple[np.ndarray, np.ndarray]:

@@ -151,6 +151,10 @@ typedef struct {
   double mu[2], cov[3], conic[3], o, z, tau;
   double P[6];              /* 2x3, P = J W (P:L139 footnote) */
   double col[3];
+  int sh_k;                 /* 0: colour = rgb planes; else (degree + 1)^2 SH coefficients per channel */
+  double Y[16];             /* SH basis at the view direction */
+  double cmask[3];          /* 1 where the colour is not clamped at 0 */
+  double dcol_dp[3][3];     /* d colour_ch / d p_k through the view direction */
   double dcov[10][3];       /* d(cov xx, xy, yy)/d theta_k; k = p0..2, ls0..2, q0..3 */
   double dmu[2][3];         /* d mu / d p */
 } gproj;
@@ -201,9 +205,103 @@ static void sandwich2(const double* P, const double* A, double* out) {
   out[0] = c[0]; out[1] = 0.5 * (c[1] + c[2]); out[2] = c[3];
 }
 
+/* View-dependent colour (NEXT f3): real spherical harmonics of degree <= 3 in the 3DGS
+ * ordering and constants, colour = max(0, sum_k Y_k(dir) f_k + 1/2).  Y[k] and the partial
+ * derivatives dY[k][j] = dY_k / d dir_j of the polynomials (x, y, z = dir). */
+static const double SH_C0 = 0.28209479177387814, SH_C1 = 0.4886025119029199;
+static const double SH_C2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005,
+                                -1.0925484305920792, 0.5462742152960396};
+static const double SH_C3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658,
+                                0.3731763325901154, -0.4570457994644658, 1.445305721320277,
+                                -0.5900435899266435};
+
+static void sh_basis(const double* v, int deg, double* Y, double (*dY)[3]) {
+  const double x = v[0], y = v[1], z = v[2];
+  for (int k = 0; k < 16; ++k) { Y[k] = 0; dY[k][0] = dY[k][1] = dY[k][2] = 0; }
+  Y[0] = SH_C0;
+  if (deg < 1) return;
+  Y[1] = -SH_C1 * y; dY[1][1] = -SH_C1;
+  Y[2] = SH_C1 * z;  dY[2][2] = SH_C1;
+  Y[3] = -SH_C1 * x; dY[3][0] = -SH_C1;
+  if (deg < 2) return;
+  Y[4] = SH_C2[0] * x * y;                   dY[4][0] = SH_C2[0] * y; dY[4][1] = SH_C2[0] * x;
+  Y[5] = SH_C2[1] * y * z;                   dY[5][1] = SH_C2[1] * z; dY[5][2] = SH_C2[1] * y;
+  Y[6] = SH_C2[2] * (2 * z * z - x * x - y * y);
+  dY[6][0] = -2 * SH_C2[2] * x; dY[6][1] = -2 * SH_C2[2] * y; dY[6][2] = 4 * SH_C2[2] * z;
+  Y[7] = SH_C2[3] * x * z;                   dY[7][0] = SH_C2[3] * z; dY[7][2] = SH_C2[3] * x;
+  Y[8] = SH_C2[4] * (x * x - y * y);         dY[8][0] = 2 * SH_C2[4] * x; dY[8][1] = -2 * SH_C2[4] * y;
+  if (deg < 3) return;
+  Y[9] = SH_C3[0] * y * (3 * x * x - y * y);
+  dY[9][0] = 6 * SH_C3[0] * x * y; dY[9][1] = SH_C3[0] * (3 * x * x - 3 * y * y);
+  Y[10] = SH_C3[1] * x * y * z;
+  dY[10][0] = SH_C3[1] * y * z; dY[10][1] = SH_C3[1] * x * z; dY[10][2] = SH_C3[1] * x * y;
+  Y[11] = SH_C3[2] * y * (4 * z * z - x * x - y * y);
+  dY[11][0] = -2 * SH_C3[2] * x * y; dY[11][1] = SH_C3[2] * (4 * z * z - x * x - 3 * y * y);
+  dY[11][2] = 8 * SH_C3[2] * y * z;
+  Y[12] = SH_C3[3] * z * (2 * z * z - 3 * x * x - 3 * y * y);
+  dY[12][0] = -6 * SH_C3[3] * x * z; dY[12][1] = -6 * SH_C3[3] * y * z;
+  dY[12][2] = SH_C3[3] * (6 * z * z - 3 * x * x - 3 * y * y);
+  Y[13] = SH_C3[4] * x * (4 * z * z - x * x - y * y);
+  dY[13][0] = SH_C3[4] * (4 * z * z - 3 * x * x - y * y); dY[13][1] = -2 * SH_C3[4] * x * y;
+  dY[13][2] = 8 * SH_C3[4] * x * z;
+  Y[14] = SH_C3[5] * z * (x * x - y * y);
+  dY[14][0] = 2 * SH_C3[5] * x * z; dY[14][1] = -2 * SH_C3[5] * y * z; dY[14][2] = SH_C3[5] * (x * x - y * y);
+  Y[15] = SH_C3[6] * x * (x * x - 3 * y * y);
+  dY[15][0] = SH_C3[6] * (3 * x * x - 3 * y * y); dY[15][1] = -6 * SH_C3[6] * x * y;
+}
+
+void orc_sh_basis(const double* dir, int32_t degree, double* Y, double* dY) {
+  double d[16][3];
+  sh_basis(dir, degree, Y, d);
+  if (dY) for (int k = 0; k < 16; ++k) for (int j = 0; j < 3; ++j) dY[3 * k + j] = d[k][j];
+}
+
+/* colour of Gaussian i seen from `cam` (C1 / f3): view direction dir = (p - o)/|p - o| with the
+ * camera centre o = -R^T t (pinhole) or the camera axis R^T e_z (affine, no dependence on p). */
+static void sh_colour(const double* params, int64_t ld, int64_t i, const orc_sh* sh, const orc_camera* cam,
+                      const double* p, gproj* g, int want_jac) {
+  const double* W = cam->R;
+  double dir[3], r = 1.0;
+  if (cam->model == 0) {
+    double v[3];
+    for (int k = 0; k < 3; ++k) {
+      const double o = -(W[k] * cam->t[0] + W[3 + k] * cam->t[1] + W[6 + k] * cam->t[2]);
+      v[k] = p[k] - o;
+    }
+    r = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+    for (int k = 0; k < 3; ++k) dir[k] = v[k] / r;
+  } else {
+    for (int k = 0; k < 3; ++k) dir[k] = W[6 + k];
+  }
+  double dY[16][3];
+  sh_basis(dir, sh->degree, g->Y, dY);
+  g->sh_k = (sh->degree + 1) * (sh->degree + 1);
+  double f[16][3];
+  for (int ch = 0; ch < 3; ++ch) f[0][ch] = params[(11 + ch) * ld + i];
+  for (int k = 1; k < g->sh_k; ++k)
+    for (int ch = 0; ch < 3; ++ch) f[k][ch] = sh->rest[(int64_t)(3 * (k - 1) + ch) * sh->ld + i];
+  for (int ch = 0; ch < 3; ++ch) {
+    double raw = 0.5;
+    for (int k = 0; k < g->sh_k; ++k) raw += g->Y[k] * f[k][ch];
+    g->col[ch] = raw > 0 ? raw : 0.0;
+    g->cmask[ch] = raw > 0 ? 1.0 : 0.0;
+  }
+  for (int ch = 0; ch < 3; ++ch)
+    for (int m = 0; m < 3; ++m) g->dcol_dp[ch][m] = 0.0;
+  if (!want_jac || cam->model != 0) return;
+  /* d dir / d p = (I - dir dir^T) / r */
+  for (int ch = 0; ch < 3; ++ch) {
+    double gd[3] = {0, 0, 0};   /* d raw_ch / d dir */
+    for (int k = 1; k < g->sh_k; ++k)
+      for (int j = 0; j < 3; ++j) gd[j] += f[k][ch] * dY[k][j];
+    const double dot = gd[0] * dir[0] + gd[1] * dir[1] + gd[2] * dir[2];
+    for (int m = 0; m < 3; ++m) g->dcol_dp[ch][m] = g->cmask[ch] * (gd[m] - dot * dir[m]) / r;
+  }
+}
+
 /* Projection of Gaussian i with mean overridden by `pm` (NULL = own mean). */
 static void project_one(const double* params, int64_t ld, int64_t i, const orc_camera* cam,
-                        const orc_raster* rp, const double* pm, gproj* g, int want_jac) {
+                        const orc_raster* rp, const double* pm, gproj* g, int want_jac, const orc_sh* sh) {
   const double* W = cam->R;
   double p[3];
   for (int k = 0; k < 3; ++k) p[k] = pm ? pm[k] : params[k * ld + i];
@@ -252,7 +350,12 @@ static void project_one(const double* params, int64_t ld, int64_t i, const orc_c
   g->conic[0] = g->cov[2] / det; g->conic[1] = -g->cov[1] / det; g->conic[2] = g->cov[0] / det;
   g->o = sigmoid(params[10 * ld + i]);
   g->tau = (rp->alpha_min > 0) ? 2.0 * log(g->o / rp->alpha_min) : INFINITY;
-  for (int k = 0; k < 3; ++k) g->col[k] = params[(11 + k) * ld + i];
+  g->sh_k = 0;
+  if (sh) {
+    sh_colour(params, ld, i, sh, cam, p, g, want_jac);
+  } else {
+    for (int k = 0; k < 3; ++k) g->col[k] = params[(11 + k) * ld + i];
+  }
   if (!want_jac) return;
 
   /* d mu / d p = J W = P (mean path) */
@@ -330,7 +433,7 @@ void orc_project_f64(const double* params, int64_t ld, int64_t n, const orc_came
                      double* opacity, double* depth) {
   for (int64_t i = 0; i < n; ++i) {
     gproj g;
-    project_one(params, ld, i, cam, rp, NULL, &g, 0);
+    project_one(params, ld, i, cam, rp, NULL, &g, 0, NULL);
     if (mu) { mu[2 * i] = g.mu[0]; mu[2 * i + 1] = g.mu[1]; }
     if (cov2d) for (int k = 0; k < 3; ++k) cov2d[3 * i + k] = g.cov[k];
     if (conic) for (int k = 0; k < 3; ++k) conic[3 * i + k] = g.conic[k];
@@ -351,7 +454,7 @@ double orc_eval_sigma(const double* params, int64_t ld, int64_t i, const orc_cam
                       const orc_raster* rp, double x, double y) {
   gproj g;
   double d[2];
-  project_one(params, ld, i, cam, rp, NULL, &g, 0);
+  project_one(params, ld, i, cam, rp, NULL, &g, 0, NULL);
   return sigma_at(&g, x, y, d);
 }
 
@@ -375,7 +478,7 @@ void orc_position_hessian(const double* params, int64_t ld, int64_t i, const orc
                           const orc_raster* rp, double x, double y, double* H) {
   gproj g;
   double d[2];
-  project_one(params, ld, i, cam, rp, NULL, &g, 0);
+  project_one(params, ld, i, cam, rp, NULL, &g, 0, NULL);
   const double sigma = sigma_at(&g, x, y, d);
   hessian_pair(&g, sigma, d, H);
 }
@@ -424,7 +527,8 @@ int64_t orc_render_view(const double* params, int64_t ld, int64_t n, const orc_c
                         int32_t x0, int32_t y0, int32_t w, int32_t h, int32_t brute_force,
                         const orc_split* split, const double* dL_dimage,
                         double* image, double* final_T, int32_t* n_comp, uint8_t* amb_px,
-                        double* grad, double* absg, uint8_t* amb_g, double* grad_mu) {
+                        double* grad, double* absg, uint8_t* amb_g, double* grad_mu,
+                        const orc_sh* sh, double* grad_sh) {
   const int want_bwd = dL_dimage != NULL;
   /* Candidates: visible Gaussians (fp32 decision) whose alpha support can reach the window. */
   int64_t ncand = 0, cap = 1024;
@@ -435,7 +539,7 @@ int64_t orc_render_view(const double* params, int64_t ld, int64_t n, const orc_c
     for (int j = 0; j < split->m; ++j) {
       double pm[3];
       for (int k = 0; k < 3; ++k) pm[k] = params[k * ld + split->index] + split->delta[j][k];
-      project_one(params, ld, split->index, cam, rp, pm, &off[j], 0);
+      project_one(params, ld, split->index, cam, rp, pm, &off[j], 0, sh);
     }
   }
   for (int64_t i = 0; i < n; ++i) {
@@ -449,7 +553,7 @@ int64_t orc_render_view(const double* params, int64_t ld, int64_t n, const orc_c
     cand_t* c = &cand[ncand];
     c->gid = i;
     c->key = depth_key[i];
-    project_one(params, ld, i, cam, rp, NULL, &c->g, want_bwd);
+    project_one(params, ld, i, cam, rp, NULL, &c->g, want_bwd, sh);
     /* exact AABB of {d : d^T Q d <= tau} is |d_x| <= sqrt(tau cov_xx) (plus 1e-6 px) */
     const double ex = sqrt(c->g.tau * c->g.cov[0]) + 1e-6, ey = sqrt(c->g.tau * c->g.cov[2]) + 1e-6;
     c->bb[0] = c->g.mu[0] - ex; c->bb[1] = c->g.mu[0] + ex;
@@ -511,11 +615,16 @@ int64_t orc_render_view(const double* params, int64_t ld, int64_t n, const orc_c
 
   const int nthr = orc_num_threads();
   double* tacc = NULL;   /* per-thread [ncand][ACCW] accumulators (grad 20 + abs 20 + dL/dmu 2) */
+  double* tsh = NULL;    /* per-thread [ncand][45] SH rest-coefficient accumulators (f3) */
   uint8_t* tamb = NULL;
+  const int nrest = sh ? 3 * ((sh->degree + 1) * (sh->degree + 1) - 1) : 0;
   if (want_bwd) {
     tacc = (double*)calloc((size_t)nthr * (size_t)(ncand > 0 ? ncand : 1) * ACCW, sizeof(double));
     tamb = (uint8_t*)calloc((size_t)(ncand > 0 ? ncand : 1), 1);
-    if (!tacc || !tamb) { free(cand); free(start); free(list); free(tacc); free(tamb); return -1; }
+    if (nrest > 0) tsh = (double*)calloc((size_t)nthr * (size_t)(ncand > 0 ? ncand : 1) * 45, sizeof(double));
+    if (!tacc || !tamb || (nrest > 0 && !tsh)) {
+      free(cand); free(start); free(list); free(tacc); free(tamb); free(tsh); return -1;
+    }
   }
   int64_t total_comp = 0;
   const double amin = rp->alpha_min, amax = rp->alpha_max, tmin = rp->t_min;
@@ -528,6 +637,7 @@ int64_t orc_render_view(const double* params, int64_t ld, int64_t n, const orc_c
     const int tid = 0;
 #endif
     double* acc = want_bwd ? tacc + (size_t)tid * (size_t)ncand * ACCW : NULL;
+    double* ash = tsh ? tsh + (size_t)tid * (size_t)ncand * 45 : NULL;
     rec_t* recs = (rec_t*)malloc(sizeof(rec_t) * (size_t)(ncand > 0 ? ncand : 1));
 #pragma omp for schedule(static)
     for (int32_t ky = 0; ky < h; ++ky) {
@@ -593,6 +703,14 @@ int64_t orc_render_view(const double* params, int64_t ld, int64_t n, const orc_c
           }
           contrib[10] = ga * sg * (1.0 - g->o);                 /* d sigma / d logit */
           for (int ch = 0; ch < 3; ++ch) contrib[11 + ch] = rc->alpha * rc->T * dLdC[ch];
+          if (g->sh_k) {   /* f3: dL/dcolour -> SH coefficients (masked by the clamp) and the mean */
+            for (int ch = 0; ch < 3; ++ch) {
+              const double gc = contrib[11 + ch] * g->cmask[ch];
+              for (int k = 0; k < 3; ++k) contrib[k] += contrib[11 + ch] * g->dcol_dp[ch][k];
+              for (int k = 1; k < g->sh_k; ++k) ash[(size_t)rc->c * 45 + 3 * (k - 1) + ch] += gc * g->Y[k];
+              contrib[11 + ch] = gc * g->Y[0];
+            }
+          }
           double H[9];
           hessian_pair(g, sg, d, H);
           contrib[14] = ga * H[0]; contrib[15] = ga * H[1]; contrib[16] = ga * H[2];
@@ -616,11 +734,15 @@ int64_t orc_render_view(const double* params, int64_t ld, int64_t n, const orc_c
           if (absg) absg[k * ld + gi] += a[20 + k];
         }
         if (grad_mu) { grad_mu[gi] += a[40]; grad_mu[ld + gi] += a[41]; }
+        if (grad_sh && tsh) {
+          const double* b = tsh + ((size_t)t * (size_t)ncand + (size_t)c) * 45;
+          for (int k = 0; k < nrest; ++k) grad_sh[(int64_t)k * ld + gi] += b[k];
+        }
       }
       if (amb_g && tamb[c]) amb_g[gi] = 1;
     }
   }
-  free(tacc); free(tamb); free(cand); free(start); free(list);
+  free(tacc); free(tsh); free(tamb); free(cand); free(start); free(list);
   return total_comp;
 }
 

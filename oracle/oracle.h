@@ -49,6 +49,17 @@ typedef struct {               /* merged-slot split of one Gaussian
   double delta[4][3];          /* position offsets of the offspring */
 } orc_split;
 
+/* View-dependent SH colour (NEXT f3): the DC coefficients are parameter planes 11-13, the
+ * rest [3 ((degree + 1)^2 - 1)][ld] planes, plane 3 (k - 1) + ch = coefficient k of channel ch. */
+typedef struct {
+  const double* rest;
+  int64_t ld;
+  int32_t degree;              /* 0..3 */
+} orc_sh;
+/* Real SH basis (3DGS ordering / constants) at unit direction dir: Y[16] (zero above the degree),
+ * dY[16][3] (optional) = partial derivatives of the basis polynomials. */
+void orc_sh_basis(const double* dir, int32_t degree, double* Y, double* dY);
+
 /* fp32 decision chain: visibility, depth key, pixel rect [n][4] = jmin,jmax,
  * kmin,kmax (inclusive, -1 if culled), tiles_touched.  Returns number visible. */
 int64_t orc_decide_f32(const double* params, int64_t ld, int64_t n, const orc_camera* cam,
@@ -74,14 +85,17 @@ void orc_position_hessian(const double* params, int64_t ld, int64_t i, const orc
  * brute_force = 1: candidates = every visible Gaussian; 0: per-Gaussian fp64 AABB scatter.
  * amb_px[h][w] = 1 where some candidate sits within a rounding band of a threshold
  * (DESIGN.md §3.4).  split != NULL renders the merged-slot model (fwd only).  grad_mu (optional,
- * [2][ld]) += dL/dPi(p) of this view, the 2D-mean gradient ADC thresholds.
+ * [2][ld]) += dL/dPi(p) of this view, the 2D-mean gradient ADC thresholds.  sh != NULL:
+ * colours from spherical harmonics (f3); grad_sh [3 (K - 1)][ld] += the rest-coefficient gradients,
+ * grad planes 11-13 get the DC-coefficient gradients and planes 0-2 include the view-direction term.
  * Returns the number of composited pairs, or -1 on allocation failure. */
 int64_t orc_render_view(const double* params, int64_t ld, int64_t n, const orc_camera* cam,
                         const orc_raster* rp, const uint8_t* visible, const uint32_t* depth_key,
                         int32_t x0, int32_t y0, int32_t w, int32_t h, int32_t brute_force,
                         const orc_split* split, const double* dL_dimage,
                         double* image, double* final_T, int32_t* n_comp, uint8_t* amb_px,
-                        double* grad, double* absg, uint8_t* amb_g, double* grad_mu);
+                        double* grad, double* absg, uint8_t* amb_g, double* grad_mu,
+                        const orc_sh* sh, double* grad_sh);
 
 /* Symmetric 3x3 eigen-decomposition by cyclic Jacobi.  A = (xx,xy,xz,yy,yz,zz).
  * lam ascending; V columns are unit eigenvectors (V[3*r + c] = component r of vector c), each

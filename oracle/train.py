@@ -43,6 +43,15 @@ def adam_step(p, g, m, v, lr, beta1, beta2, eps, t):
     p -= lr_plane * m_hat / (np.sqrt(v_hat) + eps)
 
 
+def adam_step_dense(p, g, m, v, lr, beta1, beta2, eps, t):
+    """The same Adam step with one learning rate for every plane (SH rest coefficients, f3)."""
+    m *= beta1
+    m += (1.0 - beta1) * g
+    v *= beta2
+    v += (1.0 - beta2) * g * g
+    p -= lr * (m / (1.0 - beta1 ** t)) / (np.sqrt(v / (1.0 - beta2 ** t)) + eps)
+
+
 def is_densify_step(t: int, t_start: int, t_split: int) -> bool:
     return t >= t_start and (t - t_start) % t_split == 0
 
@@ -53,10 +62,12 @@ def window_restarts_after(t: int, t_start: int, t_split: int) -> bool:
 
 def train(params0, n0: int, capacity: int, batches, T: int, t_start: int, t_split: int, lr, beta1=0.9,
           beta2=0.999, eps=1e-15, rp=None, eps_split=-1e-6, eta=0.5, eps_grad=None, budget=None,
-          density="sdc", adc=None, normals=None):
+          density="sdc", adc=None, normals=None, sh_degree=None, sh_rest0=None, sh_lr=2.5e-3 / 20):
     """Run steps t = 1..T.  batches(t) -> (cams, targets [V][3][H][W]) for gradient steps.
     density = "adc": the 3DGS baseline (oracle/adc.py) with adc = dict(eps_adc, tau_adc, clone_step,
     scale_factor) and normals(t) -> [6][>=n] standard normals for that densify step.
+    sh_degree (f3): SH colours (DC = planes 11-13, rest [3 (K - 1)][n] from sh_rest0), the rest
+    coefficients trained by Adam with the single rate sh_lr and copied to offspring.
     Returns dict(params [14][n], n, n_split, lambda_min [n] and ||G / T_split|| [n] per densify step, loss per
     gradient step); for "adc" lambda_min holds the mean view-gradient statistic and g_norm ||Sigma||_2."""
     P = np.zeros((14, capacity))
@@ -69,6 +80,17 @@ def train(params0, n0: int, capacity: int, batches, T: int, t_start: int, t_spli
     st_cnt = np.zeros(capacity)
     n = n0
     opt_t = 0
+    nrest = 3 * ((sh_degree + 1) ** 2 - 1) if sh_degree is not None else 0
+    SHr = np.zeros((nrest, capacity)); mr = np.zeros((nrest, capacity)); vr = np.zeros((nrest, capacity))
+    if nrest:
+        SHr[:, :n0] = np.asarray(sh_rest0, dtype=np.float64)[:nrest, :n0]
+
+    def spawn_rest(dest, reset):
+        if nrest:
+            for i in np.flatnonzero(dest >= 0):
+                SHr[:, dest[i]] = SHr[:, i]
+            mr[:, reset] = 0.0
+            vr[:, reset] = 0.0
     splits, losses, lams, gnorms = [], [], [], []
     for t in range(1, T + 1):
         if is_densify_step(t, t_start, t_split) and density == "adc":
@@ -87,6 +109,7 @@ def train(params0, n0: int, capacity: int, batches, T: int, t_start: int, t_spli
             reset[n:n + ns] = True
             m[:, reset] = 0.0
             v[:, reset] = 0.0
+            spawn_rest(d["dest"], reset)
             n += ns
             splits.append(ns)
         elif is_densify_step(t, t_start, t_split):
@@ -106,28 +129,35 @@ def train(params0, n0: int, capacity: int, batches, T: int, t_start: int, t_spli
             reset[n:n + ns] = True
             m[:, reset] = 0.0
             v[:, reset] = 0.0
+            spawn_rest(d["dest"], reset)
             n += ns
             splits.append(ns)
         else:
             cams, targets = batches(t)
             V = len(cams)
             grad = np.zeros((20, n))
+            gsh = np.zeros((nrest, n))
+            shkw = dict(sh_rest=SHr[:, :n], sh_degree=sh_degree) if sh_degree is not None else {}
             loss = 0.0
             for k, cam in enumerate(cams):
-                fw = _render(P[:, :n], cam, rp)
+                fw = _render(P[:, :n], cam, rp, **shkw)
                 img = fw["image"]
                 H, W = img.shape[1:]
                 r = img - np.asarray(targets[k], dtype=np.float64)
                 scale = 1.0 / (3.0 * H * W * V)
                 loss += scale * np.abs(r).sum()
-                bw = _render(P[:, :n], cam, rp, dl_dimage=np.sign(r) * scale, decision=fw["decision"])
+                bw = _render(P[:, :n], cam, rp, dl_dimage=np.sign(r) * scale, decision=fw["decision"], **shkw)
                 grad += bw["grad"]
+                if nrest:
+                    gsh += bw["grad_sh"]
                 vis = fw["decision"]["visible"] != 0
                 st_sum[:n] += np.where(vis, np.hypot(bw["grad_mu"][0], bw["grad_mu"][1]), 0.0)
                 st_cnt[:n] += vis
             losses.append(loss)
             opt_t += 1
             adam_step(P[:, :n], grad[:14], m[:, :n], v[:, :n], lr, beta1, beta2, eps, opt_t)
+            if nrest:
+                adam_step_dense(SHr[:, :n], gsh, mr[:, :n], vr[:, :n], sh_lr, beta1, beta2, eps, opt_t)
             G[:, :n] += grad[0:3]
             S[:, :n] += grad[14:20]
         if window_restarts_after(t, t_start, t_split):
@@ -135,4 +165,5 @@ def train(params0, n0: int, capacity: int, batches, T: int, t_start: int, t_spli
             S[:] = 0.0
             st_sum[:] = 0.0
             st_cnt[:] = 0.0
-    return dict(params=P[:, :n].copy(), n=n, n_split=splits, loss=losses, lambda_min=lams, g_norm=gnorms)
+    return dict(params=P[:, :n].copy(), n=n, n_split=splits, loss=losses, lambda_min=lams, g_norm=gnorms,
+                sh_rest=SHr[:, :n].copy())

@@ -82,7 +82,11 @@ def lib():
             "steepgs_adc_workspace_size": [I64, P],
             "steepgs_densify_adc": [P, I64, I64, I64, P, I64, P, P, I64, P, P, P, P, P, P, C.c_size_t, P],
             "steepgs_adam_step": [P, I64, I64, P, I64, P, P, I64, P, I64, P, I32, P],
-            "steepgs_reset_moments": [P, P, I64, I64, P, P, I32, P],
+            "steepgs_reset_moments": [P, P, I64, I64, P, P, I32, I32, P],
+            "steepgs_project_sh": [P, I64, I64, P, I64, I32, P, I32, P, P, P, P, P, P],
+            "steepgs_sh_bwd": [P, I64, I64, P, I64, I32, P, I32, P, P, I64, P, I64, I32, P],
+            "steepgs_adam_step_planes": [P, I64, I32, I64, P, I64, P, P, I64, P, I64, P],
+            "steepgs_copy_offspring": [P, I64, I32, I64, P, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -249,7 +253,33 @@ def adam_step(params, n, grad_S, m, v, ap, step, gacc=None, gacc_accumulate=True
 
 def reset_moments(m, v, n, split_mask, n_split, mask_value=1, stream=None):
     _check("steepgs_reset_moments", lib().steepgs_reset_moments(ptr(m), ptr(v), m.shape[1], n, ptr(split_mask),
-                                                                ptr(n_split), int(mask_value), stream_ptr(stream)))
+                                                                ptr(n_split), int(mask_value), m.shape[0],
+                                                                stream_ptr(stream)))
+
+
+def project_sh(params, ld, n, sh_rest, sh_degree, cams_arr, V, rp, splats, depth_key, tile_rect, tiles_touched,
+               stream=None):
+    _check("steepgs_project_sh", lib().steepgs_project_sh(
+        ptr(params), ld, n, ptr(sh_rest), sh_rest.shape[1] if sh_rest is not None else 0, int(sh_degree), cams_arr, V,
+        C.byref(rp), ptr(splats), ptr(depth_key), ptr(tile_rect), ptr(tiles_touched), stream_ptr(stream)))
+
+
+def sh_bwd(params, n, sh_rest, sh_degree, cams_arr, V, moments, grad_S, grad_sh, accumulate, stream=None):
+    _check("steepgs_sh_bwd", lib().steepgs_sh_bwd(
+        ptr(params), params.shape[1], n, ptr(sh_rest), sh_rest.shape[1] if sh_rest is not None else 0, int(sh_degree),
+        cams_arr, V, ptr(moments), ptr(grad_S), grad_S.shape[1], ptr(grad_sh),
+        grad_sh.shape[1] if grad_sh is not None else 0, int(accumulate), stream_ptr(stream)))
+
+
+def adam_step_planes(params, n, grad, m, v, ap, step, stream=None):
+    _check("steepgs_adam_step_planes", lib().steepgs_adam_step_planes(
+        ptr(params), params.shape[1], params.shape[0], n, ptr(grad), grad.shape[1], ptr(m), ptr(v), m.shape[1],
+        C.byref(ap), int(step), stream_ptr(stream)))
+
+
+def copy_offspring(arr, n, dest_index, stream=None):
+    _check("steepgs_copy_offspring", lib().steepgs_copy_offspring(ptr(arr), arr.shape[1], arr.shape[0], n,
+                                                                  ptr(dest_index), stream_ptr(stream)))
 
 
 def launch_count() -> int:

@@ -109,9 +109,75 @@ steepgs_status steepgs_project(const float* params, int64_t ld, int64_t n, const
   if (n > 0 && (!params || !splats || !depth_key || !tile_rect || !tiles_touched))
     return fail(STEEPGS_ERR_INVALID_ARGUMENT, "null pointer");
   if (!aligned(splats, 16) || !aligned(tile_rect, 8)) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "misaligned output");
-  const cudaError_t e = launch_project(params, ld, n, pack, V, raster_k(rp), splats, depth_key, tile_rect,
-                                       tiles_touched, (cudaStream_t)stream);
+  const cudaError_t e = launch_project(params, ld, n, nullptr, 0, -1, pack, V, raster_k(rp), splats, depth_key,
+                                       tile_rect, tiles_touched, (cudaStream_t)stream);
   return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_project");
+}
+
+steepgs_status steepgs_project_sh(const float* params, int64_t ld, int64_t n, const float* sh_rest, int64_t ld_sh,
+                                  int32_t sh_degree, const steepgs_camera* cams, int32_t V,
+                                  const steepgs_raster_params* rp, steepgs_splat* splats, uint32_t* depth_key,
+                                  uint32_t* tile_rect, int32_t* tiles_touched, void* stream) {
+  steepgs_status s;
+  if ((s = device_ok()) != STEEPGS_OK) return s;
+  CamPack pack;
+  if ((s = check_views(cams, V, &pack)) != STEEPGS_OK) return s;
+  if ((s = check_raster(rp)) != STEEPGS_OK) return s;
+  if (n < 0 || ld < n) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "need 0 <= n <= ld");
+  if (sh_degree < 0 || sh_degree > 3) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "sh_degree must be 0..3");
+  if (sh_degree > 0 && n > 0 && (!sh_rest || ld_sh < n)) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "bad sh_rest");
+  if ((int64_t)V * n >= (1ll << 32)) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "V * n must be < 2^32");
+  if (n > 0 && (!params || !splats || !depth_key || !tile_rect || !tiles_touched))
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "null pointer");
+  if (!aligned(splats, 16) || !aligned(tile_rect, 8)) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "misaligned output");
+  const cudaError_t e = launch_project(params, ld, n, sh_rest, ld_sh, sh_degree, pack, V, raster_k(rp), splats,
+                                       depth_key, tile_rect, tiles_touched, (cudaStream_t)stream);
+  return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_project_sh");
+}
+
+steepgs_status steepgs_sh_bwd(const float* params, int64_t ld, int64_t n, const float* sh_rest, int64_t ld_sh,
+                              int32_t sh_degree, const steepgs_camera* cams, int32_t V, const float* moments_ws,
+                              float* grad_S, int64_t ldg, float* grad_sh, int64_t ldg_sh, int32_t accumulate,
+                              void* stream) {
+  steepgs_status s;
+  if ((s = device_ok()) != STEEPGS_OK) return s;
+  CamPack pack;
+  if ((s = check_views(cams, V, &pack)) != STEEPGS_OK) return s;
+  if (n < 0 || ld < n || ldg < n) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "need 0 <= n <= ld, ldg");
+  if (sh_degree < 0 || sh_degree > 3) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "sh_degree must be 0..3");
+  if (accumulate < 0 || accumulate > 2) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "accumulate must be 0, 1 or 2");
+  if (n > 0 && (!params || !moments_ws || !grad_S)) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "null pointer");
+  if (sh_degree > 0 && n > 0 && (!sh_rest || !grad_sh || ld_sh < n || ldg_sh < n))
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "bad sh_rest / grad_sh");
+  if (!aligned(moments_ws, 16)) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "moments_ws must be 16-byte aligned");
+  const cudaError_t e = launch_sh_bwd(params, ld, n, sh_rest, ld_sh, sh_degree, pack, V, moments_ws, grad_S, ldg,
+                                      grad_sh, ldg_sh, accumulate, (cudaStream_t)stream);
+  return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_sh_bwd");
+}
+
+steepgs_status steepgs_adam_step_planes(float* params, int64_t ld, int32_t planes, int64_t n, const float* grad,
+                                        int64_t ldg, float* adam_m, float* adam_v, int64_t ldm,
+                                        const steepgs_adam_params* ap, int64_t step, void* stream) {
+  steepgs_status s;
+  if ((s = device_ok()) != STEEPGS_OK) return s;
+  if (!ap || step < 1 || n < 0 || planes < 0 || ld < n || ldg < n || ldm < n || !(ap->beta1 >= 0.0 && ap->beta1 < 1.0) ||
+      !(ap->beta2 >= 0.0 && ap->beta2 < 1.0) || !(ap->eps > 0.0))
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "bad adam arguments");
+  if (n > 0 && planes > 0 && (!params || !grad || !adam_m || !adam_v))
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "null pointer");
+  const cudaError_t e = launch_adam_planes(params, ld, planes, n, grad, ldg, adam_m, adam_v, ldm, *ap, step,
+                                           (cudaStream_t)stream);
+  return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_adam_step_planes");
+}
+
+steepgs_status steepgs_copy_offspring(float* arr, int64_t ld, int32_t planes, int64_t n, const int32_t* dest_index,
+                                      void* stream) {
+  steepgs_status s;
+  if ((s = device_ok()) != STEEPGS_OK) return s;
+  if (n < 0 || planes < 0 || ld < n || (n > 0 && planes > 0 && (!arr || !dest_index)))
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "bad copy_offspring arguments");
+  const cudaError_t e = launch_copy_offspring(arr, ld, planes, n, dest_index, (cudaStream_t)stream);
+  return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_copy_offspring");
 }
 
 steepgs_status steepgs_bin_sort_workspace_size(int64_t n, int32_t V, int32_t width, int32_t height,
@@ -182,7 +248,8 @@ steepgs_status steepgs_render_bwd_split(const float* params, int64_t ld, int64_t
   if ((s = check_raster(rp)) != STEEPGS_OK) return s;
   if ((s = check_binning(b, V, cams)) != STEEPGS_OK) return s;
   if (n < 0 || ld < n || ldg < n) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "need 0 <= n <= ld, ldg");
-  if (accumulate < 0 || accumulate > 2) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "accumulate must be 0, 1 or 2");
+  if ((accumulate & ~7) || (accumulate & 3) == 3)
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "accumulate must be 0, 1 or 2 (| 4 after steepgs_sh_bwd)");
   if (view_grad_stats && n > 0 && !tiles_touched)
     return fail(STEEPGS_ERR_INVALID_ARGUMENT, "view_grad_stats needs tiles_touched");
   if (n > 0 && (!params || !splats || !final_T || !n_contrib || !dL_dimage || !moments_ws || !grad_S))
@@ -224,7 +291,8 @@ steepgs_status steepgs_gauss_bwd_split(const float* params, int64_t ld, int64_t 
   if ((s = check_views(cams, V, &pack)) != STEEPGS_OK) return s;
   if ((s = check_raster(rp)) != STEEPGS_OK) return s;
   if (n < 0 || ld < n || ldg < n) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "need 0 <= n <= ld, ldg");
-  if (accumulate < 0 || accumulate > 2) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "accumulate must be 0, 1 or 2");
+  if ((accumulate & ~7) || (accumulate & 3) == 3)
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "accumulate must be 0, 1 or 2 (| 4 after steepgs_sh_bwd)");
   if (view_grad_stats && n > 0 && !tiles_touched)
     return fail(STEEPGS_ERR_INVALID_ARGUMENT, "view_grad_stats needs tiles_touched");
   if (n > 0 && (!params || !moments_ws || !grad_S)) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "null pointer");
@@ -275,13 +343,13 @@ steepgs_status steepgs_adam_step(float* params, int64_t ld, int64_t n, const flo
 
 steepgs_status steepgs_reset_moments(float* adam_m, float* adam_v, int64_t ldm, int64_t n,
                                      const uint8_t* split_mask, const int64_t* n_split, int32_t mask_value,
-                                     void* stream) {
+                                     int32_t planes, void* stream) {
   steepgs_status s;
   if ((s = device_ok()) != STEEPGS_OK) return s;
   if (!adam_m || !adam_v || !n_split || n < 0 || ldm < n || (n > 0 && !split_mask) || mask_value < 1 ||
-      mask_value > 255)
+      mask_value > 255 || planes < 0)
     return fail(STEEPGS_ERR_INVALID_ARGUMENT, "bad reset_moments arguments");
-  const cudaError_t e = launch_reset_moments(adam_m, adam_v, ldm, n, split_mask, n_split, mask_value, ldm,
+  const cudaError_t e = launch_reset_moments(adam_m, adam_v, ldm, n, split_mask, n_split, mask_value, planes, ldm,
                                             (cudaStream_t)stream);
   return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_reset_moments");
 }

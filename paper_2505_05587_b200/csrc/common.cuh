@@ -31,9 +31,43 @@ void note_launch(int k = 1);
 cudaError_t check_launch(const char* what);
 
 // ---- launchers (one per .cu) ----
-cudaError_t launch_project(const float* params, int64_t ld, int64_t n, const CamPack& cams, int V,
-                           const RasterK& rk, steepgs_splat* splats, uint32_t* depth_key, uint32_t* tile_rect,
-                           int32_t* tiles_touched, cudaStream_t st);
+cudaError_t launch_project(const float* params, int64_t ld, int64_t n, const float* sh_rest, int64_t ld_sh,
+                           int sh_degree, const CamPack& cams, int V, const RasterK& rk, steepgs_splat* splats,
+                           uint32_t* depth_key, uint32_t* tile_rect, int32_t* tiles_touched, cudaStream_t st);
+cudaError_t launch_sh_bwd(const float* params, int64_t ld, int64_t n, const float* sh_rest, int64_t ld_sh,
+                          int sh_degree, const CamPack& cams, int V, const float* moments, float* grad_S,
+                          int64_t ldg, float* grad_sh, int64_t ldg_sh, int accumulate, cudaStream_t st);
+cudaError_t launch_adam_planes(float* params, int64_t ld, int planes, int64_t n, const float* grad, int64_t ldg,
+                               float* m, float* v, int64_t ldm, const steepgs_adam_params& ap, int64_t step,
+                               cudaStream_t st);
+cudaError_t launch_copy_offspring(float* arr, int64_t ld, int planes, int64_t n, const int32_t* dest,
+                                  cudaStream_t st);
+
+// Real spherical harmonics of degree <= D at unit direction d (3DGS ordering and constants; NEXT f3).
+template <int D>
+__device__ __forceinline__ void sh_basis(const float* d, float* Y) {
+  const float x = d[0], y = d[1], z = d[2];
+  Y[0] = 0.28209479177387814f;
+  if (D < 1) return;
+  Y[1] = -0.4886025119029199f * y;
+  Y[2] = 0.4886025119029199f * z;
+  Y[3] = -0.4886025119029199f * x;
+  if (D < 2) return;
+  const float xx = x * x, yy = y * y, zz = z * z;
+  Y[4] = 1.0925484305920792f * x * y;
+  Y[5] = -1.0925484305920792f * y * z;
+  Y[6] = 0.31539156525252005f * (2.0f * zz - xx - yy);
+  Y[7] = -1.0925484305920792f * x * z;
+  Y[8] = 0.5462742152960396f * (xx - yy);
+  if (D < 3) return;
+  Y[9] = -0.5900435899266435f * y * (3.0f * xx - yy);
+  Y[10] = 2.890611442640554f * x * y * z;
+  Y[11] = -0.4570457994644658f * y * (4.0f * zz - xx - yy);
+  Y[12] = 0.3731763325901154f * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+  Y[13] = -0.4570457994644658f * x * (4.0f * zz - xx - yy);
+  Y[14] = 1.445305721320277f * z * (xx - yy);
+  Y[15] = -0.5900435899266435f * x * (xx - 3.0f * yy);
+}
 
 struct SortWs;  // bin_sort workspace carve-up (sort.cu)
 size_t bin_sort_ws_bytes(int64_t n, int V, int tiles, int64_t max_instances);
@@ -62,7 +96,8 @@ cudaError_t launch_adam(float* params, int64_t ld, int64_t n, const float* grad,
                         int64_t ldm, const steepgs_adam_params& ap, int64_t step, float* gacc, int gacc_accumulate,
                         cudaStream_t st);
 cudaError_t launch_reset_moments(float* m, float* v, int64_t ldm, int64_t n, const uint8_t* mask,
-                                 const int64_t* n_split, int mask_value, int64_t capacity, cudaStream_t st);
+                                 const int64_t* n_split, int mask_value, int planes, int64_t capacity,
+                                 cudaStream_t st);
 
 size_t adc_ws_bytes(int64_t n);
 cudaError_t launch_adc(float* params, int64_t ld, int64_t n, int64_t capacity, float* grad_S, int64_t ldg,

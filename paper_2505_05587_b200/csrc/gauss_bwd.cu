@@ -198,16 +198,23 @@ __global__ void __launch_bounds__(128) k_gauss_bwd(const float* __restrict__ par
   out[11] = gc[0]; out[12] = gc[1]; out[13] = gc[2];
 #pragma unroll
   for (int k = 0; k < 6; ++k) out[14 + k] = S6[k];
-  // accumulate: 0 = overwrite all 20 planes, 1 = += all, 2 = overwrite the 14 gradient planes and
-  // += the 6 S planes (Alg. 1: per-step gradients for the optimizer, S summed over T_split steps)
-  const bool acc_g = accumulate == 1, acc_s = accumulate != 0;
+  // accumulate & 3: 0 = overwrite all 20 planes, 1 = += all, 2 = overwrite the 14 gradient planes and
+  // += the 6 S planes (Alg. 1: per-step gradients for the optimizer, S summed over T_split steps).
+  // accumulate & 4 (SH colour, f3): k_sh_bwd has written planes 0-2 (view-direction term) and 11-13
+  // (DC coefficients) for this call, so planes 0-2 are added to and 11-13 left alone.
+  const int mode = accumulate & 3;
+  const bool shm = (accumulate & 4) != 0;
+  const bool acc_g = mode == 1, acc_s = mode != 0;
 #pragma unroll
-  for (int k = 0; k < 14; ++k) grad_S[k * ldg + i] = acc_g ? grad_S[k * ldg + i] + out[k] : out[k];
+  for (int k = 0; k < 14; ++k) {
+    if (shm && k >= 11) continue;
+    grad_S[k * ldg + i] = (acc_g || (shm && k < 3)) ? grad_S[k * ldg + i] + out[k] : out[k];
+  }
 #pragma unroll
   for (int k = 14; k < 20; ++k) grad_S[k * ldg + i] = acc_s ? grad_S[k * ldg + i] + out[k] : out[k];
-  if (vstats) {   // same window semantics as S: accumulate = 0 opens a new window
-    vstats[i] = accumulate ? vstats[i] + vsum : vsum;
-    vstats[ldg + i] = accumulate ? vstats[ldg + i] + vcnt : vcnt;
+  if (vstats) {   // same window semantics as S: mode 0 opens a new window
+    vstats[i] = mode ? vstats[i] + vsum : vsum;
+    vstats[ldg + i] = mode ? vstats[ldg + i] + vcnt : vcnt;
   }
 }
 

@@ -37,12 +37,12 @@ __global__ void __launch_bounds__(256) k_adam(float* __restrict__ params, int64_
 
 __global__ void __launch_bounds__(256) k_reset_moments(float* __restrict__ m, float* __restrict__ v, int64_t ldm,
                                                        int64_t n, const uint8_t* __restrict__ mask,
-                                                       const int64_t* __restrict__ n_split, int mask_value) {
+                                                       const int64_t* __restrict__ n_split, int mask_value,
+                                                       int planes) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t end = n + *n_split;
   if (i >= end || (i < n && mask[i] != mask_value)) return;
-#pragma unroll
-  for (int k = 0; k < 14; ++k) {
+  for (int k = 0; k < planes; ++k) {
     m[k * ldm + i] = 0.0f;
     v[k * ldm + i] = 0.0f;
   }
@@ -69,9 +69,10 @@ cudaError_t launch_adam(float* params, int64_t ld, int64_t n, const float* grad,
 }
 
 cudaError_t launch_reset_moments(float* m, float* v, int64_t ldm, int64_t n, const uint8_t* mask,
-                                 const int64_t* n_split, int mask_value, int64_t capacity, cudaStream_t st) {
+                                 const int64_t* n_split, int mask_value, int planes, int64_t capacity,
+                                 cudaStream_t st) {
   if (capacity == 0) return cudaSuccess;
-  k_reset_moments<<<(unsigned)((capacity + 255) / 256), 256, 0, st>>>(m, v, ldm, n, mask, n_split, mask_value);
+  k_reset_moments<<<(unsigned)((capacity + 255) / 256), 256, 0, st>>>(m, v, ldm, n, mask, n_split, mask_value, planes);
   note_launch();
   return check_launch("k_reset_moments");
 }

@@ -36,7 +36,12 @@ __device__ __forceinline__ double drcp(double x) {
   return r;
 }
 
+// kSH = -1: colour = rgb planes 11-13; kSH = 0..3: view-dependent colour from real spherical harmonics
+// (NEXT f3): colour = max(0, sum_k Y_k(dir) f_k + 1/2), DC f_0 = planes 11-13, the rest from
+// sh_rest (plane 3 (k - 1) + ch), dir = (p - o)/|p - o| with o = -R^T t (pinhole) or R^T e_z (affine).
+template <int kSH>
 __global__ void __launch_bounds__(256) k_project(const float* __restrict__ params, int64_t ld, int64_t n,
+                                                 const float* __restrict__ sh_rest, int64_t ld_sh,
                                                  const CamPack cams, int V, const RasterK rk,
                                                  steepgs_splat* __restrict__ splats,
                                                  uint32_t* __restrict__ depth_key, uint2* __restrict__ tile_rect,
@@ -203,7 +208,30 @@ __global__ void __launch_bounds__(256) k_project(const float* __restrict__ param
     float4* s1 = reinterpret_cast<float4*>(sp) + 1;
     *s0 = make_double2(mx, my);
     s1[0] = make_float4((float)((a11 + dil) * sc), (float)(-2.0 * a01 * sc), (float)((a00 + dil) * sc), log2o);
-    s1[1] = make_float4(cr, cg, cb, o);
+    float col[3] = {cr, cg, cb};
+    if (kSH >= 0) {
+      float d[3];
+      if (c.model == 0) {
+        float v3[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) v3[k] = (k == 0 ? p0 : (k == 1 ? p1 : p2)) +
+                                             (R[k] * c.t[0] + R[3 + k] * c.t[1] + R[6 + k] * c.t[2]);
+        const float rn = rsqrtf(v3[0] * v3[0] + v3[1] * v3[1] + v3[2] * v3[2]);
+        d[0] = v3[0] * rn; d[1] = v3[1] * rn; d[2] = v3[2] * rn;
+      } else {
+        d[0] = R[6]; d[1] = R[7]; d[2] = R[8];
+      }
+      float Y[16];
+      sh_basis<kSH>(d, Y);
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) {
+        float raw = 0.5f + Y[0] * col[ch];
+#pragma unroll
+        for (int k = 1; k < (kSH + 1) * (kSH + 1); ++k) raw += Y[k] * __ldg(sh_rest + (int64_t)(3 * (k - 1) + ch) * ld_sh + i);
+        col[ch] = fmaxf(raw, 0.0f);
+      }
+    }
+    s1[1] = make_float4(col[0], col[1], col[2], o);
     s1[2] = make_float4(hx, hy, tau, 0.0f);
   }
 }
@@ -213,14 +241,23 @@ __global__ void __launch_bounds__(256) k_project(const float* __restrict__ param
 #undef SUB
 #undef DIV
 
-cudaError_t launch_project(const float* params, int64_t ld, int64_t n, const CamPack& cams, int V,
-                           const RasterK& rk, steepgs_splat* splats, uint32_t* depth_key, uint32_t* tile_rect,
-                           int32_t* tiles_touched, cudaStream_t st) {
+cudaError_t launch_project(const float* params, int64_t ld, int64_t n, const float* sh_rest, int64_t ld_sh,
+                           int sh_degree, const CamPack& cams, int V, const RasterK& rk, steepgs_splat* splats,
+                           uint32_t* depth_key, uint32_t* tile_rect, int32_t* tiles_touched, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   const int threads = 256;
   const unsigned blocks = (unsigned)((n + threads - 1) / threads);
-  k_project<<<blocks, threads, 0, st>>>(params, ld, n, cams, V, rk, splats, depth_key,
-                                        reinterpret_cast<uint2*>(tile_rect), tiles_touched);
+#define SGS_PROJECT(D)                                                                                     \
+  k_project<D><<<blocks, threads, 0, st>>>(params, ld, n, sh_rest, ld_sh, cams, V, rk, splats, depth_key, \
+                                           reinterpret_cast<uint2*>(tile_rect), tiles_touched)
+  switch (sh_degree) {
+    case 0: SGS_PROJECT(0); break;
+    case 1: SGS_PROJECT(1); break;
+    case 2: SGS_PROJECT(2); break;
+    case 3: SGS_PROJECT(3); break;
+    default: SGS_PROJECT(-1); break;
+  }
+#undef SGS_PROJECT
   note_launch();
   return check_launch("k_project");
 }

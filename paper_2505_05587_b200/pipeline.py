@@ -75,12 +75,19 @@ class Rasterizer:
         self._HW = HW
 
     # ---- a1 ----
-    def project(self, params: torch.Tensor, n: int, cams: list[dict]):
+    def project(self, params: torch.Tensor, n: int, cams: list[dict], sh_rest: torch.Tensor | None = None,
+                sh_degree: int | None = None):
+        """a1; with sh_degree (0..3) the colour comes from spherical harmonics (f3): DC = planes 11-13,
+        sh_rest [3 ((deg + 1)^2 - 1)][ld_sh]."""
         assert len(cams) == self.V and params.shape[0] == N_PLANES and n <= self.cap
         self.n = int(n)
         self.cams_arr = _lib.cameras(cams)
-        _lib.project(params, params.shape[1], self.n, self.cams_arr, self.V, self.rp, self.splats, self.depth_key,
-                     self.tile_rect, self.tiles_touched)
+        if sh_degree is None:
+            _lib.project(params, params.shape[1], self.n, self.cams_arr, self.V, self.rp, self.splats, self.depth_key,
+                         self.tile_rect, self.tiles_touched)
+        else:
+            _lib.project_sh(params, params.shape[1], self.n, sh_rest, sh_degree, self.cams_arr, self.V, self.rp,
+                            self.splats, self.depth_key, self.tile_rect, self.tiles_touched)
 
     # ---- a2 ----
     def bin_sort(self):
@@ -117,6 +124,12 @@ class Rasterizer:
         _lib.gauss_bwd_split(params, params.shape[1], self.n, self.cams_arr, self.V, self.rp,
                              self.moments, grad_S, grad_S.shape[1], accumulate,
                              self.tiles_touched if view_grad_stats is not None else None, view_grad_stats)
+
+    def sh_bwd(self, params: torch.Tensor, grad_S: torch.Tensor, sh_rest, sh_degree: int, grad_sh,
+               accumulate: int = 0):
+        """f3: SH colour backward (between render_bwd_moments and gauss_bwd(accumulate | 4))."""
+        _lib.sh_bwd(params, self.n, sh_rest, sh_degree, self.cams_arr, self.V, self.moments, grad_S, grad_sh,
+                    accumulate)
 
     # ---- a8 ----
     def densify(self, params: torch.Tensor, grad_S: torch.Tensor, n: int, capacity: int, eps_split=-1e-6, eta=0.5,
@@ -211,7 +224,8 @@ class Trainer:
 
     def __init__(self, params0: torch.Tensor, n: int, capacity: int, V: int, width: int, height: int,
                  raster: Raster | None = None, adam: Adam | None = None, schedule: Schedule | None = None,
-                 max_instances: int | None = None, group=None, seed: int = 0, normals_fn=None):
+                 max_instances: int | None = None, group=None, seed: int = 0, normals_fn=None,
+                 sh_degree: int | None = None, sh_rest0: torch.Tensor | None = None, sh_lr: float = 2.5e-3 / 20):
         require_cuda()
         self.cap, self.n = int(capacity), int(n)
         if self.n > self.cap:
@@ -230,7 +244,17 @@ class Trainer:
         self.normals_fn = normals_fn     # ADC: t -> [6][>= n] device normals; default: drawn on the device
         self.generator = torch.Generator(device=d)
         self.generator.manual_seed(seed)
+        self.sh_degree = sh_degree
+        self.sh_rest = self.grad_sh = self.m_sh = self.v_sh = None
+        if sh_degree is not None:
+            planes = 3 * ((sh_degree + 1) ** 2 - 1)
+            mk = lambda: torch.zeros(max(planes, 1), self.cap, dtype=torch.float32, device=d)[:planes]
+            self.sh_rest, self.grad_sh, self.m_sh, self.v_sh = mk(), mk(), mk(), mk()
+            if sh_rest0 is not None and planes > 0:
+                self.sh_rest[:, :self.n].copy_(sh_rest0[:planes, :self.n])
         self.adam = adam or Adam()
+        self.ap_sh = _lib.adam_params((sh_lr,) * 5, (adam or Adam()).beta1, (adam or Adam()).beta2,
+                                      (adam or Adam()).eps)
         self.ap = _lib.adam_params(self.adam.lr, self.adam.beta1, self.adam.beta2, self.adam.eps)
         self.sched = schedule or Schedule()
         self.group = group
@@ -261,17 +285,27 @@ class Trainer:
             info = self._densify(t)
         else:
             rz = self.rz
-            rz.project(self.params, self.n, cams)
+            sh = self.sh_degree is not None
+            rz.project(self.params, self.n, cams, self.sh_rest, self.sh_degree)
             rz.bin_sort()
             rz.render_fwd()
             count = 3 * rz._HW
             _lib.l1_grad(rz.image, targets, rz.V, count, 1.0 / (count * rz.V * self._world()), rz.dL, rz.loss)
             rz.render_bwd_moments()
-            rz.gauss_bwd(self.params, self.grad_S, accumulate=0 if self.fresh else 2, view_grad_stats=self.vstats)
+            mode = 0 if self.fresh else 2
+            if sh:
+                rz.sh_bwd(self.params, self.grad_S, self.sh_rest, self.sh_degree, self.grad_sh, mode)
+            rz.gauss_bwd(self.params, self.grad_S, accumulate=mode | (4 if sh else 0), view_grad_stats=self.vstats)
             self._allreduce_planes(0, N_PLANES)
+            if sh and self.grad_sh.shape[0] > 0 and self._world() > 1:
+                from .parallel import allreduce_planes
+                allreduce_planes(self.grad_sh, 0, self.grad_sh.shape[0], self.n, self.group)
             self.opt_steps += 1
             _lib.adam_step(self.params, self.n, self.grad_S, self.m, self.v, self.ap, self.opt_steps, self.gacc,
                            gacc_accumulate=not self.fresh)
+            if sh and self.grad_sh.shape[0] > 0:
+                _lib.adam_step_planes(self.sh_rest, self.n, self.grad_sh, self.m_sh, self.v_sh, self.ap_sh,
+                                      self.opt_steps)
             self.fresh = False
             info = dict(t=t, kind="grad")
         if self.sched.window_restarts_after(t):
@@ -304,6 +338,9 @@ class Trainer:
         if st != 0:
             raise _lib.SteepGSError("steepgs_densify", 3, f"capacity {self.cap} < {n} + {ns}")
         _lib.reset_moments(self.m, self.v, n, reset_mask, rz.n_split, reset_value)
+        if self.sh_rest is not None and self.sh_rest.shape[0] > 0:
+            _lib.copy_offspring(self.sh_rest, n, rz.dest_index)          # offspring inherit the SH rest
+            _lib.reset_moments(self.m_sh, self.v_sh, n, reset_mask, rz.n_split, reset_value)
         self.n = n + ns
         info = dict(t=t, kind="densify", n_before=n, n_split=ns)
         self.history.append(info)

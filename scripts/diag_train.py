@@ -14,11 +14,14 @@ p, cams, tg = synth.scene_for(cfg), synth.ring_cameras(8, 64, 64, 7), synth.targ
 def b(t):
     idx = [(2 * t + k) % 8 for k in range(2)]
     return [cams[i] for i in idx], tg[idx]
-for eps in (1e-8, 1e-15):
-    for T in (10, 16):
-        ora = train(p, 64, 4096, b, T=T, t_start=4, t_split=3, lr=LR, eps=eps, rp=SM, budget=16)
+variant = sys.argv[1] if len(sys.argv) > 1 else "budget"
+kw = dict(budget=16, eps_grad=None) if variant == "budget" else (dict(budget=None, eps_grad=1e-3) if variant == "gate"
+                                                                 else dict(budget=None, eps_grad=None))
+for eps in (1e-15,):
+    for T in (4, 6, 7, 9, 10):
+        ora = train(p, 64, 4096, b, T=T, t_start=4, t_split=3, lr=LR, eps=eps, rp=SM, **kw)
         tr = Trainer(torch.from_numpy(p).cuda(), 64, 4096, 2, 64, 64, raster_of(SM), Adam(LR, 0.9, 0.999, eps),
-                     Schedule(4, 3, -1e-6, 0.5, None, 16))
+                     Schedule(4, 3, -1e-6, 0.5, kw["eps_grad"], kw["budget"]))
         for t in range(1, T + 1):
             c, y = b(t)
             tr.step(c, torch.from_numpy(np.ascontiguousarray(y)).cuda())
@@ -27,4 +30,6 @@ for eps in (1e-8, 1e-15):
         if not ok:
             print(eps, T, "n mismatch", tr.n, ora["n"]); continue
         e = np.abs(got - ora["params"]) / np.asarray(LR)[GROUP][:, None]
-        print(f"eps={eps} T={T} n={tr.n} max err/lr per plane:", np.round(e.max(1), 5), "p99.9", np.quantile(e, 0.999))
+        k = np.unravel_index(np.argmax(e), e.shape)
+        print(f"eps={eps} T={T} n={tr.n} max err/lr per plane:", np.round(e.max(1), 5), "worst", k,
+              "p99.9", np.quantile(e, 0.999))

@@ -195,7 +195,10 @@ def test_training_loop_parity(orc, variant):
     ref = ora["params"]
     lr = np.asarray(LR)[GROUP][:, None]
     err = np.abs(got - ref)
-    tol = 5e-3 * lr + 1e-6 * np.abs(ref)     # measured worst: 7e-4 lr (scripts/diag_train.py)
+    # measured worst (scripts/diag_train.py): 1.5e-3 lr on non-position planes; positions up to 5e-3 lr
+    # because an offspring's displacement eps v_min amplifies S's fp32 error by ||S|| / eigengap
+    tol = 5e-3 * lr + 1e-6 * np.abs(ref)
+    tol[0:3] = 2e-2 * lr[0:3] + 1e-6 * np.abs(ref[0:3])
     if not (err <= tol).all():
         bad = np.argwhere(err > tol)
         raise AssertionError(f"{len(bad)} params off; worst {(err / tol).max():.3g} x tol at {bad[:5].tolist()}")

@@ -160,6 +160,17 @@ steepgs_status steepgs_render_fwd(const steepgs_splat* splats, int64_t n, const 
 steepgs_status steepgs_l1_grad(const float* image, const float* target, int32_t V, int64_t count,
                                float scale, float* dL_dimage, float* loss, void* stream);
 
+/* NEXT f3: the 3DGS photometric loss with the SSIM term (P:L150 footnote), per view
+ *   loss[v] = (1 - lambda) mean |C - C_hat| + lambda (1 - SSIM(C, C_hat))   (3DGS: lambda = 0.2),
+ * SSIM = mean over [3][H][W] of the SSIM map (11x11 Gaussian window, sigma 1.5, zero padding,
+ * C1 = 0.01^2, C2 = 0.03^2); dL_dimage = scale * d loss[v] / d image (scale = 1/V for a batch
+ * mean).  image, target, dL_dimage [V][3][H][W]; loss [V] device or NULL; workspace >=
+ * steepgs_loss_workspace_size(V, H, W) bytes (SSIM partial maps + per-view sums). */
+steepgs_status steepgs_loss_workspace_size(int32_t V, int32_t height, int32_t width, size_t* bytes /*[host]*/);
+steepgs_status steepgs_l1_ssim_grad(const float* image, const float* target, int32_t V, int32_t height, int32_t width,
+                                    float lambda_ssim, float scale, float* dL_dimage, float* loss, void* workspace,
+                                    size_t ws_bytes, void* stream);
+
 /* ---- a5 + a6: backward with the splitting matrix (Thm 1; S per P:L356-358; Alg. 1
  * P:L537-538).  Replays each pixel back to front, accumulates per (view, Gaussian) 9 moments of
  * w = dL/dsigma * sigma (sum w, sum w d, sum w d d^T, sum alpha T dL/dC) into moments_ws, then per

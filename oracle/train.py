@@ -26,6 +26,7 @@ import numpy as np
 from . import densify as _densify
 from . import render as _render
 from .adc import adc_densify
+from .ssim import loss_and_grad as ssim_loss_and_grad
 
 # plane -> parameter group (mean, log-scale, quaternion, opacity logit, rgb)
 PLANE_GROUP = np.array([0, 0, 0, 1, 1, 1, 2, 2, 2, 2, 3, 4, 4, 4])
@@ -62,12 +63,14 @@ def window_restarts_after(t: int, t_start: int, t_split: int) -> bool:
 
 def train(params0, n0: int, capacity: int, batches, T: int, t_start: int, t_split: int, lr, beta1=0.9,
           beta2=0.999, eps=1e-15, rp=None, eps_split=-1e-6, eta=0.5, eps_grad=None, budget=None,
-          density="sdc", adc=None, normals=None, sh_degree=None, sh_rest0=None, sh_lr=2.5e-3 / 20):
+          density="sdc", adc=None, normals=None, sh_degree=None, sh_rest0=None, sh_lr=2.5e-3 / 20,
+          ssim_lambda=None):
     """Run steps t = 1..T.  batches(t) -> (cams, targets [V][3][H][W]) for gradient steps.
     density = "adc": the 3DGS baseline (oracle/adc.py) with adc = dict(eps_adc, tau_adc, clone_step,
     scale_factor) and normals(t) -> [6][>=n] standard normals for that densify step.
     sh_degree (f3): SH colours (DC = planes 11-13, rest [3 (K - 1)][n] from sh_rest0), the rest
     coefficients trained by Adam with the single rate sh_lr and copied to offspring.
+    ssim_lambda (f3): per-view loss (1 - lambda) l1 + lambda (1 - SSIM) (oracle/ssim.py), batch mean.
     Returns dict(params [14][n], n, n_split, lambda_min [n] and ||G / T_split|| [n] per densify step, loss per
     gradient step); for "adc" lambda_min holds the mean view-gradient statistic and g_norm ||Sigma||_2."""
     P = np.zeros((14, capacity))
@@ -145,8 +148,14 @@ def train(params0, n0: int, capacity: int, batches, T: int, t_start: int, t_spli
                 H, W = img.shape[1:]
                 r = img - np.asarray(targets[k], dtype=np.float64)
                 scale = 1.0 / (3.0 * H * W * V)
-                loss += scale * np.abs(r).sum()
-                bw = _render(P[:, :n], cam, rp, dl_dimage=np.sign(r) * scale, decision=fw["decision"], **shkw)
+                if ssim_lambda is None:
+                    loss += scale * np.abs(r).sum()
+                    dl = np.sign(r) * scale
+                else:
+                    lv, gv = ssim_loss_and_grad(img, targets[k], ssim_lambda)
+                    loss += lv / V
+                    dl = gv / V
+                bw = _render(P[:, :n], cam, rp, dl_dimage=dl, decision=fw["decision"], **shkw)
                 grad += bw["grad"]
                 if nrest:
                     gsh += bw["grad_sh"]

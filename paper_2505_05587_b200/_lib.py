@@ -87,6 +87,8 @@ def lib():
             "steepgs_sh_bwd": [P, I64, I64, P, I64, I32, P, I32, P, P, I64, P, I64, I32, P],
             "steepgs_adam_step_planes": [P, I64, I32, I64, P, I64, P, P, I64, P, I64, P],
             "steepgs_copy_offspring": [P, I64, I32, I64, P, P],
+            "steepgs_loss_workspace_size": [I32, I32, I32, P],
+            "steepgs_l1_ssim_grad": [P, P, I32, I32, I32, F, F, P, P, P, C.c_size_t, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -275,6 +277,19 @@ def adam_step_planes(params, n, grad, m, v, ap, step, stream=None):
     _check("steepgs_adam_step_planes", lib().steepgs_adam_step_planes(
         ptr(params), params.shape[1], params.shape[0], n, ptr(grad), grad.shape[1], ptr(m), ptr(v), m.shape[1],
         C.byref(ap), int(step), stream_ptr(stream)))
+
+
+def loss_workspace_size(V, H, W) -> int:
+    out = C.c_size_t(0)
+    _check("steepgs_loss_workspace_size", lib().steepgs_loss_workspace_size(V, H, W, C.byref(out)))
+    return int(out.value)
+
+
+def l1_ssim_grad(image, target, lam, scale, dL, loss, ws, stream=None):
+    V, _, H, W = image.shape
+    _check("steepgs_l1_ssim_grad", lib().steepgs_l1_ssim_grad(ptr(image), ptr(target), V, H, W, float(lam), float(scale),
+                                                              ptr(dL), ptr(loss), ptr(ws), ws.numel() * ws.element_size(),
+                                                              stream_ptr(stream)))
 
 
 def copy_offspring(arr, n, dest_index, stream=None):

@@ -170,6 +170,27 @@ steepgs_status steepgs_adam_step_planes(float* params, int64_t ld, int32_t plane
   return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_adam_step_planes");
 }
 
+steepgs_status steepgs_loss_workspace_size(int32_t V, int32_t height, int32_t width, size_t* bytes) {
+  if (!bytes || V < 1 || V > kMaxViews || height <= 0 || width <= 0)
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "bad arguments");
+  *bytes = loss_ws_bytes(V, height, width);
+  return STEEPGS_OK;
+}
+
+steepgs_status steepgs_l1_ssim_grad(const float* image, const float* target, int32_t V, int32_t height, int32_t width,
+                                    float lambda_ssim, float scale, float* dL_dimage, float* loss, void* workspace,
+                                    size_t ws_bytes, void* stream) {
+  steepgs_status s;
+  if ((s = device_ok()) != STEEPGS_OK) return s;
+  if (V < 1 || V > kMaxViews || height <= 0 || width <= 0 || !(lambda_ssim >= 0.f && lambda_ssim <= 1.f))
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "need 1 <= V <= 64, H, W > 0, 0 <= lambda <= 1");
+  if (!image || !target || !dL_dimage || !workspace) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "null pointer");
+  if (ws_bytes < loss_ws_bytes(V, height, width)) return fail(STEEPGS_ERR_WORKSPACE_TOO_SMALL, "loss workspace");
+  const cudaError_t e = launch_ssim_loss(image, target, V, height, width, lambda_ssim, scale, dL_dimage, loss,
+                                         workspace, (cudaStream_t)stream);
+  return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_l1_ssim_grad");
+}
+
 steepgs_status steepgs_copy_offspring(float* arr, int64_t ld, int32_t planes, int64_t n, const int32_t* dest_index,
                                       void* stream) {
   steepgs_status s;

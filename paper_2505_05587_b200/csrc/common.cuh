@@ -40,6 +40,9 @@ cudaError_t launch_sh_bwd(const float* params, int64_t ld, int64_t n, const floa
 cudaError_t launch_adam_planes(float* params, int64_t ld, int planes, int64_t n, const float* grad, int64_t ldg,
                                float* m, float* v, int64_t ldm, const steepgs_adam_params& ap, int64_t step,
                                cudaStream_t st);
+size_t loss_ws_bytes(int V, int H, int W);
+cudaError_t launch_ssim_loss(const float* image, const float* target, int V, int H, int W, float lam, float scale,
+                             float* dL, float* loss, void* ws, cudaStream_t st);
 cudaError_t launch_copy_offspring(float* arr, int64_t ld, int planes, int64_t n, const int32_t* dest,
                                   cudaStream_t st);
 

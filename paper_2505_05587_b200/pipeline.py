@@ -225,7 +225,8 @@ class Trainer:
     def __init__(self, params0: torch.Tensor, n: int, capacity: int, V: int, width: int, height: int,
                  raster: Raster | None = None, adam: Adam | None = None, schedule: Schedule | None = None,
                  max_instances: int | None = None, group=None, seed: int = 0, normals_fn=None,
-                 sh_degree: int | None = None, sh_rest0: torch.Tensor | None = None, sh_lr: float = 2.5e-3 / 20):
+                 sh_degree: int | None = None, sh_rest0: torch.Tensor | None = None, sh_lr: float = 2.5e-3 / 20,
+                 ssim_lambda: float | None = None):
         require_cuda()
         self.cap, self.n = int(capacity), int(n)
         if self.n > self.cap:
@@ -252,6 +253,10 @@ class Trainer:
             self.sh_rest, self.grad_sh, self.m_sh, self.v_sh = mk(), mk(), mk(), mk()
             if sh_rest0 is not None and planes > 0:
                 self.sh_rest[:, :self.n].copy_(sh_rest0[:planes, :self.n])
+        self.ssim_lambda = ssim_lambda   # None: l1 loss; else (1 - lambda) l1 + lambda (1 - SSIM) (3DGS: 0.2)
+        self.loss_ws = None
+        if ssim_lambda is not None:
+            self.loss_ws = torch.empty(_lib.loss_workspace_size(V, height, width), dtype=torch.uint8, device=d)
         self.adam = adam or Adam()
         self.ap_sh = _lib.adam_params((sh_lr,) * 5, (adam or Adam()).beta1, (adam or Adam()).beta2,
                                       (adam or Adam()).eps)
@@ -290,7 +295,11 @@ class Trainer:
             rz.bin_sort()
             rz.render_fwd()
             count = 3 * rz._HW
-            _lib.l1_grad(rz.image, targets, rz.V, count, 1.0 / (count * rz.V * self._world()), rz.dL, rz.loss)
+            if self.ssim_lambda is None:
+                _lib.l1_grad(rz.image, targets, rz.V, count, 1.0 / (count * rz.V * self._world()), rz.dL, rz.loss)
+            else:
+                _lib.l1_ssim_grad(rz.image, targets, self.ssim_lambda, 1.0 / (rz.V * self._world()), rz.dL, rz.loss,
+                                  self.loss_ws)
             rz.render_bwd_moments()
             mode = 0 if self.fresh else 2
             if sh:

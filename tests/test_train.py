@@ -157,7 +157,7 @@ def _batches(cams, tg, V=2):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("variant", ["plain", "budget", "gate"])
+@pytest.mark.parametrize("variant", ["plain", "budget", "gate", "ssim"])
 def test_training_loop_parity(orc, variant):
     """The Trainer (C1 scene, 2 views per step, densify at steps 4, 7, 10) against oracle/train.py:
     split counts bit-exact, parameters within the tolerance of DESIGN.md §3.4 (f1)."""
@@ -172,7 +172,9 @@ def test_training_loop_parity(orc, variant):
     elif variant == "gate":
         kw["eps_grad"] = 1e-3
     T, t_start, t_split, cap, eps = 10, 4, 3, 512, 1e-15     # 3DGS's Adam eps
-    ora = train(p, 64, cap, _batches(cams, tg), T=T, t_start=t_start, t_split=t_split, lr=LR, eps=eps, rp=SMOOTH, **kw)
+    ssim_lam = 0.2 if variant == "ssim" else None
+    ora = train(p, 64, cap, _batches(cams, tg), T=T, t_start=t_start, t_split=t_split, lr=LR, eps=eps, rp=SMOOTH,
+                ssim_lambda=ssim_lam, **kw)
     # the comparison is only decisive when no oracle decision sits within the fp32 noise of its threshold
     for lam, gn in zip(ora["lambda_min"], ora["g_norm"]):
         scale = np.abs(lam).max()
@@ -183,7 +185,7 @@ def test_training_loop_parity(orc, variant):
             srt = np.sort(lam)
             assert srt[15] < -1e-6 and srt[16] - srt[15] > 1e-4 * scale
     tr = Trainer(torch.from_numpy(p).cuda(), 64, cap, 2, 64, 64, raster_of(SMOOTH), Adam(LR, 0.9, 0.999, eps),
-                 Schedule(t_start, t_split, -1e-6, 0.5, kw["eps_grad"], kw["budget"]))
+                 Schedule(t_start, t_split, -1e-6, 0.5, kw["eps_grad"], kw["budget"]), ssim_lambda=ssim_lam)
     b = _batches(cams, tg)
     for t in range(1, T + 1):
         c, y = b(t)

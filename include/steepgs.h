@@ -70,6 +70,9 @@ typedef struct {
  * accumulated views/steps (S_bar = S / denom), must be > 0.
  * gate = 1: the "compactest" variant (App. A.2): a Gaussian is split only if also
  *   ||G_p / denom||_2 <= eps_grad, G_p = the accumulated position-gradient planes 0-2 (Z12, Z21).
+ * gate = 2: Alg. 1's "condition on G" read as 3DGS's densification condition (C24): split
+ *   only if grad_S[0][i] / grad_S[1][i] >= eps_grad, planes 0, 1 holding the view_grad_stats of
+ *   steepgs_gauss_bwd_split (sum of ||dL/dPi(p)|| over visible views, their count).
  * budget >= 0: "densification with increment budget" (App. A.2): of the Gaussians
  *   that pass the rule, split at most `budget`, those with the least lambda_min (ties: lower
  *   index first); budget < 0: unlimited. */

@@ -215,15 +215,17 @@ def eig_sym3(A) -> tuple[np.ndarray, np.ndarray]:
 
 
 def densify(params, acc, n: int, capacity: int, denom: float = 1.0, eps_split: float = -1e-6,
-            eta: float = 0.5, eps_abs: float = 0.0, eps_grad: float | None = None, budget: int | None = None) -> dict:
+            eta: float = 0.5, eps_abs: float = 0.0, eps_grad: float | None = None, budget: int | None = None,
+            grad_gate: float | None = None) -> dict:
     """In-place SDC densify on float64 copies.  params [14][cap], acc [20][cap].  eps_grad: compactest
     gate; budget: increment budget (App. A.2)."""
     p = np.ascontiguousarray(np.array(params, dtype=np.float64))
     a = np.ascontiguousarray(np.array(acc, dtype=np.float64))
     ld, ldg = p.shape[1], a.shape[1]
     mask = np.zeros(n, np.uint8); dest = np.zeros(n, np.int32); lam = np.zeros(n)
-    ns = lib().orc_densify(_ptr(p), ld, n, capacity, _ptr(a), ldg, denom, eps_split, eta, eps_abs,
-                           0 if eps_grad is None else 1, 0.0 if eps_grad is None else float(eps_grad),
+    gate, eg = (2, float(grad_gate)) if grad_gate is not None else ((0, 0.0) if eps_grad is None
+                                                                     else (1, float(eps_grad)))
+    ns = lib().orc_densify(_ptr(p), ld, n, capacity, _ptr(a), ldg, denom, eps_split, eta, eps_abs, gate, eg,
                            -1 if budget is None else int(budget), _ptr(mask), _ptr(dest), _ptr(lam))
     return dict(params=p, acc=a, mask=mask, dest=dest, lambda_min=lam, n_split=int(ns))
 

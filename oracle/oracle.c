@@ -834,10 +834,13 @@ int64_t orc_densify(double* params, int64_t ld, int64_t n, int64_t capacity, dou
     lam0[i] = lam[0];
     for (int k = 0; k < 3; ++k) vmin[3 * i + k] = V[3 * k + 0];
     int split = lam[0] < eps_split;                                            /* P:L545, Z11 */
-    if (split && gate) {
+    if (split && gate == 1) {
       double g2 = 0;
       for (int k = 0; k < 3; ++k) { const double g = acc[k * ldg + i] / denom; g2 += g * g; }
       split = sqrt(g2) <= eps_grad;
+    } else if (split && gate == 2) {          /* Alg. 1 "condition on G" as 3DGS's (C24) */
+      const double cnt = acc[1 * ldg + i];
+      split = cnt > 0 && acc[0 * ldg + i] / cnt >= eps_grad;
     }
     mask[i] = (uint8_t)split;
     ncand += split;

@@ -104,7 +104,9 @@ int64_t orc_render_view(const double* params, int64_t ld, int64_t n, const orc_c
 int orc_eig_sym3(const double* A, double* lam, double* V);
 
 /* SDC densify (Thm 2, Alg. 1) on fp64 planes, in place.  Variants of App. A.2:
- * gate = 1 also requires ||acc[0..2] / denom||_2 <= eps_grad (compactest); budget >= 0
+ * gate = 1 also requires ||acc[0..2] / denom||_2 <= eps_grad (compactest); gate = 2
+ * requires acc[0] / acc[1] >= eps_grad (Alg. 1's "condition on G" read as 3DGS's mean view-space
+ * gradient-norm threshold, acc[0] = sum of norms, acc[1] = visible views; C24); budget >= 0
  * keeps at most `budget` splits, those with the least lambda_min, ties by index.
  * S planes are read from
  * acc[14..19][ld].  Offspring A in slot i (p + eps v), B in slot n + rank (p - eps v), both with

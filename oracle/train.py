@@ -64,13 +64,14 @@ def window_restarts_after(t: int, t_start: int, t_split: int) -> bool:
 def train(params0, n0: int, capacity: int, batches, T: int, t_start: int, t_split: int, lr, beta1=0.9,
           beta2=0.999, eps=1e-15, rp=None, eps_split=-1e-6, eta=0.5, eps_grad=None, budget=None,
           density="sdc", adc=None, normals=None, sh_degree=None, sh_rest0=None, sh_lr=2.5e-3 / 20,
-          ssim_lambda=None):
+          ssim_lambda=None, grad_gate=None):
     """Run steps t = 1..T.  batches(t) -> (cams, targets [V][3][H][W]) for gradient steps.
     density = "adc": the 3DGS baseline (oracle/adc.py) with adc = dict(eps_adc, tau_adc, clone_step,
     scale_factor) and normals(t) -> [6][>=n] standard normals for that densify step.
     sh_degree (f3): SH colours (DC = planes 11-13, rest [3 (K - 1)][n] from sh_rest0), the rest
     coefficients trained by Adam with the single rate sh_lr and copied to offspring.
     ssim_lambda (f3): per-view loss (1 - lambda) l1 + lambda (1 - SSIM) (oracle/ssim.py), batch mean.
+    grad_gate (C24): SDC splits only Gaussians whose mean view-space gradient norm >= grad_gate.
     Returns dict(params [14][n], n, n_split, lambda_min [n] and ||G / T_split|| [n] per densify step, loss per
     gradient step); for "adc" lambda_min holds the mean view-gradient statistic and g_norm ||Sigma||_2."""
     P = np.zeros((14, capacity))
@@ -118,13 +119,19 @@ def train(params0, n0: int, capacity: int, batches, T: int, t_start: int, t_spli
         elif is_densify_step(t, t_start, t_split):
             acc = np.zeros((20, capacity))
             acc[0:3] = G
+            if grad_gate is not None:       # Alg. 1's condition on G as 3DGS's statistic (C24)
+                acc[0], acc[1], acc[2] = st_sum, st_cnt, 0.0
             acc[14:20] = S
             d = _densify(P, acc, n, capacity, denom=float(t_split), eps_split=eps_split, eta=eta,
-                         eps_grad=eps_grad, budget=budget)
+                         eps_grad=eps_grad, budget=budget, grad_gate=grad_gate)
             if d["n_split"] < 0:
                 raise RuntimeError("capacity exceeded")
             lams.append(d["lambda_min"].copy())
-            gnorms.append(np.linalg.norm(G[:, :n], axis=0) / t_split)
+            if grad_gate is not None:
+                with np.errstate(invalid="ignore", divide="ignore"):
+                    gnorms.append(np.where(st_cnt[:n] > 0, st_sum[:n] / st_cnt[:n], 0.0))
+            else:
+                gnorms.append(np.linalg.norm(G[:, :n], axis=0) / t_split)
             P = d["params"]
             ns = d["n_split"]
             reset = np.zeros(capacity, bool)

@@ -138,10 +138,14 @@ def raster_params(alpha_min=1.0 / 255.0, alpha_max=0.99, t_min=1e-4, dilation=0.
     return r
 
 
-def densify_params(eps_split=-1e-6, eta=0.5, eps_abs=0.0, denom=1.0, eps_grad=None, budget=None):
+def densify_params(eps_split=-1e-6, eta=0.5, eps_abs=0.0, denom=1.0, eps_grad=None, budget=None, grad_gate=None):
+    """eps_grad: compactest gate (gate 1); grad_gate: 3DGS-style view-gradient condition (gate 2)."""
     d = DensifyParams()
     d.eps_split, d.eta, d.eps_abs, d.denom = eps_split, eta, eps_abs, denom
-    d.gate, d.eps_grad = (0, 0.0) if eps_grad is None else (1, float(eps_grad))
+    if grad_gate is not None:
+        d.gate, d.eps_grad = 2, float(grad_gate)
+    else:
+        d.gate, d.eps_grad = (0, 0.0) if eps_grad is None else (1, float(eps_grad))
     d.budget = -1 if budget is None else int(budget)
     return d
 

@@ -398,8 +398,8 @@ steepgs_status steepgs_densify(float* params, int64_t ld, int64_t n, int64_t cap
                                size_t ws_bytes, void* stream) {
   steepgs_status s;
   if ((s = device_ok()) != STEEPGS_OK) return s;
-  if (!dp || !(dp->denom > 0.f) || (dp->gate != 0 && dp->gate != 1))
-    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "densify params: denom > 0, gate in {0, 1}");
+  if (!dp || !(dp->denom > 0.f) || dp->gate < 0 || dp->gate > 2)
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "densify params: denom > 0, gate in {0, 1, 2}");
   if (n < 0 || capacity < n || ld < capacity || ldg < capacity || capacity >= (1ll << 31))
     return fail(STEEPGS_ERR_INVALID_ARGUMENT, "need 0 <= n <= capacity <= ld, ldg < 2^31");
   if (!params || !grad_S || !n_split || !status || !workspace || (n > 0 && (!split_mask || !dest_index)))

@@ -197,8 +197,15 @@ __device__ __forceinline__ void spawn(float* __restrict__ params, int64_t ld, fl
 }
 
 // Compactest gate (App. A.2): ||G_p / denom||_2 <= eps_grad on the position gradient.
+// gate 1 — compactest (App. A.2): ||G_p / denom||_2 <= eps_grad on the position gradient;
+// gate 2 — Alg. 1's "condition on G" read as 3DGS's densification condition (C24): the mean view-space
+// gradient norm (planes 0, 1 = sum of ||dL/dPi(p)||, visible views) >= eps_grad.
 __device__ __forceinline__ bool gate_ok(const float* __restrict__ grad_S, int64_t ldg, int64_t i, float inv_denom,
-                                        float eps_grad) {
+                                        int gate, float eps_grad) {
+  if (gate == 2) {
+    const float cnt = grad_S[1 * ldg + i];
+    return cnt > 0.0f && __fdiv_rn(grad_S[0 * ldg + i], cnt) >= eps_grad;
+  }
   const float g0 = grad_S[0 * ldg + i] * inv_denom, g1 = grad_S[1 * ldg + i] * inv_denom;
   const float g2 = grad_S[2 * ldg + i] * inv_denom;
   return sqrtf(g0 * g0 + g1 * g1 + g2 * g2) <= eps_grad;
@@ -227,7 +234,7 @@ __global__ void __launch_bounds__(kThreads) k_budget_keys(const float* __restric
     load_sbar(grad_S, ldg, i, inv_denom, S6);
     const float lam = decide_lambda(S6, eps_split);
     if (lambda) lambda[i] = lam;
-    cand = lam < eps_split && (!gate || gate_ok(grad_S, ldg, i, inv_denom, eps_grad));
+    cand = lam < eps_split && (!gate || gate_ok(grad_S, ldg, i, inv_denom, gate, eps_grad));
     keys[i] = cand ? orderable(lam) : 0xFFFFFFFFu;
   }
   const uint32_t b = __ballot_sync(0xffffffffu, cand);
@@ -314,7 +321,7 @@ __global__ void __launch_bounds__(kThreads) k_densify_decide(float* __restrict__
         load_sbar(grad_S, ldg, i, inv_denom, S6);
         const float lam = decide_lambda(S6, eps_split);
         split[j] = lam < eps_split;                   // Thm 2 / Alg. 1 P:L545 (strict, Z11)
-        if (gate && split[j]) split[j] = gate_ok(grad_S, ldg, i, inv_denom, eps_grad);
+        if (gate && split[j]) split[j] = gate_ok(grad_S, ldg, i, inv_denom, gate, eps_grad);
         if (lambda) lambda[i] = lam;
       }
     }

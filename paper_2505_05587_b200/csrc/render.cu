@@ -115,7 +115,8 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 template <bool kFwd, class BatchOf>
 __device__ __forceinline__ void run_producer(Smem& sm, const uint32_t* __restrict__ ids,
                                              const steepgs_splat* __restrict__ vs, uint32_t first, int nb,
-                                             BatchOf batch_of, double ox, double oy, float* mom_view, int lane) {
+                                             BatchOf batch_of, double ox, double oy, float* mom_view, float lmin,
+                                             int lane) {
   uint32_t gcur[kBatch / 32], gnext[kBatch / 32];
   auto load_ids = [&](int k, uint32_t* g) {
     int rel = 0, cnt = 0;
@@ -167,17 +168,34 @@ __device__ __forceinline__ void run_producer(Smem& sm, const uint32_t* __restric
         B.par[kk] = make_float4(a.z, a.w, 0.0f, 0.0f);
         B.col[kk] = make_float4(b.x, b.y, b.z, 0.0f);
         if (mom_view) B.mptr[kk] = mom_view + (size_t)gcur[q] * 12;
-        uint32_t xb = 0u, yb = 0u;
+        uint32_t xb = 0u;
 #pragma unroll
         for (int t = 0; t < 2; ++t)
           if (gx - c.x <= 8.0f * t + 7.5f && gx + c.x >= 8.0f * t + 0.5f) xb |= 1u << t;
-#pragma unroll
-        for (int t = 0; t < 4; ++t)
-          if (gy - c.y <= 4.0f * t + 3.5f && gy + c.y >= 4.0f * t + 0.5f) yb |= 1u << t;
+        // per 4-row strip, the x-range of the ellipse {m' <= tau'} over the strip's pixel-centre rows:
+        // centre line -b dy / 2a (extremes at the strip ends) +- the half-width at the dy nearest 0,
+        // sqrt(4 a tau' - (4ac - b^2) dy^2) / 2a.  Conservative (tau' and the range padded), so only
+        // sub-blocks without a pixel in the alpha support are dropped (16% of the AABB's, C2).
+        const float tq = fmaf(a.w - lmin, 1.0001f, 1e-4f);
+        const float qa = a.x, qb = a.y, qc = a.z;
+        const float delta = 4.0f * qa * qc - qb * qb;
+        const float inv2a = 0.5f / qa, slope = -qb * inv2a;
         uint32_t m = 0u;
 #pragma unroll
-        for (int t = 0; t < 4; ++t)
-          if (yb & (1u << t)) m |= xb << (2 * t);
+        for (int t = 0; t < 4; ++t) {
+          if (!(gy - c.y <= 4.0f * t + 3.5f && gy + c.y >= 4.0f * t + 0.5f)) continue;
+          const float dy0 = 4.0f * t + 0.5f - gy, dy1 = dy0 + 3.0f;
+          const float dym = fminf(fmaxf(0.0f, dy0), dy1);
+          const float D = 4.0f * qa * tq - delta * dym * dym;
+          if (D < 0.0f) continue;
+          const float hw = sqrtf(D) * inv2a + 0.01f;
+          const float x0 = slope * dy0, x1 = slope * dy1;
+          const float lo = gx + fminf(x0, x1) - hw, hi = gx + fmaxf(x0, x1) + hw;
+          uint32_t xs = 0u;
+          if (hi >= 0.5f && lo <= 7.5f) xs |= 1u;
+          if (hi >= 8.5f && lo <= 15.5f) xs |= 2u;
+          m |= (xs & xb) << (2 * t);
+        }
         B.mask[kk] = m;
       }
     }
@@ -212,6 +230,7 @@ __device__ __forceinline__ int build_list(const Buffer& B, uint8_t* __restrict__
   return total;
 }
 
+template <bool kCount>   // kCount: also count composited / evaluated pairs (the roofline's units)
 __global__ void __launch_bounds__(kThreads, 4) k_render_fwd(const steepgs_splat* __restrict__ splats,
                                                          const uint32_t* __restrict__ ids,
                                                          const uint2* __restrict__ ranges, int64_t n, int W, int H,
@@ -240,7 +259,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_fwd(const steepgs_splat*
     const int len = (int)(rg.y - rg.x);
     run_producer<true>(sm, ids, splats + (int64_t)view * n, rg.x, nb,
                        [len](int k, int& rel, int& cnt) { rel = k * kBatch; cnt = min(len - rel, kBatch); }, ox, oy,
-                       nullptr, lane);
+                       nullptr, __log2f(rk.alpha_min), lane);
     return;
   }
 
@@ -263,7 +282,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_fwd(const steepgs_splat*
       uint8_t* lst = sm.buf[s].list[warp];
       const int nl = build_list(B, lst, warp, lane);
       const int base1 = B.base + 1;
-      if (!done) neval += nl;
+      if (kCount && !done) neval += nl;
       for (int t = 0; t < nl; ++t) {
         const int j = lst[t];
         const float4 g = B.geo[j];
@@ -281,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_fwd(const steepgs_splat*
         C2 = __fmaf_rn(aT, c.z, C2);
         T = Tn;
         last = base1 + j;
-        ++ncomp;
+        if (kCount) ++ncomp;
       }
       if (__all_sync(0xffffffffu, done)) {
         warp_done = true;
@@ -304,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_fwd(const steepgs_splat*
     const int wl = __reduce_max_sync(0xffffffffu, last);   // the tile's composited prefix, for the backward
     if (lane == 0 && wl > 0) atomicMax(tile_last + (int64_t)view * tiles_per_view + tile, (uint32_t)wl);
   }
-  if (pair_counts) {
+  if (kCount) {
     unsigned long long c = (unsigned long long)ncomp, e = (unsigned long long)neval;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -391,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
                           rel = (nb - 1 - k) * kBatch;
                           cnt = min(L - rel, kBatch);
                         },
-                        ox, oy, moments + (int64_t)view * n * 12, lane);
+                        ox, oy, moments + (int64_t)view * n * 12, __log2f(rk.alpha_min), lane);
     return;
   }
 
@@ -525,9 +544,13 @@ cudaError_t launch_render_fwd(const steepgs_splat* splats, int64_t n, const stee
                               int64_t* pair_counts, cudaStream_t st) {
   const int tpv = b.tiles_x * b.tiles_y;
   dim3 grid(tpv, b.V);
-  k_render_fwd<<<grid, kThreads, 0, st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
-                                          b.tiles_x, tpv, rk, image, final_T, n_contrib, b.tile_last,
-                                          reinterpret_cast<unsigned long long*>(pair_counts));
+  if (pair_counts)
+    k_render_fwd<true><<<grid, kThreads, 0, st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
+                                                  b.tiles_x, tpv, rk, image, final_T, n_contrib, b.tile_last,
+                                                  reinterpret_cast<unsigned long long*>(pair_counts));
+  else
+    k_render_fwd<false><<<grid, kThreads, 0, st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
+                                                   b.tiles_x, tpv, rk, image, final_T, n_contrib, b.tile_last, nullptr);
   note_launch();
   return check_launch("k_render_fwd");
 }

@@ -90,9 +90,22 @@ class Rasterizer:
                             self.splats, self.depth_key, self.tile_rect, self.tiles_touched)
 
     # ---- a2 ----
-    def bin_sort(self):
+    def bin_sort(self, check: bool = False):
+        """a2.  check=True reads the instance count back (one host sync) and, if it exceeds
+        max_instances, grows the instance buffers to 1.5x the count and sorts again; without it an
+        overflow is only flagged on the device (binning_arrays()["overflow"]) and the step is invalid."""
         self.binning = _lib.bin_sort(self.depth_key, self.tile_rect, self.tiles_touched, self.n, self.cams_arr, self.V,
                                      self.rp, self.sort_ws, self.max_instances)
+        if check:
+            base = self.sort_ws.data_ptr()
+            off = self.binning.n_instances - base
+            inst = int(self.sort_ws[off:off + 8].view(torch.int64).item())
+            if inst > self.max_instances:
+                self.max_instances = int(inst * 1.5) + 1024
+                ws = _lib.bin_sort_workspace_size(self.cap, self.V, self.W, self.H, self.max_instances)
+                self.sort_ws = torch.empty(ws, dtype=torch.uint8, device=self.device)
+                self.binning = _lib.bin_sort(self.depth_key, self.tile_rect, self.tiles_touched, self.n, self.cams_arr,
+                                             self.V, self.rp, self.sort_ws, self.max_instances)
 
     # ---- a3 ----
     def render_fwd(self, pair_counts: torch.Tensor | None = None):
@@ -133,9 +146,10 @@ class Rasterizer:
 
     # ---- a8 ----
     def densify(self, params: torch.Tensor, grad_S: torch.Tensor, n: int, capacity: int, eps_split=-1e-6, eta=0.5,
-                eps_abs=0.0, denom=1.0, want_lambda=True, eps_grad=None, budget=None):
-        """SDC densify (Thm 2).  eps_grad: compactest gate (App. A.2); budget: split at most this many."""
-        dp = _lib.densify_params(eps_split, eta, eps_abs, denom, eps_grad, budget)
+                eps_abs=0.0, denom=1.0, want_lambda=True, eps_grad=None, budget=None, grad_gate=None):
+        """SDC densify (Thm 2).  eps_grad: compactest gate (App. A.2); budget: split at most this many;
+        grad_gate: Alg. 1's condition on G as 3DGS's view-gradient threshold (planes 0, 1 = statistic)."""
+        dp = _lib.densify_params(eps_split, eta, eps_abs, denom, eps_grad, budget, grad_gate)
         _lib.densify(params, params.shape[1], n, capacity, grad_S, grad_S.shape[1], dp, self.split_mask,
                      self.dest_index, self.lambda_min if want_lambda else None, self.n_split, self.dens_status,
                      self.dens_ws)
@@ -201,6 +215,8 @@ class Schedule:
     eps_grad: float | None = None   # compactest gate (App. A.2)
     budget: int | None = None       # increment budget (App. A.2)
     density: str = "sdc"            # "sdc" (Alg. 1) or "adc" (3DGS baseline, f4)
+    grad_gate: float | None = None  # SDC: Alg. 1's "condition on G" as 3DGS's mean view-gradient threshold
+                                    # (pixel units, C24); None: no condition (Z12)
     eps_adc: float | None = None    # ADC threshold on the mean ||dL/dPi(p)|| in pixel units; None: 3DGS's
                                     # 0.0002 in NDC units = 0.0004 / W (C22)
     tau_adc: float = 2e-3           # ADC clone/split boundary on ||Sigma||_2 = (0.01 x scene extent ~4.4)^2
@@ -239,8 +255,9 @@ class Trainer:
         self.m = torch.zeros(N_PLANES, self.cap, dtype=torch.float32, device=d)
         self.v = torch.zeros(N_PLANES, self.cap, dtype=torch.float32, device=d)
         self.gacc = torch.zeros(3, self.cap, dtype=torch.float32, device=d)
-        self.vstats = torch.zeros(2, self.cap, dtype=torch.float32, device=d) if (schedule or Schedule()).density == "adc" \
-            else None
+        sch = schedule or Schedule()
+        self.vstats = torch.zeros(2, self.cap, dtype=torch.float32, device=d) \
+            if (sch.density == "adc" or sch.grad_gate is not None) else None
         self.normals = None
         self.normals_fn = normals_fn     # ADC: t -> [6][>= n] device normals; default: drawn on the device
         self.generator = torch.Generator(device=d)
@@ -267,6 +284,7 @@ class Trainer:
         self.opt_steps = 0      # Adam steps done
         self.fresh = True       # the next gradient step opens an accumulation window
         self.history: list[dict] = []
+        self.check_overflow = True   # grow the tile-instance buffers when needed (one 8-B read per step)
 
     def _world(self) -> int:
         import torch.distributed as dist
@@ -292,7 +310,7 @@ class Trainer:
             rz = self.rz
             sh = self.sh_degree is not None
             rz.project(self.params, self.n, cams, self.sh_rest, self.sh_degree)
-            rz.bin_sort()
+            rz.bin_sort(check=self.check_overflow)
             rz.render_fwd()
             count = 3 * rz._HW
             if self.ssim_lambda is None:
@@ -340,8 +358,11 @@ class Trainer:
             reset_mask, reset_value = rz.adc_kind, 2                   # clone parents keep their Adam state
         else:
             self._allreduce_planes(14, 6)
+            if s.grad_gate is not None:                                # statistic -> planes 0, 1 (gate 2)
+                self._allreduce_stats()
+                _lib.copy_planes(self.grad_S, self.vstats, n, 0, 2)
             rz.densify(self.params, self.grad_S, n, self.cap, eps_split=s.eps_split, eta=s.eta,
-                       denom=float(s.t_split), eps_grad=s.eps_grad, budget=s.budget)
+                       denom=float(s.t_split), eps_grad=s.eps_grad, budget=s.budget, grad_gate=s.grad_gate)
             reset_mask, reset_value = rz.split_mask, 1
         ns, st = int(rz.n_split.item()), int(rz.dens_status.item())
         if st != 0:

@@ -443,6 +443,23 @@ def test_densify_budget_and_gate_parity(orc, fused):
         assert np.array_equal(rz.dest_index[:n].cpu().numpy(), r["dest"]), kw
         if "budget" in kw:
             assert r["n_split"] <= kw["budget"]
+    # gate 2 (C24): planes 0, 1 = (sum of view-gradient norms, visible views)
+    cnt = rng.integers(0, 5, size=n).astype(np.float32)
+    ssum = (cnt * rng.uniform(0, 2e-3, size=n)).astype(np.float32)
+    with np.errstate(invalid="ignore", divide="ignore"):
+        mean = np.where(cnt > 0, ssum.astype(np.float64) / cnt, 0.0)
+    gg = 7e-4
+    ssum[np.abs(mean - gg) <= 1e-4 * gg] *= 1.5
+    G2 = np.zeros((3, n), np.float32); G2[0] = ssum; G2[1] = cnt
+    for kw in (dict(grad_gate=gg), dict(grad_gate=gg, budget=K // 3)):
+        accd[:] = 0.0
+        accd[14:20, :n] = S
+        accd[0:3, :n] = G2
+        r = orc.densify(pd, accd, n, cap, denom=denom, **kw)
+        rz, P, A = _gpu_densify_g(p, S, G2, n, cap, denom=denom, **kw)
+        assert int(rz.n_split.item()) == r["n_split"] > 0, kw
+        assert np.array_equal(rz.split_mask[:n].cpu().numpy(), r["mask"]), kw
+        assert np.array_equal(rz.dest_index[:n].cpu().numpy(), r["dest"]), kw
 
 
 def test_densify_budget_exact_ties(orc):

@@ -419,3 +419,10 @@ def test_budget_and_gate_variants_spec_examples(orc):
     acc10[14:20] *= 10.0                    # same S_bar with denom = 10; |G / denom| = 0.5 for index 0
     r = orc.densify(p, acc10, 4, 16, eps_grad=1.0, denom=10.0)
     assert list(r["mask"]) == [1, 1, 1, 0]
+    # gate 2 (C24): planes 0, 1 = (sum of view-gradient norms, visible views); split iff mean >= eps
+    acc2 = _acc_from_S(mats, 4, 16)
+    acc2[0:2, 0] = [0.3, 2.0]               # mean 0.15
+    acc2[0:2, 1] = [1.0, 0.0]               # never visible
+    acc2[0:2, 2] = [0.1, 4.0]               # mean 0.025
+    r = orc.densify(p, acc2, 4, 16, grad_gate=0.1)
+    assert list(r["mask"]) == [1, 0, 0, 0] and list(r["dest"]) == [4, -1, -1, -1]

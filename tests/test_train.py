@@ -157,7 +157,7 @@ def _batches(cams, tg, V=2):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("variant", ["plain", "budget", "gate", "ssim"])
+@pytest.mark.parametrize("variant", ["plain", "budget", "gate", "ssim", "grad_gate"])
 def test_training_loop_parity(orc, variant):
     """The Trainer (C1 scene, 2 views per step, densify at steps 4, 7, 10) against oracle/train.py:
     split counts bit-exact, parameters within the tolerance of DESIGN.md §3.4 (f1)."""
@@ -166,11 +166,13 @@ def test_training_loop_parity(orc, variant):
     from gpu_run import raster_of
     from paper_2505_05587_b200 import Adam, Schedule, Trainer
     p, cams, tg = _scene()
-    kw = dict(budget=None, eps_grad=None)
+    kw = dict(budget=None, eps_grad=None, grad_gate=None)
     if variant == "budget":
         kw["budget"] = 16
     elif variant == "gate":
         kw["eps_grad"] = 1e-3
+    elif variant == "grad_gate":
+        kw["grad_gate"] = 7e-5
     T, t_start, t_split, cap, eps = 10, 4, 3, 512, 1e-15     # 3DGS's Adam eps
     ssim_lam = 0.2 if variant == "ssim" else None
     ora = train(p, 64, cap, _batches(cams, tg), T=T, t_start=t_start, t_split=t_split, lr=LR, eps=eps, rp=SMOOTH,
@@ -180,12 +182,15 @@ def test_training_loop_parity(orc, variant):
         scale = np.abs(lam).max()
         if variant == "gate":
             assert np.abs(gn - 1e-3).min() > 1e-3 * 1e-3
+        if variant == "grad_gate":
+            assert np.abs(gn / 7e-5 - 1).min() > 2e-4
         assert np.abs(lam - (-1e-6)).min() > 1e-4 * scale
         if variant == "budget":
             srt = np.sort(lam)
             assert srt[15] < -1e-6 and srt[16] - srt[15] > 1e-4 * scale
     tr = Trainer(torch.from_numpy(p).cuda(), 64, cap, 2, 64, 64, raster_of(SMOOTH), Adam(LR, 0.9, 0.999, eps),
-                 Schedule(t_start, t_split, -1e-6, 0.5, kw["eps_grad"], kw["budget"]), ssim_lambda=ssim_lam)
+                 Schedule(t_start, t_split, -1e-6, 0.5, kw["eps_grad"], kw["budget"], grad_gate=kw["grad_gate"]),
+                 ssim_lambda=ssim_lam)
     b = _batches(cams, tg)
     for t in range(1, T + 1):
         c, y = b(t)

@@ -116,3 +116,21 @@ def test_argument_validation():
     assert e.value.status == 2
     with pytest.raises(_lib.SteepGSError):
         Rasterizer(64, 65, 64, 64)                                           # > 64 views
+
+
+def test_instance_overflow_auto_grow():
+    """bin_sort(check=True) grows the instance buffers and re-sorts, so the render is the one of a
+    generously sized binning."""
+    from gpu_run import run_forward, to_dev
+    from paper_2505_05587_b200.pipeline import Raster, Rasterizer
+    cfg = synth.CONFIGS["C1"]
+    p = synth.scene_for(cfg)
+    cams = synth.cameras_for(cfg, views=2)
+    ref, _ = run_forward(p, cams, DEFAULT)
+    rz = Rasterizer(p.shape[1], 2, 64, 64, Raster(), max_instances=16)
+    rz.project(to_dev(p), p.shape[1], cams)
+    rz.bin_sort(check=True)
+    rz.render_fwd()
+    b = rz.binning_arrays()
+    assert b["overflow"] == 0 and rz.max_instances >= b["n_instances"] > 16
+    assert torch.equal(rz.image, ref.image)

@@ -436,30 +436,40 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
     for (int t_hi = nl; t_hi > 0; t_hi -= kChunk) {
       const int t_lo = max(0, t_hi - kChunk);
       // ---- phase 1: pixel-parallel recursion over entries t_hi-1 .. t_lo ----
-      for (int t = t_hi - 1; t >= t_lo; --t) {
-        const int j = lst[t];
-        const int e = t - t_lo;
-        bool contrib = false;
-        if (j < lim) {
-          const float4 g = B.geo[j];
-          const float4 p = B.par[j];
-          const float ee = pair_e(__fsub_rn(fx, g.x), __fsub_rn(fy, g.y), g, p);
-          if (ee >= lmin) {
-            contrib = true;
-            const float sigma = ex2_approx(ee);
-            const float alpha = fminf(amax, sigma);
-            const float4 c = B.col[j];
-            const float om = 1.0f - alpha;
-            T = T * rcp_approx(om);                         // T_i (before this splat)
-            const float gsum = dl0 * (c.x - B0) + dl1 * (c.y - B1) + dl2 * (c.z - B2);
-            B0 = alpha * c.x + om * B0;
-            B1 = alpha * c.y + om * B1;
-            B2 = alpha * c.z + om * B2;
-            swat[e][lane] = make_float2(T * gsum * sigma, alpha * T);  // dL/dalpha * sigma (Z3), alpha T
-          }
+      // Two entries per iteration: both pair tests are evaluated before the (serial) recursion, so
+      // their shared-memory loads and arithmetic overlap.
+      auto recurse = [&](bool hit, float ee, int j, int e) {
+        if (hit) {
+          const float sigma = ex2_approx(ee);
+          const float alpha = fminf(amax, sigma);
+          const float4 c = B.col[j];
+          const float om = 1.0f - alpha;
+          T = T * rcp_approx(om);                           // T_i (before this splat)
+          const float gsum = dl0 * (c.x - B0) + dl1 * (c.y - B1) + dl2 * (c.z - B2);
+          B0 = alpha * c.x + om * B0;
+          B1 = alpha * c.y + om * B1;
+          B2 = alpha * c.z + om * B2;
+          swat[e][lane] = make_float2(T * gsum * sigma, alpha * T);  // dL/dalpha * sigma (Z3), alpha T
         }
-        const uint32_t bal = __ballot_sync(0xffffffffu, contrib);
+        const uint32_t bal = __ballot_sync(0xffffffffu, hit);
         if (lane == 0) scm[e] = bal;
+      };
+      int t = t_hi - 1;
+      for (; t > t_lo; t -= 2) {
+        const int ja = lst[t], jb = lst[t - 1];
+        const float4 ga = B.geo[ja], gb = B.geo[jb];
+        const float4 pa = B.par[ja], pb = B.par[jb];
+        const float ea = pair_e(__fsub_rn(fx, ga.x), __fsub_rn(fy, ga.y), ga, pa);
+        const float eb = pair_e(__fsub_rn(fx, gb.x), __fsub_rn(fy, gb.y), gb, pb);
+        recurse(ja < lim && ea >= lmin, ea, ja, t - t_lo);
+        recurse(jb < lim && eb >= lmin, eb, jb, t - 1 - t_lo);
+      }
+      if (t == t_lo) {
+        const int ja = lst[t];
+        const float4 ga = B.geo[ja];
+        const float4 pa = B.par[ja];
+        const float ea = pair_e(__fsub_rn(fx, ga.x), __fsub_rn(fy, ga.y), ga, pa);
+        recurse(ja < lim && ea >= lmin, ea, ja, 0);
       }
       __syncwarp();
       // ---- phase 2: splat-parallel sums (lanes e2 and e2 + 16 own entry e2) ----

@@ -283,16 +283,12 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_fwd(const steepgs_splat*
       const int nl = build_list(B, lst, warp, lane);
       const int base1 = B.base + 1;
       if (kCount && !done) neval += nl;
-      for (int t = 0; t < nl; ++t) {
-        const int j = lst[t];
-        const float4 g = B.geo[j];
-        const float2 p = *reinterpret_cast<const float2*>(&B.par[j]);
-        if (done) continue;
-        const float e = pair_e(__fsub_rn(fx, g.x), __fsub_rn(fy, g.y), g, make_float4(p.x, p.y, 0.f, 0.f));
-        if (e < lmin) continue;                           // sigma < alpha_min: C8 skip
+      // Two entries per iteration: both pair tests ahead of the serial compositing (as in the bwd).
+      auto blend = [&](float e, int j) {
+        if (done || e < lmin) return;                     // sigma < alpha_min: C8 skip
         const float alpha = fminf(amax, ex2_approx(e));
         const float Tn = __fmul_rn(T, __fsub_rn(1.0f, alpha));
-        if (Tn < tmin) { done = true; continue; }         // C8 termination
+        if (Tn < tmin) { done = true; return; }           // C8 termination
         const float4 c = B.col[j];
         const float aT = __fmul_rn(alpha, T);
         C0 = __fmaf_rn(aT, c.x, C0);
@@ -301,6 +297,24 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_fwd(const steepgs_splat*
         T = Tn;
         last = base1 + j;
         if (kCount) ++ncomp;
+      };
+      int t = 0;
+      for (; t + 1 < nl; t += 2) {
+        const int ja = lst[t], jb = lst[t + 1];
+        const float4 ga = B.geo[ja], gb = B.geo[jb];
+        const float2 pa = *reinterpret_cast<const float2*>(&B.par[ja]);
+        const float2 pb = *reinterpret_cast<const float2*>(&B.par[jb]);
+        if (done) continue;
+        const float ea = pair_e(__fsub_rn(fx, ga.x), __fsub_rn(fy, ga.y), ga, make_float4(pa.x, pa.y, 0.f, 0.f));
+        const float eb = pair_e(__fsub_rn(fx, gb.x), __fsub_rn(fy, gb.y), gb, make_float4(pb.x, pb.y, 0.f, 0.f));
+        blend(ea, ja);
+        blend(eb, jb);
+      }
+      if (t < nl && !done) {
+        const int ja = lst[t];
+        const float4 ga = B.geo[ja];
+        const float2 pa = *reinterpret_cast<const float2*>(&B.par[ja]);
+        blend(pair_e(__fsub_rn(fx, ga.x), __fsub_rn(fy, ga.y), ga, make_float4(pa.x, pa.y, 0.f, 0.f)), ja);
       }
       if (__all_sync(0xffffffffu, done)) {
         warp_done = true;

@@ -469,21 +469,25 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
         if (lane == 0) scm[e] = bal;
       };
       int t = t_hi - 1;
-      for (; t > t_lo; t -= 2) {
-        const int ja = lst[t], jb = lst[t - 1];
-        const float4 ga = B.geo[ja], gb = B.geo[jb];
-        const float4 pa = B.par[ja], pb = B.par[jb];
-        const float ea = pair_e(__fsub_rn(fx, ga.x), __fsub_rn(fy, ga.y), ga, pa);
-        const float eb = pair_e(__fsub_rn(fx, gb.x), __fsub_rn(fy, gb.y), gb, pb);
-        recurse(ja < lim && ea >= lmin, ea, ja, t - t_lo);
-        recurse(jb < lim && eb >= lmin, eb, jb, t - 1 - t_lo);
+      for (; t - 3 >= t_lo; t -= 4) {
+        int jj[4];
+        float ee[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          jj[u] = lst[t - u];
+          const float4 g = B.geo[jj[u]];
+          const float4 p = B.par[jj[u]];
+          ee[u] = pair_e(__fsub_rn(fx, g.x), __fsub_rn(fy, g.y), g, p);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) recurse(jj[u] < lim && ee[u] >= lmin, ee[u], jj[u], t - u - t_lo);
       }
-      if (t == t_lo) {
+      for (; t >= t_lo; --t) {
         const int ja = lst[t];
         const float4 ga = B.geo[ja];
         const float4 pa = B.par[ja];
         const float ea = pair_e(__fsub_rn(fx, ga.x), __fsub_rn(fy, ga.y), ga, pa);
-        recurse(ja < lim && ea >= lmin, ea, ja, 0);
+        recurse(ja < lim && ea >= lmin, ea, ja, t - t_lo);
       }
       __syncwarp();
       // ---- phase 2: splat-parallel sums (lanes e2 and e2 + 16 own entry e2) ----

@@ -299,18 +299,21 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_fwd(const steepgs_splat*
         if (kCount) ++ncomp;
       };
       int t = 0;
-      for (; t + 1 < nl; t += 2) {
-        const int ja = lst[t], jb = lst[t + 1];
-        const float4 ga = B.geo[ja], gb = B.geo[jb];
-        const float2 pa = *reinterpret_cast<const float2*>(&B.par[ja]);
-        const float2 pb = *reinterpret_cast<const float2*>(&B.par[jb]);
+      for (; t + 3 < nl; t += 4) {
+        int jj[4];
+        float ee[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          jj[u] = lst[t + u];
+          const float4 g = B.geo[jj[u]];
+          const float2 p = *reinterpret_cast<const float2*>(&B.par[jj[u]]);
+          ee[u] = pair_e(__fsub_rn(fx, g.x), __fsub_rn(fy, g.y), g, make_float4(p.x, p.y, 0.f, 0.f));
+        }
         if (done) continue;
-        const float ea = pair_e(__fsub_rn(fx, ga.x), __fsub_rn(fy, ga.y), ga, make_float4(pa.x, pa.y, 0.f, 0.f));
-        const float eb = pair_e(__fsub_rn(fx, gb.x), __fsub_rn(fy, gb.y), gb, make_float4(pb.x, pb.y, 0.f, 0.f));
-        blend(ea, ja);
-        blend(eb, jb);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) blend(ee[u], jj[u]);
       }
-      if (t < nl && !done) {
+      for (; t < nl && !done; ++t) {
         const int ja = lst[t];
         const float4 ga = B.geo[ja];
         const float2 pa = *reinterpret_cast<const float2*>(&B.par[ja]);

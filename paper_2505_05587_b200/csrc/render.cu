@@ -371,7 +371,7 @@ __device__ __forceinline__ void red_v4(float* p, float a, float b, float c, floa
 //   phase 1 (pixel-parallel): each lane runs its pixel's recursion over the chunk and leaves
 //     w = dL/dsigma * sigma and alpha T in shared memory, plus a ballot of contributing pixels;
 //   phase 2 (splat-parallel): lanes e and e + 16 own entry e and sum its 9 moments over the
-//     contributing pixels (even / odd columns), combine with one xor-16 shuffle per value, and
+//     contributing pixels (even / odd rank), combine with one xor-16 shuffle per value, and
 //     add them with two 16-B + one 4-B vector REDs.
 // No per-(warp, splat) cross-lane reduction tree: the reduction costs O(contributing pairs).
 __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat* __restrict__ splats,
@@ -441,7 +441,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
   const float4* spix = sc.pix[warp];
   const float* sdl2 = sc.pdl2[warp];
   const int e2 = lane & (kChunk - 1), half = lane >> 4;
-  const uint32_t half_mask = half ? 0xAAAAAAAAu : 0x55555555u;   // alternate columns: balanced halves
   for (int k = 0; k < nb; ++k) {
     const int s = k % kStages;
     mbar_wait(&sm.full[s], (k / kStages) & 1, 32);
@@ -504,7 +503,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
       if (valid) {
         j2 = lst[t_lo + e2];
         full_bits = scm[e2];
-        uint32_t bits = full_bits & half_mask;
+        // the two lanes of an entry take the contributing pixels of even / odd rank (prefix parity)
+        uint32_t x = full_bits;
+        x ^= x << 1; x ^= x << 2; x ^= x << 4; x ^= x << 8; x ^= x << 16;
+        const uint32_t odd = full_bits & (x << 1);
+        uint32_t bits = half ? odd : (full_bits & ~odd);
         const float2 gm = *reinterpret_cast<const float2*>(&B.geo[j2]);
         const float2* row = swat[e2];
         while (bits) {

@@ -510,13 +510,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
         uint32_t bits = half ? odd : (full_bits & ~odd);
         const float2 gm = *reinterpret_cast<const float2*>(&B.geo[j2]);
         const float2* row = swat[e2];
-        while (bits) {
-          const int pp = 31 - __clz(bits);
-          bits ^= 1u << pp;
-          const float2 wa = row[pp];
-          const float4 d = spix[pp];
-          const float dl2p = sdl2[pp];
-          const float w = wa.x, at = wa.y;
+        auto add = [&](float w, float at, float4 d, float dl2p) {
           const float dx = d.x - gm.x, dy = d.y - gm.y;
           const float wdx = w * dx, wdy = w * dy;
           acc[0] += w;
@@ -528,6 +522,18 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
           acc[6] = fmaf(at, d.z, acc[6]);
           acc[7] = fmaf(at, d.w, acc[7]);
           acc[8] = fmaf(at, dl2p, acc[8]);
+        };
+        while (bits) {        // two pixels per iteration; a missing second one adds zeros
+          const int pa = 31 - __clz(bits);
+          bits ^= 1u << pa;
+          const bool two = bits != 0u;
+          const int pb = two ? 31 - __clz(bits) : pa;
+          bits &= ~(two ? (1u << pb) : 0u);
+          const float2 wa = row[pa], wb = row[pb];
+          const float4 da = spix[pa], db = spix[pb];
+          const float la = sdl2[pa], lb = sdl2[pb];
+          add(wa.x, wa.y, da, la);
+          add(two ? wb.x : 0.0f, two ? wb.y : 0.0f, db, lb);
         }
       }
 #pragma unroll

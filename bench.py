@@ -180,6 +180,7 @@ def main():
 
     from paper_2505_05587_b200 import _lib
     from paper_2505_05587_b200.pipeline import Rasterizer
+    from paper_2505_05587_b200.parallel import allreduce_accumulators
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -231,7 +232,7 @@ def main():
         rz.gauss_bwd(params, grad_S, accumulate=False)
         mark(7)
         if ws > 1:
-            dist.all_reduce(grad_S)
+            allreduce_accumulators(grad_S, n=n)          # 20 row slices [k, :n], NCCL
         mark(8)
         rz.densify(params, grad_S, n, cap, denom=float(V * ws), want_lambda=False)
         mark(9)

@@ -22,26 +22,26 @@ def shard_views(n_views: int, rank: int, world: int) -> list[int]:
 def allreduce_accumulators(acc: torch.Tensor, group=None, n: int | None = None) -> torch.Tensor:
     """Sum the [20][ld] gradient + splitting-matrix accumulator over ranks, in place.
 
-    With `n` given and ld > n, only the first n columns are reduced (20 row slices, coalesced into
-    one NCCL group call); otherwise the whole contiguous buffer is reduced in one call."""
+    With `n` given and ld > n, only the first n columns are reduced: one in-place allreduce per
+    plane row acc[k, :n] (each row slice is contiguous), issued asynchronously so NCCL pipelines
+    them; otherwise the whole contiguous buffer is reduced in one call."""
     if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
         return acc
     if n is None or n >= acc.shape[1]:
         dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
         return acc
-    flat = acc[:, :n].contiguous()
-    dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
-    acc[:, :n].copy_(flat)
-    return acc
+    return allreduce_planes(acc, 0, acc.shape[0], n, group)
 
 
 def allreduce_planes(acc: torch.Tensor, first: int, count: int, n: int, group=None) -> torch.Tensor:
-    """Sum planes [first, first + count), columns [0, n) of a planar accumulator over ranks, in place."""
+    """Sum planes [first, first + count), columns [0, n) of a planar accumulator over ranks, in place
+    (one asynchronous allreduce per contiguous row slice, no staging copies)."""
     if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
         return acc
-    blk = acc[first:first + count, :n].contiguous()
-    dist.all_reduce(blk, op=dist.ReduceOp.SUM, group=group)
-    acc[first:first + count, :n].copy_(blk)
+    works = [dist.all_reduce(acc[k, :n], op=dist.ReduceOp.SUM, group=group, async_op=True)
+             for k in range(first, first + count)]
+    for w in works:
+        w.wait()
     return acc
 
 

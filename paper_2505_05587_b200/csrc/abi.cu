@@ -50,7 +50,16 @@ static steepgs_status check_views(const steepgs_camera* cams, int32_t V, CamPack
     if (cams[v].width >= 65536 * kTile || cams[v].height >= 65536 * kTile)
       return fail(STEEPGS_ERR_INVALID_ARGUMENT, "image too large");
     if (cams[v].model != 0 && cams[v].model != 1) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "camera model must be 0 or 1");
-    if (pack) pack->cam[v] = cams[v];
+    if (pack) {
+      pack->cam[v] = cams[v];
+      // same fp32 operations as the decision chain (MUL(guard, DIV(MUL(0.5, W), fx))), evaluated
+      // once per camera; volatile keeps each operation a separately rounded IEEE single op
+      volatile float hw = 0.5f * (float)cams[v].width, hh = 0.5f * (float)cams[v].height;
+      volatile float qx = hw / cams[v].fx, qy = hh / cams[v].fy;
+      volatile float lx = cams[v].guard * qx, ly = cams[v].guard * qy;
+      pack->lim[v][0] = lx;
+      pack->lim[v][1] = ly;
+    }
   }
   return STEEPGS_OK;
 }

@@ -10,8 +10,10 @@ namespace sgs {
 constexpr int kTile = 16;          // tile edge in pixels (16x16 = 256 threads per tile block)
 constexpr int kMaxViews = 64;      // cameras passed by value in kernel parameters
 
-struct CamPack {                   // by-value kernel parameter (<= 64 * 80 B)
+struct CamPack {                   // by-value kernel parameter (<= 64 * 92 B)
   steepgs_camera cam[kMaxViews];
+  float lim[kMaxViews][2];          // guard * (W/2) / fx, guard * (H/2) / fy: the decision chain's
+                                    // per-camera cull limits (§3.2), IEEE fp32 on the host
 };
 
 struct RasterK {

@@ -112,8 +112,7 @@ __global__ void __launch_bounds__(256) k_project(const float* __restrict__ param
     if (c.model == 0) {
       vis = vis && (tz > c.znear);
       const float xz = DIV(tx, tz), yz = DIV(ty, tz);
-      const float limx = MUL(c.guard, DIV(MUL(0.5f, (float)c.width), c.fx));
-      const float limy = MUL(c.guard, DIV(MUL(0.5f, (float)c.height), c.fy));
+      const float limx = cams.lim[v][0], limy = cams.lim[v][1];   // MUL(guard, DIV(MUL(0.5, W), fx)), host
       vis = vis && (fabsf(xz) <= limx) && (fabsf(yz) <= limy);
       mux = ADD(MUL(c.fx, xz), c.cx);
       muy = ADD(MUL(c.fy, yz), c.cy);

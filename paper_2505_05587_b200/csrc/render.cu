@@ -34,7 +34,9 @@ namespace sgs {
 namespace {
 
 constexpr int kConsumers = 8;                       // one pixel per thread, 8 warps per 16x16 tile
-constexpr int kThreads = 32 * (kConsumers + 1);     // + 1 producer warp
+constexpr int kThreads = 32 * (kConsumers + 1);     // + 1 producer warp (backward)
+constexpr int kFwdProducers = 2;                    // the forward's consumers are faster: 2 producer warps
+constexpr int kThreadsFwd = 32 * (kConsumers + kFwdProducers);
 constexpr int kBatch = 128;                         // splats per staged batch
 constexpr int kStages = 3;                          // ring depth
 
@@ -54,6 +56,7 @@ struct Smem {
   uint4 raw[4][kBatch];          // producer staging: the next batch's 64-B records (cp.async), SoA by 16 B
   unsigned long long full[kStages], empty[kStages];
   int done_warps;
+  int stop_flag[2];              // forward: the producers' shared early-exit decision (double-buffered)
 };
 
 __device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -112,18 +115,20 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // round trip once it runs ahead.  Staging a record is then two fp64 subtractions and eight
 // interval tests of the padded extents against the 8x4 sub-blocks.
 // kFwd: stop early once every consumer warp has terminated (forward early exit).
-template <bool kFwd, class BatchOf>
+template <bool kFwd, int kProd, class BatchOf>
 __device__ __forceinline__ void run_producer(Smem& sm, const uint32_t* __restrict__ ids,
                                              const steepgs_splat* __restrict__ vs, uint32_t first, int nb,
                                              BatchOf batch_of, double ox, double oy, float* mom_view, float lmin,
-                                             int lane) {
-  uint32_t gcur[kBatch / 32], gnext[kBatch / 32];
+                                             int pw, int lane) {
+  // producer warp pw of kProd stages the batch slots kk = (q kProd + pw) * 32 + lane
+  constexpr int kQ = kBatch / 32 / kProd;
+  uint32_t gcur[kQ], gnext[kQ];
   auto load_ids = [&](int k, uint32_t* g) {
     int rel = 0, cnt = 0;
     if (k < nb) batch_of(k, rel, cnt);
 #pragma unroll
-    for (int q = 0; q < kBatch / 32; ++q) {
-      const int kk = q * 32 + lane;
+    for (int q = 0; q < kQ; ++q) {
+      const int kk = (q * kProd + pw) * 32 + lane;
       g[q] = kk < cnt ? __ldg(ids + first + rel + kk) : 0u;
     }
   };
@@ -132,8 +137,8 @@ __device__ __forceinline__ void run_producer(Smem& sm, const uint32_t* __restric
       int rel, cnt;
       batch_of(k, rel, cnt);
 #pragma unroll
-      for (int q = 0; q < kBatch / 32; ++q) {
-        const int kk = q * 32 + lane;
+      for (int q = 0; q < kQ; ++q) {
+        const int kk = (q * kProd + pw) * 32 + lane;
         if (kk < cnt) {
           const uint4* src = reinterpret_cast<const uint4*>(vs + g[q]);
 #pragma unroll
@@ -150,14 +155,24 @@ __device__ __forceinline__ void run_producer(Smem& sm, const uint32_t* __restric
     const int s = k % kStages;
     if (k >= kStages) mbar_wait(&sm.empty[s], ((k / kStages) & 1) ^ 1, 256);
     Buffer& B = sm.buf[s];
-    const int stop = kFwd ? (*reinterpret_cast<volatile int*>(&sm.done_warps) == kConsumers) : 0;
+    int stop = 0;
+    if (kFwd) {   // one decision per batch for all producer warps (a split decision would deadlock)
+      if (kProd == 1) {
+        stop = *reinterpret_cast<volatile int*>(&sm.done_warps) == kConsumers;
+      } else {
+        if (pw == 0 && lane == 0)
+          sm.stop_flag[k & 1] = *reinterpret_cast<volatile int*>(&sm.done_warps) == kConsumers;
+        asm volatile("bar.sync 1, %0;" ::"r"(32 * kProd) : "memory");
+        stop = *reinterpret_cast<volatile int*>(&sm.stop_flag[k & 1]);
+      }
+    }
     int rel, cnt;
     batch_of(k, rel, cnt);
     cp_async_wait_all();
     if (!stop) {
 #pragma unroll
-      for (int q = 0; q < kBatch / 32; ++q) {
-        const int kk = q * 32 + lane;
+      for (int q = 0; q < kQ; ++q) {
+        const int kk = (q * kProd + pw) * 32 + lane;
         if (kk >= cnt) { B.mask[kk] = 0u; continue; }
         const double2 mean = *reinterpret_cast<const double2*>(&sm.raw[0][kk]);
         const float4 a = *reinterpret_cast<const float4*>(&sm.raw[1][kk]);   // conic', log2 o
@@ -199,7 +214,7 @@ __device__ __forceinline__ void run_producer(Smem& sm, const uint32_t* __restric
         B.mask[kk] = m;
       }
     }
-    if (lane == 0) {
+    if (pw == 0 && lane == 0) {
       B.base = rel;
       B.stop = stop;
     }
@@ -207,7 +222,7 @@ __device__ __forceinline__ void run_producer(Smem& sm, const uint32_t* __restric
     mbar_arrive(&sm.full[s]);
     if (stop) break;
 #pragma unroll
-    for (int q = 0; q < kBatch / 32; ++q) gcur[q] = gnext[q];
+    for (int q = 0; q < kQ; ++q) gcur[q] = gnext[q];
     issue(k + 1, gcur);
     load_ids(k + 2, gnext);
   }
@@ -231,7 +246,7 @@ __device__ __forceinline__ int build_list(const Buffer& B, uint8_t* __restrict__
 }
 
 template <bool kCount>   // kCount: also count composited / evaluated pairs (the roofline's units)
-__global__ void __launch_bounds__(kThreads, 4) k_render_fwd(const steepgs_splat* __restrict__ splats,
+__global__ void __launch_bounds__(kThreadsFwd, 4) k_render_fwd(const steepgs_splat* __restrict__ splats,
                                                          const uint32_t* __restrict__ ids,
                                                          const uint2* __restrict__ ranges, int64_t n, int W, int H,
                                                          int tiles_x, int tiles_per_view, const RasterK rk,
@@ -248,18 +263,18 @@ __global__ void __launch_bounds__(kThreads, 4) k_render_fwd(const steepgs_splat*
   const int nb = (int)((rg.y - rg.x + kBatch - 1) / kBatch);
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&sm.full[s], 32);
+      mbar_init(&sm.full[s], 32 * kFwdProducers);
       mbar_init(&sm.empty[s], 32 * kConsumers);
     }
     sm.done_warps = 0;
   }
   __syncthreads();
 
-  if (warp == kConsumers) {  // ---------------- producer ----------------
+  if (warp >= kConsumers) {  // ---------------- producers ----------------
     const int len = (int)(rg.y - rg.x);
-    run_producer<true>(sm, ids, splats + (int64_t)view * n, rg.x, nb,
-                       [len](int k, int& rel, int& cnt) { rel = k * kBatch; cnt = min(len - rel, kBatch); }, ox, oy,
-                       nullptr, __log2f(rk.alpha_min), lane);
+    run_producer<true, kFwdProducers>(sm, ids, splats + (int64_t)view * n, rg.x, nb,
+                                      [len](int k, int& rel, int& cnt) { rel = k * kBatch; cnt = min(len - rel, kBatch); },
+                                      ox, oy, nullptr, __log2f(rk.alpha_min), warp - kConsumers, lane);
     return;
   }
 
@@ -422,12 +437,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
   const int wmax = __reduce_max_sync(0xffffffffu, last);
 
   if (warp == kConsumers) {  // ---------------- producer: batches from the back ----------------
-    run_producer<false>(sm, ids, splats + (int64_t)view * n, rg.x, nb,
+    run_producer<false, 1>(sm, ids, splats + (int64_t)view * n, rg.x, nb,
                         [nb, L](int k, int& rel, int& cnt) {
                           rel = (nb - 1 - k) * kBatch;
                           cnt = min(L - rel, kBatch);
                         },
-                        ox, oy, moments + (int64_t)view * n * 12, __log2f(rk.alpha_min), lane);
+                        ox, oy, moments + (int64_t)view * n * 12, __log2f(rk.alpha_min), 0, lane);
     return;
   }
 
@@ -585,11 +600,11 @@ cudaError_t launch_render_fwd(const steepgs_splat* splats, int64_t n, const stee
   const int tpv = b.tiles_x * b.tiles_y;
   dim3 grid(tpv, b.V);
   if (pair_counts)
-    k_render_fwd<true><<<grid, kThreads, 0, st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
+    k_render_fwd<true><<<grid, kThreadsFwd, 0, st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
                                                   b.tiles_x, tpv, rk, image, final_T, n_contrib, b.tile_last,
                                                   reinterpret_cast<unsigned long long*>(pair_counts));
   else
-    k_render_fwd<false><<<grid, kThreads, 0, st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
+    k_render_fwd<false><<<grid, kThreadsFwd, 0, st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
                                                    b.tiles_x, tpv, rk, image, final_T, n_contrib, b.tile_last, nullptr);
   note_launch();
   return check_launch("k_render_fwd");

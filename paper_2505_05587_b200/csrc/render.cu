@@ -229,14 +229,15 @@ __device__ __forceinline__ void run_producer(Smem& sm, const uint32_t* __restric
   cp_async_wait_all();
 }
 
-// Consumer: compact the staged batch to the splats whose mask has bit `w` (ascending order) into
-// the warp's own list; returns the count.
-__device__ __forceinline__ int build_list(const Buffer& B, uint8_t* __restrict__ list, int w, int lane) {
+// Consumer: compact the staged batch to the splats whose mask has bit `w` (ascending order, slots
+// below `limit`) into the warp's own list; returns the count.
+__device__ __forceinline__ int build_list(const Buffer& B, uint8_t* __restrict__ list, int w, int lane,
+                                          int limit = kBatch) {
   int total = 0;
   const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
   for (int q = 0; q < kBatch / 32; ++q) {
-    const bool hit = (B.mask[q * 32 + lane] >> w) & 1u;
+    const bool hit = ((B.mask[q * 32 + lane] >> w) & 1u) && q * 32 + lane < limit;
     const uint32_t bal = __ballot_sync(0xffffffffu, hit);
     if (hit) list[total + __popc(bal & lt)] = (uint8_t)(q * 32 + lane);
     total += __popc(bal);
@@ -461,8 +462,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
     mbar_wait(&sm.full[s], (k / kStages) & 1, 32);
     const Buffer& B = sm.buf[s];
     uint8_t* lst = sm.buf[s].list[warp];
-    int nl = build_list(B, lst, warp, lane);
-    while (nl > 0 && B.base + lst[nl - 1] >= wmax) --nl;   // beyond every pixel's prefix (warp-uniform)
+    const int nl = build_list(B, lst, warp, lane, wmax - B.base);   // only entries before the warp's prefix end
     const int lim = last - B.base;                          // this pixel composited list positions < last
     for (int t_hi = nl; t_hi > 0; t_hi -= kChunk) {
       const int t_lo = max(0, t_hi - kChunk);

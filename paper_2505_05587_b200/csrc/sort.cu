@@ -175,16 +175,22 @@ __global__ void __launch_bounds__(kRadixThreads, 3) k_radix_pass(const uint32_t*
     d[j] = ok ? ((k[j] >> shift) & 255u) : 256u;
   }
   const uint32_t lt = lanemask_lt();
+  // warp-level ranking: peers by match.any; the lowest peer adds the group's size to the warp's
+  // digit counter with a returning shared atomic.  The 12 atomics are independent instructions
+  // issued in item order (one warp, in-order issue), so their latencies overlap instead of
+  // forming a load -> store chain through shared memory, and equal digits keep item order.
+  uint32_t peers[kRadixItems], old[kRadixItems];
+#pragma unroll
+  for (int j = 0; j < kRadixItems; ++j) peers[j] = __match_any_sync(0xffffffffu, d[j]);
 #pragma unroll
   for (int j = 0; j < kRadixItems; ++j) {
-    const uint32_t peers = __match_any_sync(0xffffffffu, d[j]);
-    const uint32_t before_lanes = __popc(peers & lt);
-    uint32_t before = 0;
-    if (d[j] < 256u) before = s_whist[warp][d[j]];
-    __syncwarp();
-    if (d[j] < 256u && before_lanes == 0) s_whist[warp][d[j]] = before + __popc(peers);
-    __syncwarp();
-    rank[j] = before + before_lanes;
+    old[j] = 0u;
+    if (d[j] < 256u && (peers[j] & lt) == 0u) old[j] = atomicAdd(&s_whist[warp][d[j]], (uint32_t)__popc(peers[j]));
+  }
+#pragma unroll
+  for (int j = 0; j < kRadixItems; ++j) {
+    const uint32_t before = __shfl_sync(0xffffffffu, old[j], __ffs(peers[j]) - 1);
+    rank[j] = before + __popc(peers[j] & lt);
   }
   __syncthreads();
   // per digit (thread = digit): exclusive over warps, block total, look-back, bases

@@ -313,24 +313,43 @@ __global__ void __launch_bounds__(kScanThreads) k_duplicate(const uint32_t* __re
   }
   __syncthreads();
   const uint64_t bex = s_excl;
+  // Load-balanced emission: the warp emits the instances of its 32 items of group j together,
+  // lane e handling instance e, e + 32, ... of the group; the source item is the last lane whose
+  // exclusive prefix is <= e (5-step shuffle search), so a Gaussian covering many tiles is spread
+  // over the warp and each store instruction writes 32 consecutive instances.
 #pragma unroll
   for (int j = 0; j < kScanItems; ++j) {
     const uint32_t tt = rec[j].w & 0xFFFFFFu;
-    if (tt == 0) continue;
-    uint64_t pos = bex + s_cnt[j][warp] + pre[j];
-    const uint32_t view = rec[j].w >> 24;
-    const uint32_t x0 = rec[j].x & 0xFFFFu, x1 = rec[j].x >> 16, y0 = rec[j].y & 0xFFFFu, y1 = rec[j].y >> 16;
-    const uint32_t vbase = view * (uint32_t)tiles_per_view;
-    for (uint32_t ty = y0; ty <= y1; ++ty)
-      for (uint32_t tx = x0; tx <= x1; ++tx, ++pos) {
-        if ((int64_t)pos >= max_instances) continue;
-        const uint32_t key = vbase + ty * (uint32_t)tiles_x + tx;
-        inst_keys[pos] = key;
-        inst_ids[pos] = rec[j].z;
-        atomicAdd(&s_hist[0][key & 255u], 1u);
-        if (tile_passes > 1) atomicAdd(&s_hist[1][(key >> 8) & 255u], 1u);
-        if (tile_passes > 2) atomicAdd(&s_hist[2][(key >> 16) & 255u], 1u);
+    const uint32_t total = __shfl_sync(0xffffffffu, pre[j] + tt, 31);
+    if (total == 0) continue;
+    const uint64_t gbase = bex + s_cnt[j][warp];
+    const uint32_t w = (rec[j].x >> 16) - (rec[j].x & 0xFFFFu) + 1u;
+    for (uint32_t e0 = 0; e0 < total; e0 += 32) {
+      const uint32_t e = e0 + (uint32_t)lane;
+      int src = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const uint32_t p = __shfl_sync(0xffffffffu, pre[j], src + step);
+        if (p <= e) src += step;
       }
+      const uint32_t local = e - __shfl_sync(0xffffffffu, pre[j], src);
+      const uint32_t sw = __shfl_sync(0xffffffffu, w, src);
+      const uint32_t sx = __shfl_sync(0xffffffffu, rec[j].x, src);
+      const uint32_t sy = __shfl_sync(0xffffffffu, rec[j].y, src);
+      const uint32_t sid = __shfl_sync(0xffffffffu, rec[j].z, src);
+      const uint32_t sview = __shfl_sync(0xffffffffu, rec[j].w, src) >> 24;
+      if (e >= total) continue;
+      const uint32_t dy = local / sw, dx = local - dy * sw;
+      const uint32_t key = sview * (uint32_t)tiles_per_view + ((sy & 0xFFFFu) + dy) * (uint32_t)tiles_x +
+                           (sx & 0xFFFFu) + dx;
+      const uint64_t pos = gbase + e;
+      if ((int64_t)pos >= max_instances) continue;
+      inst_keys[pos] = key;
+      inst_ids[pos] = sid;
+      atomicAdd(&s_hist[0][key & 255u], 1u);
+      if (tile_passes > 1) atomicAdd(&s_hist[1][(key >> 8) & 255u], 1u);
+      if (tile_passes > 2) atomicAdd(&s_hist[2][(key >> 16) & 255u], 1u);
+    }
   }
   __syncthreads();
   for (int k = tid; k < 3 * 256; k += kScanThreads) {

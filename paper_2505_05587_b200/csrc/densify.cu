@@ -156,15 +156,26 @@ __device__ __forceinline__ float decide_lambda(const float* S6, float eps_split)
 
 // Offspring of split parent i (Thm 2 / Alg. 1): A in slot i at p + eps v, B in slot b at
 // p - eps v, both with opacity logit(o/2) (Z15), other planes copied (Z14); B's accumulators zeroed.
-__device__ __forceinline__ void spawn(float* __restrict__ params, int64_t ld, float* __restrict__ grad_S,
-                                      int64_t ldg, int64_t i, int64_t b, const float* S6, float eta, float eps_abs) {
-  float v[3], lam_unused;
-  eig_min_robust(S6, true, lam_unused, v);
+// Split in two so the fused kernel can do the arithmetic and the parent loads before its look-back
+// completes and only the stores after it.
+struct Spawn {
+  float v[3], eps, p[3], lg;
+  float rest[10];   // planes 3-9 (log-scale, quaternion) and 11-13 (colour)
+};
+
+__device__ __forceinline__ void spawn_prepare(const float* __restrict__ params, int64_t ld, int64_t i,
+                                              const float* S6, float eta, float eps_abs, Spawn& sp) {
+  float lam_unused;
+  eig_min_robust(S6, true, lam_unused, sp.v);
   // parent: p, Sigma = R diag(s^2) R^T, o
-  const float p0 = params[0 * ld + i], p1 = params[1 * ld + i], p2 = params[2 * ld + i];
+  sp.p[0] = params[0 * ld + i]; sp.p[1] = params[1 * ld + i]; sp.p[2] = params[2 * ld + i];
+#pragma unroll
+  for (int k = 0; k < 7; ++k) sp.rest[k] = params[(3 + k) * ld + i];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) sp.rest[7 + k] = params[(11 + k) * ld + i];
   float eps = eps_abs;
   if (eta >= 0.f) {
-    const float qw = params[6 * ld + i], qx = params[7 * ld + i], qy = params[8 * ld + i], qz = params[9 * ld + i];
+    const float qw = sp.rest[3], qx = sp.rest[4], qy = sp.rest[5], qz = sp.rest[6];
     const float qn = rsqrtf(qw * qw + qx * qx + qy * qy + qz * qz);
     const float w = qw * qn, x = qx * qn, y = qy * qn, z = qz * qn;
     const float r[9] = {1.f - 2.f * (y * y + z * z), 2.f * (x * y - w * z), 2.f * (x * z + w * y),
@@ -173,30 +184,42 @@ __device__ __forceinline__ void spawn(float* __restrict__ params, int64_t ld, fl
     float vsv = 0.f;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      const float s = expf(params[(3 + k) * ld + i]);
-      const float rv = r[k] * v[0] + r[3 + k] * v[1] + r[6 + k] * v[2];
+      const float s = expf(sp.rest[k]);
+      const float rv = r[k] * sp.v[0] + r[3 + k] * sp.v[1] + r[6 + k] * sp.v[2];
       vsv += s * s * rv * rv;
     }
     eps = eta * sqrtf(vsv);
   }
+  sp.eps = eps;
   const double o = 1.0 / (1.0 + exp(-(double)params[10 * ld + i]));
   const double h = 0.5 * o;                                   // Z15: w = 1/2 absorbed in opacity
-  const float lg = (float)(log(h) - log1p(-h));
+  sp.lg = (float)(log(h) - log1p(-h));
+}
+
+__device__ __forceinline__ void spawn_commit(float* __restrict__ params, int64_t ld, float* __restrict__ grad_S,
+                                             int64_t ldg, int64_t i, int64_t b, const Spawn& sp) {
 #pragma unroll
-  for (int k = 3; k < 14; ++k) params[k * ld + b] = params[k * ld + i];
-  params[0 * ld + b] = p0 - eps * v[0];
-  params[1 * ld + b] = p1 - eps * v[1];
-  params[2 * ld + b] = p2 - eps * v[2];
-  params[10 * ld + b] = lg;
-  params[0 * ld + i] = p0 + eps * v[0];
-  params[1 * ld + i] = p1 + eps * v[1];
-  params[2 * ld + i] = p2 + eps * v[2];
-  params[10 * ld + i] = lg;
+  for (int k = 0; k < 7; ++k) params[(3 + k) * ld + b] = sp.rest[k];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) params[(11 + k) * ld + b] = sp.rest[7 + k];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    params[a * ld + b] = sp.p[a] - sp.eps * sp.v[a];
+    params[a * ld + i] = sp.p[a] + sp.eps * sp.v[a];
+  }
+  params[10 * ld + b] = sp.lg;
+  params[10 * ld + i] = sp.lg;
 #pragma unroll
   for (int k = 0; k < 20; ++k) grad_S[k * ldg + b] = 0.f;
 }
 
-// Compactest gate (App. A.2): ||G_p / denom||_2 <= eps_grad on the position gradient.
+__device__ __forceinline__ void spawn(float* __restrict__ params, int64_t ld, float* __restrict__ grad_S,
+                                      int64_t ldg, int64_t i, int64_t b, const float* S6, float eta, float eps_abs) {
+  Spawn sp;
+  spawn_prepare(params, ld, i, S6, eta, eps_abs, sp);
+  spawn_commit(params, ld, grad_S, ldg, i, b, sp);
+}
+
 // gate 1 — compactest (App. A.2): ||G_p / denom||_2 <= eps_grad on the position gradient;
 // gate 2 — Alg. 1's "condition on G" read as 3DGS's densification condition (C24): the mean view-space
 // gradient norm (planes 0, 1 = sum of ||dL/dPi(p)||, visible views) >= eps_grad.
@@ -309,20 +332,26 @@ __global__ void __launch_bounds__(kThreads) k_densify_decide(float* __restrict__
   const int64_t base = (int64_t)tile * (kThreads * kIt);
   bool split[kIt];
   uint32_t pos[kIt];
+  float S6k[kFused ? kIt : 1][6];   // fused: S_bar kept for the offspring
 #pragma unroll
   for (int j = 0; j < kIt; ++j) {
     const int64_t i = base + (int64_t)j * kThreads + tid;
     split[j] = false;
     if (i < n) {
+      float S6[6];
       if (kSel) {
         split[j] = sel[i] != 0;
+        if (kFused && split[j]) load_sbar(grad_S, ldg, i, inv_denom, S6);
       } else {
-        float S6[6];
         load_sbar(grad_S, ldg, i, inv_denom, S6);
         const float lam = decide_lambda(S6, eps_split);
         split[j] = lam < eps_split;                   // Thm 2 / Alg. 1 P:L545 (strict, Z11)
         if (gate && split[j]) split[j] = gate_ok(grad_S, ldg, i, inv_denom, gate, eps_grad);
         if (lambda) lambda[i] = lam;
+      }
+      if (kFused) {
+#pragma unroll
+        for (int k = 0; k < 6; ++k) S6k[kFused ? j : 0][k] = S6[k];
       }
     }
     const uint32_t b = __ballot_sync(0xffffffffu, split[j]);
@@ -330,6 +359,7 @@ __global__ void __launch_bounds__(kThreads) k_densify_decide(float* __restrict__
     if (lane == 0) s_cnt[j][warp] = __popc(b);
   }
   __syncthreads();
+  __shared__ uint32_t s_agg;
   if (warp == 0) {
     constexpr int nw = kThreads / 32, nv = kIt * nw;   // <= 64 counts, two per lane, (j, warp) order
     uint32_t* cnt = &s_cnt[0][0];
@@ -344,7 +374,23 @@ __global__ void __launch_bounds__(kThreads) k_densify_decide(float* __restrict__
     if (2 * lane < nv) cnt[2 * lane] = ex;
     if (2 * lane + 1 < nv) cnt[2 * lane + 1] = ex + a;
     const uint32_t agg = __shfl_sync(0xffffffffu, inc, 31);
-    const uint64_t excl = lookback_warp(status, tile, agg);
+    if (lane == 0) {
+      publish_aggregate(status, tile, agg);        // early: successors can look past this tile
+      s_agg = agg;
+    }
+  }
+  // fused: the offspring arithmetic and parent loads overlap the look-back
+  Spawn sp[kFused ? kIt : 1];
+  if (kFused) {
+#pragma unroll
+    for (int j = 0; j < kIt; ++j) {
+      const int64_t i = base + (int64_t)j * kThreads + tid;
+      if (i < n && split[j]) spawn_prepare(params, ld, i, S6k[kFused ? j : 0], eta, eps_abs, sp[kFused ? j : 0]);
+    }
+  }
+  if (warp == 0) {
+    const uint32_t agg = __shfl_sync(0xffffffffu, s_agg, 0);
+    const uint64_t excl = lookback_published(status, tile, agg);
     if (lane == 0) {
       s_excl = excl;
       if (base + kThreads * kIt >= n) *n_split = (int64_t)(excl + agg);
@@ -360,11 +406,9 @@ __global__ void __launch_bounds__(kThreads) k_densify_decide(float* __restrict__
     mask[i] = split[j] ? 1 : 0;
     dest[i] = split[j] ? (int32_t)b : -1;  // Z24
     if (kFused) {
-      float S6[6];
-      if (split[j]) load_sbar(grad_S, ldg, i, inv_denom, S6);
 #pragma unroll
       for (int k = 14; k < 20; ++k) grad_S[k * ldg + i] = 0.f;   // Z23
-      if (split[j]) spawn(params, ld, grad_S, ldg, i, b, S6, eta, eps_abs);
+      if (split[j]) spawn_commit(params, ld, grad_S, ldg, i, b, sp[kFused ? j : 0]);
     }
   }
 }

@@ -479,3 +479,52 @@ def test_densify_budget_exact_ties(orc):
         assert np.array_equal(rz.split_mask[:n].cpu().numpy(), r["mask"]), K
         assert np.array_equal(rz.dest_index[:n].cpu().numpy(), r["dest"]), K
     assert list(np.flatnonzero(r["mask"])) == [3, 7, 8, 20, 21, 30, 33]
+
+
+def test_bench_launch_configuration_c2(orc):
+    """The exact launch bench.py times: C2 (1.0M Gaussians, 980x545), 8 views per call, capacity 2n,
+    max_instances 3 V n.  Binning of all 8 views bit-exact; images and dL-restricted gradients / S
+    of sampled windows in two of the views against the oracle."""
+    from gpu_run import to_dev
+    from paper_2505_05587_b200.pipeline import Rasterizer
+    cfg = synth.CONFIGS["C2"]
+    n, V = cfg.n, 8
+    p = synth.scene_for(cfg)
+    cams = synth.cameras_for(cfg, views=V)
+    cap = 2 * n
+    P = torch.zeros(14, cap, device="cuda"); P[:, :n] = to_dev(p)
+    rz = Rasterizer(cap, V, cfg.width, cfg.height, max_instances=int(3.0 * V * n))
+    rz.project(P, n, cams); rz.bin_sort(); rz.render_fwd()
+    decs = [orc.decide(p, c, DEFAULT) for c in cams]
+    ids, counts = expected_binning_fast(decs, cfg.width, cfg.height)
+    b = rz.binning_arrays()
+    assert b["overflow"] == 0 and b["n_instances"] == ids.size
+    assert np.array_equal(b["ids"].numpy().astype(np.int64), ids)
+    assert np.array_equal((b["ranges"][:, 1] - b["ranges"][:, 0]).numpy(), counts)
+    img = rz.image.cpu().numpy()
+    W, H = cfg.width, cfg.height
+    dl = np.zeros((V, 3, H, W), np.float32)
+    full = synth.dl_dimage(V, W, H, 17)
+    wins = {2: [(100, 60, 40, 32)], 5: [(W - 49, H - 45, 49, 45), (W // 2, H // 2, 32, 24)]}
+    for v, ws in wins.items():
+        for (x0, y0, w, h) in ws:
+            r = orc.render(p, cams[v], DEFAULT, window=(x0, y0, w, h), decision=decs[v])
+            ok = _img_close(img[v][:, y0:y0 + h, x0:x0 + w], r["image"], r["amb_px"])
+            assert ok.all()
+            win = full[v][:, y0:y0 + h, x0:x0 + w].copy()
+            win[:, r["amb_px"] != 0] = 0.0
+            dl[v][:, y0:y0 + h, x0:x0 + w] = win
+    acc = torch.zeros(20, cap, device="cuda")
+    rz.render_bwd(P, acc, dL=to_dev(dl))
+    g = acc[:, :n].cpu().numpy().astype(np.float64)
+    o = np.zeros((20, n)); a = np.zeros((20, n))
+    for v, ws in wins.items():
+        for (x0, y0, w, h) in ws:
+            r = orc.render(p, cams[v], DEFAULT, window=(x0, y0, w, h), dl_dimage=dl[v][:, y0:y0 + h, x0:x0 + w],
+                           decision=decs[v])
+            o += r["grad"]; a += r["absg"]
+    touched = np.flatnonzero(a[14:20].sum(0) > 0)
+    assert touched.size > 100
+    ok = _grad_close(g[:, touched], o[:, touched], a[:, touched], np.zeros(touched.size, np.uint8))
+    assert ok.all(), _grad_report(g[:, touched], o[:, touched], a[:, touched], ok)
+    assert np.abs(np.delete(g, np.flatnonzero(a.sum(0) > 0), axis=1)).max() == 0.0

@@ -19,7 +19,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
        "sm__throughput.avg.pct_of_peak_sustained_elapsed",
        "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread",
-       "smsp__inst_executed.sum", "sm__inst_issued.avg.pct_of_peak_sustained_active"]
+       "smsp__inst_executed.sum", "sm__inst_issued.avg.pct_of_peak_sustained_active",
+       "smsp__thread_inst_executed_per_inst_executed.ratio",             # warp efficiency (active lanes)
+       "FBSP.TriageCompute.dram__throughput.avg.pct_of_peak_sustained_elapsed",
+       "l1tex__m_l1tex2xbar_write_sectors_mem_global_op_red.sum",        # global RED (atomic) traffic
+       "l1tex__m_l1tex2xbar_write_sectors_mem_global_op_red.sum.pct_of_peak_sustained_elapsed",
+       "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom.sum"]
 
 
 def short(name: str) -> str:
@@ -43,7 +48,10 @@ def main():
             if m in hdr:
                 v = r[hdr.index(m)].replace(",", "")
                 u = units[hdr.index(m)]
-                x = float(v) if v else 0.0
+                try:
+                    x = float(v) if v else 0.0
+                except ValueError:          # "no data" / "n/a"
+                    continue
                 if u == "Kbyte":
                     x *= 1e3
                 elif u == "Mbyte":
@@ -81,8 +89,11 @@ def main():
         json.dump(traffic, f, indent=1)
     for d in recs:
         print(f"{d['kernel']:20s} {d.get('gpu__time_duration.sum', 0):8.3f} ms  DRAM "
-              f"{(d.get('dram__bytes_read.sum', 0) + d.get('dram__bytes_write.sum', 0)) / 1e6:8.1f} MB  "
-              f"issue {d.get('sm__inst_issued.avg.pct_of_peak_sustained_active', 0):5.1f}%  {d['top_stalls_pct']}")
+              f"{(d.get('dram__bytes_read.sum', 0) + d.get('dram__bytes_write.sum', 0)) / 1e6:8.1f} MB "
+              f"({d.get('FBSP.TriageCompute.dram__throughput.avg.pct_of_peak_sustained_elapsed', 0):4.1f}%)  "
+              f"issue {d.get('sm__inst_issued.avg.pct_of_peak_sustained_active', 0):5.1f}%  "
+              f"lanes {d.get('smsp__thread_inst_executed_per_inst_executed.ratio', 0):4.1f}  "
+              f"RED sectors {d.get('l1tex__m_l1tex2xbar_write_sectors_mem_global_op_red.sum', 0):.3g}  {d['top_stalls_pct']}")
 
 
 if __name__ == "__main__":

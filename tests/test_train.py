@@ -209,3 +209,15 @@ def test_training_loop_parity(orc, variant):
     if not (err <= tol).all():
         bad = np.argwhere(err > tol)
         raise AssertionError(f"{len(bad)} params off; worst {(err / tol).max():.3g} x tol at {bad[:5].tolist()}")
+
+
+def test_product_schedule_matches_oracle_schedule():
+    """pipeline.Schedule (the Trainer's host logic, no GPU needed) takes the same densify steps and
+    window restarts as oracle/train.py for several (t_start, T_split) pairs."""
+    from oracle.train import is_densify_step, window_restarts_after
+    from paper_2505_05587_b200.pipeline import Schedule
+    for t_start, t_split in ((500, 100), (4, 3), (1, 1), (7, 10), (100, 25)):
+        s = Schedule(t_start=t_start, t_split=t_split)
+        for t in range(1, 1200):
+            assert s.densify_at(t) == is_densify_step(t, t_start, t_split)
+            assert s.window_restarts_after(t) == window_restarts_after(t, t_start, t_split)

@@ -223,9 +223,8 @@ def main():
         mark(2)
         rz.bin_sort()
         mark(3)
-        rz.render_fwd()
+        rz.render_fwd_l1(tgt)                                # a3 + a4 fused (l1 gradient in the epilogue)
         mark(4)
-        rz.l1_grad(tgt)
         mark(5)
         rz.render_bwd_moments()
         mark(6)
@@ -291,8 +290,8 @@ def main():
         "restore": 2 * 16 * n,
         "project": 56 * n + V * 16 * n + 64 * n_vis,
         "bin_sort": V * 16 * n + 8 * n_vis + 20 * n_inst + 8 * tiles * V,
-        "render_fwd": 4 * n_inst + 64 * n_vis + 20 * px * V,
-        "l1_grad": 36 * px * V,
+        "render_fwd": 4 * n_inst + 64 * n_vis + 20 * px * V + 24 * px * V,   # + target read, dL write (fused a4)
+        "l1_grad": 0,
         "render_bwd": 4 * n_inst + 64 * n_vis + 28 * px * V + 48 * n_vis,
         "gauss_bwd_S": 56 * n + 4 * V * n + 96 * n_vis + 80 * n,
         "densify": 24 * n + 8 * n + 24 * n + n_split * (56 + 56 + 80),

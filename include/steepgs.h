@@ -157,6 +157,15 @@ steepgs_status steepgs_render_fwd(const steepgs_splat* splats, int64_t n, const 
                                   float* image, float* final_T, int32_t* n_contrib, int64_t* pair_counts,
                                   void* stream);
 
+/* a3 + a4 fused: the forward above, and in its epilogue the l1 gradient of steepgs_l1_grad
+ * (dL_dimage = scale * sign(image - target), loss[v] = scale * sum |image - target| if loss != NULL,
+ * the same expressions), so the image is not read back by a separate pass.  target / dL_dimage
+ * [V][3][H][W]. */
+steepgs_status steepgs_render_fwd_l1(const steepgs_splat* splats, int64_t n, const steepgs_binning* b,
+                                     const steepgs_camera* cams, int32_t V, const steepgs_raster_params* rp,
+                                     float* image, float* final_T, int32_t* n_contrib, const float* target,
+                                     float scale, float* dL_dimage, float* loss, int64_t* pair_counts, void* stream);
+
 /* ---- a4: l1 loss gradient helper (Eq. eqn:loss; C9, Z8):
  * dL_dimage = scale * sign(image - target) (sign(0) = 0) over V*count elements; if loss != NULL,
  * loss[v] (device, [V]) = scale * sum |image - target| over view v. */

@@ -256,6 +256,23 @@ steepgs_status steepgs_render_fwd(const steepgs_splat* splats, int64_t n, const 
   return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_render_fwd");
 }
 
+steepgs_status steepgs_render_fwd_l1(const steepgs_splat* splats, int64_t n, const steepgs_binning* b,
+                                     const steepgs_camera* cams, int32_t V, const steepgs_raster_params* rp,
+                                     float* image, float* final_T, int32_t* n_contrib, const float* target,
+                                     float scale, float* dL_dimage, float* loss, int64_t* pair_counts, void* stream) {
+  steepgs_status s;
+  if ((s = device_ok()) != STEEPGS_OK) return s;
+  if ((s = check_views(cams, V, nullptr)) != STEEPGS_OK) return s;
+  if ((s = check_raster(rp)) != STEEPGS_OK) return s;
+  if ((s = check_binning(b, V, cams)) != STEEPGS_OK) return s;
+  if (n < 0 || !image || !final_T || !n_contrib || !target || !dL_dimage || (n > 0 && !splats))
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "null pointer");
+  const L1Fused l1{target, dL_dimage, loss, scale};
+  const cudaError_t e = launch_render_fwd(splats, n, *b, cams[0].width, cams[0].height, raster_k(rp), image, final_T,
+                                          n_contrib, pair_counts, (cudaStream_t)stream, l1);
+  return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_render_fwd_l1");
+}
+
 steepgs_status steepgs_l1_grad(const float* image, const float* target, int32_t V, int64_t count, float scale,
                                float* dL_dimage, float* loss, void* stream) {
   steepgs_status s;

@@ -260,7 +260,8 @@ __global__ void __launch_bounds__(kThreadsFwd, 4) k_render_fwd(const steepgs_spl
                                                          float* __restrict__ image, float* __restrict__ final_T,
                                                          int32_t* __restrict__ n_contrib,
                                                          uint32_t* __restrict__ tile_last,
-                                                         unsigned long long* __restrict__ pair_counts) {
+                                                         unsigned long long* __restrict__ pair_counts,
+                                                         const L1Fused l1) {
   __shared__ Smem sm;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int tile = blockIdx.x, view = blockIdx.y;
@@ -348,15 +349,30 @@ __global__ void __launch_bounds__(kThreadsFwd, 4) k_render_fwd(const steepgs_spl
     }
     mbar_arrive(&sm.empty[s]);
   }
+  float ad = 0.0f;   // fused l1: this pixel's sum of |C - C_hat| over the channels
   if (inside) {
     const int64_t HW = (int64_t)W * H;
     const int64_t pix = (int64_t)py * W + px;
     float* img = image + (int64_t)view * 3 * HW;
-    img[pix] = __fmaf_rn(T, rk.bg[0], C0);
-    img[HW + pix] = __fmaf_rn(T, rk.bg[1], C1);
-    img[2 * HW + pix] = __fmaf_rn(T, rk.bg[2], C2);
+    const float out[3] = {__fmaf_rn(T, rk.bg[0], C0), __fmaf_rn(T, rk.bg[1], C1), __fmaf_rn(T, rk.bg[2], C2)};
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) img[ch * HW + pix] = out[ch];
     final_T[(int64_t)view * HW + pix] = T;
     n_contrib[(int64_t)view * HW + pix] = last;
+    if (l1.target) {   // a4 fused: dL/dC = scale sign(C - C_hat), the same expression as k_l1_grad
+      const int64_t o = (int64_t)view * 3 * HW + pix;
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) {
+        const float r = out[ch] - __ldg(l1.target + o + ch * HW);
+        l1.dL[o + ch * HW] = r > 0.0f ? l1.scale : (r < 0.0f ? -l1.scale : 0.0f);
+        ad += fabsf(r);
+      }
+    }
+  }
+  if (l1.loss) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ad += __shfl_xor_sync(0xffffffffu, ad, o);
+    if (lane == 0) atomicAdd(l1.loss + view, ad * l1.scale);
   }
   {
     const int wl = __reduce_max_sync(0xffffffffu, last);   // the tile's composited prefix, for the backward
@@ -602,16 +618,21 @@ __global__ void k_l1_grad(const float* __restrict__ image, const float* __restri
 
 cudaError_t launch_render_fwd(const steepgs_splat* splats, int64_t n, const steepgs_binning& b, int W, int H,
                               const RasterK& rk, float* image, float* final_T, int32_t* n_contrib,
-                              int64_t* pair_counts, cudaStream_t st) {
+                              int64_t* pair_counts, cudaStream_t st, const L1Fused& l1) {
   const int tpv = b.tiles_x * b.tiles_y;
   dim3 grid(tpv, b.V);
+  if (l1.loss) {
+    const cudaError_t e = cudaMemsetAsync(l1.loss, 0, sizeof(float) * (size_t)b.V, st);
+    if (e != cudaSuccess) return e;
+  }
   if (pair_counts)
     k_render_fwd<true><<<grid, kThreadsFwd, 0, st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
                                                   b.tiles_x, tpv, rk, image, final_T, n_contrib, b.tile_last,
-                                                  reinterpret_cast<unsigned long long*>(pair_counts));
+                                                  reinterpret_cast<unsigned long long*>(pair_counts), l1);
   else
     k_render_fwd<false><<<grid, kThreadsFwd, 0, st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
-                                                   b.tiles_x, tpv, rk, image, final_T, n_contrib, b.tile_last, nullptr);
+                                                   b.tiles_x, tpv, rk, image, final_T, n_contrib, b.tile_last, nullptr,
+                                                   l1);
   note_launch();
   return check_launch("k_render_fwd");
 }

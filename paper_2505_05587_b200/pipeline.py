@@ -112,6 +112,14 @@ class Rasterizer:
         _lib.render_fwd(self.splats, self.n, self.binning, self.cams_arr, self.V, self.rp, self.image, self.final_T,
                         self.n_contrib, pair_counts)
 
+    def render_fwd_l1(self, targets: torch.Tensor, scale: float | None = None, with_loss: bool = True,
+                      pair_counts: torch.Tensor | None = None):
+        """a3 + a4 fused: the forward writes dL/dimage = scale sign(image - target) (default scale
+        1/(3HW), the per-view mean) and the per-view loss in its epilogue."""
+        sc = 1.0 / (3 * self._HW) if scale is None else scale
+        _lib.render_fwd_l1(self.splats, self.n, self.binning, self.cams_arr, self.V, self.rp, self.image, self.final_T,
+                           self.n_contrib, targets, sc, self.dL, self.loss if with_loss else None, pair_counts)
+
     # ---- a4 ----
     def l1_grad(self, targets: torch.Tensor, with_loss: bool = True):
         count = 3 * self._HW
@@ -311,11 +319,11 @@ class Trainer:
             sh = self.sh_degree is not None
             rz.project(self.params, self.n, cams, self.sh_rest, self.sh_degree)
             rz.bin_sort(check=self.check_overflow)
-            rz.render_fwd()
             count = 3 * rz._HW
             if self.ssim_lambda is None:
-                _lib.l1_grad(rz.image, targets, rz.V, count, 1.0 / (count * rz.V * self._world()), rz.dL, rz.loss)
+                rz.render_fwd_l1(targets, 1.0 / (count * rz.V * self._world()))
             else:
+                rz.render_fwd()
                 _lib.l1_ssim_grad(rz.image, targets, self.ssim_lambda, 1.0 / (rz.V * self._world()), rz.dL, rz.loss,
                                   self.loss_ws)
             rz.render_bwd_moments()

@@ -528,3 +528,21 @@ def test_bench_launch_configuration_c2(orc):
     ok = _grad_close(g[:, touched], o[:, touched], a[:, touched], np.zeros(touched.size, np.uint8))
     assert ok.all(), _grad_report(g[:, touched], o[:, touched], a[:, touched], ok)
     assert np.abs(np.delete(g, np.flatnonzero(a.sum(0) > 0), axis=1)).max() == 0.0
+
+
+def test_render_fwd_l1_fused_equals_separate():
+    """a3 + a4 fused (steepgs_render_fwd_l1): image, dL/dimage bit-identical to render_fwd + l1_grad, the
+    per-view loss equal up to summation order."""
+    from gpu_run import run_forward, to_dev
+    cfg = synth.CONFIGS["C2"]
+    p = synth.scene_for(cfg)
+    cams = synth.cameras_for(cfg, views=2)
+    tg = to_dev(synth.targets_for(cfg, views=2))
+    rz, pt = run_forward(p, cams, DEFAULT)
+    rz.l1_grad(tg)
+    img0, dl0, loss0 = rz.image.clone(), rz.dL.clone(), rz.loss.clone()
+    rz.dL.zero_(); rz.loss.fill_(7.0)
+    rz.render_fwd_l1(tg)
+    torch.cuda.synchronize()
+    assert torch.equal(rz.image, img0) and torch.equal(rz.dL, dl0)
+    assert torch.allclose(rz.loss, loss0, rtol=1e-5, atol=0)

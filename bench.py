@@ -169,6 +169,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2")
     ap.add_argument("--views", type=int, default=8, help="views per GPU per step")
+    ap.add_argument("--sh-degree", type=int, default=None, help="f3: view-dependent SH colour of this degree")
+    ap.add_argument("--ssim", type=float, default=None, help="f3: loss (1 - l) l1 + l (1 - SSIM) with l = this")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -203,6 +205,15 @@ def main():
     grad_S = torch.zeros(20, cap, dtype=torch.float32, device=dev)
     targets = torch.from_numpy(tg_np).to(dev)
     rz = Rasterizer(cap, V, cfg.width, cfg.height, max_instances=int(3.0 * V * n), device=dev)
+    shd = args.sh_degree
+    sh_rest = grad_sh = loss_ws = None
+    if shd is not None:                                       # f3 workload: DC = planes 11-13 + rest
+        nrest = 3 * ((shd + 1) ** 2 - 1)
+        sh_rest = torch.zeros(max(nrest, 1), cap, dtype=torch.float32, device=dev)[:nrest]
+        sh_rest[:, :n] = torch.from_numpy(synth.sh_coefficients(n, shd, 4000 + int(cfg.name[1:]))).to(dev)
+        grad_sh = torch.zeros_like(sh_rest)
+    if args.ssim is not None:
+        loss_ws = torch.empty(_lib.loss_workspace_size(V, cfg.height, cfg.width), dtype=torch.uint8, device=dev)
     pair_counts = torch.zeros(2, dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream()
 
@@ -219,16 +230,24 @@ def main():
         _lib.copy_planes(params, pristine, n, 0, 3)          # undo last step's densify (positions,
         _lib.copy_planes(params, pristine, n, 10, 1)         # opacity) -- checkpoint restore, no kernel
         mark(1)
-        rz.project(params, n, cams)
+        rz.project(params, n, cams, sh_rest, shd)
         mark(2)
         rz.bin_sort()
         mark(3)
-        rz.render_fwd_l1(tgt)                                # a3 + a4 fused (l1 gradient in the epilogue)
-        mark(4)
-        mark(5)
+        if args.ssim is None:
+            rz.render_fwd_l1(tgt)                            # a3 + a4 fused (l1 gradient in the epilogue)
+            mark(4)
+            mark(5)
+        else:
+            rz.render_fwd()
+            mark(4)
+            _lib.l1_ssim_grad(rz.image, tgt, args.ssim, 1.0, rz.dL, rz.loss, loss_ws)
+            mark(5)
         rz.render_bwd_moments()
         mark(6)
-        rz.gauss_bwd(params, grad_S, accumulate=False)
+        if shd is not None:
+            rz.sh_bwd(params, grad_S, sh_rest, shd, grad_sh, 0)
+        rz.gauss_bwd(params, grad_S, accumulate=0 | (4 if shd is not None else 0))
         mark(7)
         if ws > 1:
             allreduce_accumulators(grad_S, n=n)          # 20 row slices [k, :n], NCCL
@@ -414,7 +433,9 @@ def main():
             metric=METRIC, value=round(value, 5), unit=UNIT, n_gpus=ws, steps=args.steps, warmup=args.warmup,
             ms_per_step=round(ms_step, 4), higher_is_better=False, scaling="weak", vs_baseline=None, dtype="f32",
             data="synthetic",
-            config=dict(workload=f"{cfg.name}: {cfg.cite}", n=n, width=cfg.width, height=cfg.height,
+            config=dict(workload=f"{cfg.name}: {cfg.cite}" + (f" + SH degree {shd}" if shd is not None else "")
+                        + (f" + SSIM loss (lambda {args.ssim})" if args.ssim is not None else ""),
+                        n=n, width=cfg.width, height=cfg.height,
                         views_per_gpu_per_step=V, views_per_step=V * ws, capacity=cap,
                         parallelism=f"view-sharded dp{ws}" + (" + NCCL allreduce(grads+S)" if ws > 1 else ""),
                         l2="no flush: per-step working set (params 56 MB + splats 48 B x V x n + sort/moment "

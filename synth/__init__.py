@@ -252,3 +252,9 @@ def splitting_matrices(n: int, seed: int, neg_frac: float = 0.3, scale: float = 
     a += shift[:, None, None] * np.eye(3)
     planes = np.stack([a[:, 0, 0], a[:, 0, 1], a[:, 0, 2], a[:, 1, 1], a[:, 1, 2], a[:, 2, 2]])
     return planes.astype(np.float32)
+
+
+def sh_coefficients(n: int, degree: int, seed: int, scale: float = 0.1) -> np.ndarray:
+    """Seeded SH rest coefficients [3 ((degree + 1)^2 - 1)][n] float32 (f3 workloads): N(0, scale^2)."""
+    K = (degree + 1) ** 2
+    return (_rng(seed).normal(size=(3 * (K - 1), n)) * scale).astype(np.float32)

@@ -99,6 +99,11 @@ __global__ void __launch_bounds__(256) k_project(const float* __restrict__ param
     dr[6] = 2.0 * (X * Z - W_ * Y) * ds0; dr[7] = 2.0 * (Y * Z + W_ * X) * ds1; dr[8] = (1.0 - 2.0 * (X * X + Y * Y)) * ds2;
   }
 
+  // SH rest coefficients: read once, used by every view (kSH >= 1)
+  constexpr int kRest = kSH >= 1 ? 3 * ((kSH + 1) * (kSH + 1) - 1) : 1;
+  float shc[kRest];
+#pragma unroll
+  for (int k = 0; k < kRest; ++k) shc[k] = kSH >= 1 ? __ldg(sh_rest + (int64_t)k * ld_sh + i) : 0.0f;
   for (int v = 0; v < V; ++v) {
     const steepgs_camera& c = cams.cam[v];
     const int64_t vi = (int64_t)v * n + i;
@@ -226,7 +231,7 @@ __global__ void __launch_bounds__(256) k_project(const float* __restrict__ param
       for (int ch = 0; ch < 3; ++ch) {
         float raw = 0.5f + Y[0] * col[ch];
 #pragma unroll
-        for (int k = 1; k < (kSH + 1) * (kSH + 1); ++k) raw += Y[k] * __ldg(sh_rest + (int64_t)(3 * (k - 1) + ch) * ld_sh + i);
+        for (int k = 1; k < (kSH + 1) * (kSH + 1); ++k) raw += Y[k] * shc[3 * (k - 1) + ch];
         col[ch] = fmaxf(raw, 0.0f);
       }
     }

@@ -1,7 +1,11 @@
 /* steepgs.h — C ABI of the SteepGS hot path on B200 (sm_100a only).
  *
  * Paper: arXiv 2505.05587 (SteepGS, "Steepest Density Control").  Citations P:L<n> are lines of
- * /root/reference/PAPER.md; canonical definitions C1..C16 and readings Z1..Z27 are DESIGN.md §3.
+ * /root/reference/PAPER.md; canonical definitions C1..C24 and readings Z1..Z27 are DESIGN.md §3.
+ * Hot path: project, bin_sort, render_fwd, l1_grad, render_bwd_split, densify.
+ * Widened rows (§8(f)): Algorithm-1 optimiser (adam_step, reset_moments), budget / gate variants of
+ * densify, SH colour (project_sh, sh_bwd, adam_step_planes, copy_offspring), the SSIM loss
+ * (l1_ssim_grad), the ADC baseline (densify_adc).
  *
  * Conventions for every call
  *  - Pointers are CUDA DEVICE pointers owned by the caller unless tagged [host].  The library never
@@ -38,7 +42,7 @@ typedef enum {
   STEEPGS_OK = 0,
   STEEPGS_ERR_INVALID_ARGUMENT = 1,    /* null/misaligned pointer, n < 0, V outside [1, 64],
                                           width/height <= 0 or differing across views, ld < n,
-                                          tile != 16, denom <= 0, gate not 0/1 */
+                                          tile != 16, denom <= 0, gate not 0/1/2 */
   STEEPGS_ERR_WORKSPACE_TOO_SMALL = 2, /* ws_bytes < steepgs_bin_sort_workspace_size(...) */
   STEEPGS_ERR_CAPACITY = 3,            /* densify: n + n_split > capacity (host-count variant) */
   STEEPGS_ERR_UNSUPPORTED_DEVICE = 5,  /* no CUDA device of compute capability 10.x */

@@ -74,3 +74,51 @@ def test_fuzz_full_path(orc, seed):
     gg = run_backward(rz, pt, dl)
     ok = _grad_close(gg, o, a, np.zeros(n, np.uint8))
     assert ok.all(), _grad_report(gg, o, a, ok)
+
+
+@pytest.mark.parametrize("seed", list(range(16)))
+def test_fuzz_sh(orc, seed):
+    """Random SH degree / coefficients (colour kept unclamped by a DC offset) through project_sh ->
+    render -> sh_bwd -> gauss_bwd(| 4)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from gpu_run import raster_of, to_dev
+    from test_gpu_parity import _grad_close, _grad_report
+    from paper_2505_05587_b200.pipeline import Rasterizer
+    p, cams, rp = _case(500 + seed)
+    rng = np.random.default_rng(900 + seed)
+    deg = int(rng.integers(0, 4))
+    n, V = p.shape[1], len(cams)
+    W, H = cams[0]["width"], cams[0]["height"]
+    p[11:14] = rng.uniform(0.4, 1.5, size=(3, n)).astype(np.float32)
+    rest = (rng.normal(size=(3 * ((deg + 1) ** 2 - 1), n)) * 0.1).astype(np.float32)
+    rz = Rasterizer(n, V, W, H, raster_of(rp))
+    dp = to_dev(p)
+    drest = to_dev(rest) if rest.size else torch.zeros(0, n, device="cuda")
+    rz.project(dp, n, cams, drest, deg)
+    rz.bin_sort(); rz.render_fwd()
+    dl = synth.dl_dimage(V, W, H, 2000 + seed)
+    img = rz.image.cpu().numpy()
+    o = np.zeros((20, n)); a = np.zeros((20, n)); osh = np.zeros((rest.shape[0], n))
+    rr = []
+    for v, cam in enumerate(cams):
+        r = orc.render(p, cam, rp, sh_rest=rest, sh_degree=deg)
+        ok = (np.abs(img[v] - r["image"]) <= 1e-4 * np.abs(r["image"]) + 1e-6) | (r["amb_px"][None] != 0)
+        assert ok.all(), (seed, v)
+        dl[v][:, r["amb_px"] != 0] = 0.0
+    for v, cam in enumerate(cams):
+        r = orc.render(p, cam, rp, dl_dimage=dl[v], sh_rest=rest, sh_degree=deg)
+        o += r["grad"]; a += r["absg"]
+        if rest.shape[0]:
+            osh += r["grad_sh"]
+    grad = torch.zeros(20, n, device="cuda")
+    gsh = torch.zeros(max(rest.shape[0], 0), n, device="cuda")
+    rz.render_bwd_moments(dL=to_dev(dl))
+    rz.sh_bwd(dp, grad, drest, deg, gsh, accumulate=0)
+    rz.gauss_bwd(dp, grad, accumulate=4)
+    g = grad.cpu().numpy().astype(np.float64)
+    ok = _grad_close(g, o, a, np.zeros(n, np.uint8))
+    assert ok.all(), _grad_report(g, o, a, ok)
+    if rest.shape[0]:
+        gs = gsh.cpu().numpy().astype(np.float64)
+        assert (np.abs(gs - osh) <= 2e-3 * np.abs(osh) + 1e-5 * np.abs(osh).max(axis=1, keepdims=True) + 1e-30).all()

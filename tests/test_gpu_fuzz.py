@@ -122,3 +122,29 @@ def test_fuzz_sh(orc, seed):
     if rest.shape[0]:
         gs = gsh.cpu().numpy().astype(np.float64)
         assert (np.abs(gs - osh) <= 2e-3 * np.abs(osh) + 1e-5 * np.abs(osh).max(axis=1, keepdims=True) + 1e-30).all()
+
+
+@pytest.mark.parametrize("seed", list(range(12)))
+def test_fuzz_densify(orc, seed):
+    """Random sizes (1 .. 20k, ragged against every tile size), denominators and capacities (fused
+    and two-kernel paths, just-enough and too-small) through steepgs_densify against the oracle."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from test_gpu_parity import _densify_inputs, _gpu_densify
+    rng = np.random.default_rng(3000 + seed)
+    n = int(rng.choice([1, 2, 255, 257, 2047, 2049, int(rng.integers(1, 20000))]))
+    denom = float(rng.choice([1.0, 3.0, 7.5]))
+    p, S = _densify_inputs(orc, n, 40 + seed, denom=denom)
+    lam = np.array([orc.eig_sym3(S[:, i].astype(np.float64) / np.float32(denom))[0][0] for i in range(n)])
+    ns = int((lam < -1e-6).sum())
+    cap = int(rng.choice([2 * n, n + ns, max(n, n + ns - 1)]))
+    accd = np.zeros((20, cap)); accd[14:20, :n] = S
+    pd = np.zeros((14, cap)); pd[:, :n] = p
+    r = orc.densify(pd, accd, n, cap, denom=denom)
+    rz, P, A = _gpu_densify(p, S, n, cap, denom=denom)
+    if r["n_split"] < 0:
+        assert int(rz.dens_status.item()) == 3
+        return
+    assert int(rz.dens_status.item()) == 0 and int(rz.n_split.item()) == r["n_split"] == ns
+    assert np.array_equal(rz.split_mask[:n].cpu().numpy(), r["mask"])
+    assert np.array_equal(rz.dest_index[:n].cpu().numpy(), r["dest"])

@@ -200,7 +200,7 @@ __device__ __forceinline__ void run_producer(Smem& sm, const uint32_t* __restric
         const float tq = fmaf(a.w - lmin, 1.0001f, 1e-4f);
         const float qa = a.x, qb = a.y, qc = a.z;
         const float delta = 4.0f * qa * qc - qb * qb;
-        const float inv2a = 0.5f / qa, slope = -qb * inv2a;
+        const float inv2a = __fdividef(0.5f, qa), slope = -qb * inv2a;   // approximate: covered by the padding
         uint32_t m = 0u;
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
@@ -209,7 +209,9 @@ __device__ __forceinline__ void run_producer(Smem& sm, const uint32_t* __restric
           const float dym = fminf(fmaxf(0.0f, dy0), dy1);
           const float D = 4.0f * qa * tq - delta * dym * dym;
           if (D < 0.0f) continue;
-          const float hw = sqrtf(D) * inv2a + 0.01f;
+          float sq;
+          asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(D));          // inf stays inf (smooth mode)
+          const float hw = sq * inv2a * 1.0001f + 0.01f;
           const float x0 = slope * dy0, x1 = slope * dy1;
           const float lo = gx + fminf(x0, x1) - hw, hi = gx + fmaxf(x0, x1) + hw;
           uint32_t xs = 0u;

@@ -307,6 +307,18 @@ steepgs_status steepgs_adam_step_planes(float* params, int64_t ld, int32_t plane
 steepgs_status steepgs_copy_offspring(float* arr, int64_t ld, int32_t planes, int64_t n, const int32_t* dest_index,
                                       void* stream);
 
+/* Opacity pruning kept from 3DGS's density control ("prunes invisible points"; 3DGS removes
+ * Gaussians with opacity < 0.005 at each densification).  keep iff params[10][i] (the opacity logit)
+ * >= logit_min (compared in logit space: an exact decision); new_index [n] i32 = rank among the kept
+ * (index order) or -1; n_keep [1] int64 device scalar.  workspace >= steepgs_prune_workspace_size(n). */
+steepgs_status steepgs_prune_workspace_size(int64_t n, size_t* bytes /*[host]*/);
+steepgs_status steepgs_prune_decide(const float* params, int64_t ld, int64_t n, float logit_min, int32_t* new_index,
+                                    int64_t* n_keep, void* workspace, size_t ws_bytes, void* stream);
+/* dst[k][new_index[i]] = src[k][i] for k < planes and every kept i (new_index >= 0); out of place
+ * (src != dst), so the kept columns keep their order. */
+steepgs_status steepgs_compact_planes(const float* src, int64_t ld_src, float* dst, int64_t ld_dst, int32_t planes,
+                                      int64_t n, const int32_t* new_index, void* stream);
+
 /* Copy planes [first, first + count) of a planar [*][ld] fp32 array, columns [0, n), device to
  * device (cudaMemcpy2DAsync; no kernel).  Used to checkpoint / restore Gaussian sets. */
 steepgs_status steepgs_copy_planes(float* dst, int64_t ld_dst, const float* src, int64_t ld_src, int64_t n,

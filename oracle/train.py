@@ -64,7 +64,7 @@ def window_restarts_after(t: int, t_start: int, t_split: int) -> bool:
 def train(params0, n0: int, capacity: int, batches, T: int, t_start: int, t_split: int, lr, beta1=0.9,
           beta2=0.999, eps=1e-15, rp=None, eps_split=-1e-6, eta=0.5, eps_grad=None, budget=None,
           density="sdc", adc=None, normals=None, sh_degree=None, sh_rest0=None, sh_lr=2.5e-3 / 20,
-          ssim_lambda=None, grad_gate=None):
+          ssim_lambda=None, grad_gate=None, min_opacity=None):
     """Run steps t = 1..T.  batches(t) -> (cams, targets [V][3][H][W]) for gradient steps.
     density = "adc": the 3DGS baseline (oracle/adc.py) with adc = dict(eps_adc, tau_adc, clone_step,
     scale_factor) and normals(t) -> [6][>=n] standard normals for that densify step.
@@ -72,6 +72,8 @@ def train(params0, n0: int, capacity: int, batches, T: int, t_start: int, t_spli
     coefficients trained by Adam with the single rate sh_lr and copied to offspring.
     ssim_lambda (f3): per-view loss (1 - lambda) l1 + lambda (1 - SSIM) (oracle/ssim.py), batch mean.
     grad_gate (C24): SDC splits only Gaussians whose mean view-space gradient norm >= grad_gate.
+    min_opacity: after each densify, Gaussians whose opacity logit is below the fp32 logit of
+    min_opacity are removed (3DGS's pruning), the rest keep their order.
     Returns dict(params [14][n], n, n_split, lambda_min [n] and ||G / T_split|| [n] per densify step, loss per
     gradient step); for "adc" lambda_min holds the mean view-gradient statistic and g_norm ||Sigma||_2."""
     P = np.zeros((14, capacity))
@@ -96,6 +98,7 @@ def train(params0, n0: int, capacity: int, batches, T: int, t_start: int, t_spli
             mr[:, reset] = 0.0
             vr[:, reset] = 0.0
     splits, losses, lams, gnorms = [], [], [], []
+    pruned, logits = [], []
     for t in range(1, T + 1):
         if is_densify_step(t, t_start, t_split) and density == "adc":
             d = adc_densify(P, G, st_sum, st_cnt, n, capacity, adc["eps_adc"], adc["tau_adc"], adc["clone_step"],
@@ -176,10 +179,20 @@ def train(params0, n0: int, capacity: int, batches, T: int, t_start: int, t_spli
                 adam_step_dense(SHr[:, :n], gsh, mr[:, :n], vr[:, :n], sh_lr, beta1, beta2, eps, opt_t)
             G[:, :n] += grad[0:3]
             S[:, :n] += grad[14:20]
+        if is_densify_step(t, t_start, t_split) and min_opacity is not None:
+            thr = float(np.float32(np.log(min_opacity / (1.0 - min_opacity))))
+            keep = np.flatnonzero(P[10, :n] >= thr)
+            logits.append(P[10, :n].copy())
+            for arr in (P, m, v, SHr, mr, vr):
+                if arr.shape[0]:
+                    arr[:, :keep.size] = arr[:, keep]
+                    arr[:, keep.size:] = 0.0
+            pruned.append(n - keep.size)
+            n = keep.size
         if window_restarts_after(t, t_start, t_split):
             G[:] = 0.0
             S[:] = 0.0
             st_sum[:] = 0.0
             st_cnt[:] = 0.0
     return dict(params=P[:, :n].copy(), n=n, n_split=splits, loss=losses, lambda_min=lams, g_norm=gnorms,
-                sh_rest=SHr[:, :n].copy())
+                sh_rest=SHr[:, :n].copy(), n_pruned=pruned, logits_at_prune=logits)

@@ -88,6 +88,9 @@ def lib():
             "steepgs_sh_bwd": [P, I64, I64, P, I64, I32, P, I32, P, P, I64, P, I64, I32, P],
             "steepgs_adam_step_planes": [P, I64, I32, I64, P, I64, P, P, I64, P, I64, P],
             "steepgs_copy_offspring": [P, I64, I32, I64, P, P],
+            "steepgs_prune_workspace_size": [I64, P],
+            "steepgs_prune_decide": [P, I64, I64, F, P, P, P, C.c_size_t, P],
+            "steepgs_compact_planes": [P, I64, P, I64, I32, I64, P, P],
             "steepgs_loss_workspace_size": [I32, I32, I32, P],
             "steepgs_l1_ssim_grad": [P, P, I32, I32, I32, F, F, P, P, P, C.c_size_t, P],
         }
@@ -303,6 +306,24 @@ def l1_ssim_grad(image, target, lam, scale, dL, loss, ws, stream=None):
     _check("steepgs_l1_ssim_grad", lib().steepgs_l1_ssim_grad(ptr(image), ptr(target), V, H, W, float(lam), float(scale),
                                                               ptr(dL), ptr(loss), ptr(ws), ws.numel() * ws.element_size(),
                                                               stream_ptr(stream)))
+
+
+def prune_workspace_size(n) -> int:
+    out = C.c_size_t(0)
+    _check("steepgs_prune_workspace_size", lib().steepgs_prune_workspace_size(n, C.byref(out)))
+    return int(out.value)
+
+
+def prune_decide(params, n, logit_min, new_index, n_keep, ws, stream=None):
+    _check("steepgs_prune_decide", lib().steepgs_prune_decide(ptr(params), params.shape[1], n, float(logit_min),
+                                                              ptr(new_index), ptr(n_keep), ptr(ws),
+                                                              ws.numel() * ws.element_size(), stream_ptr(stream)))
+
+
+def compact_planes(src, dst, n, new_index, stream=None):
+    assert src.shape[0] == dst.shape[0]
+    _check("steepgs_compact_planes", lib().steepgs_compact_planes(ptr(src), src.shape[1], ptr(dst), dst.shape[1],
+                                                                  src.shape[0], n, ptr(new_index), stream_ptr(stream)))
 
 
 def copy_offspring(arr, n, dest_index, stream=None):

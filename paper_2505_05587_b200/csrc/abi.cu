@@ -200,6 +200,35 @@ steepgs_status steepgs_l1_ssim_grad(const float* image, const float* target, int
   return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_l1_ssim_grad");
 }
 
+steepgs_status steepgs_prune_workspace_size(int64_t n, size_t* bytes) {
+  if (!bytes || n < 0) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "bad arguments");
+  *bytes = prune_ws_bytes(n);
+  return STEEPGS_OK;
+}
+
+steepgs_status steepgs_prune_decide(const float* params, int64_t ld, int64_t n, float logit_min, int32_t* new_index,
+                                    int64_t* n_keep, void* workspace, size_t ws_bytes, void* stream) {
+  steepgs_status s;
+  if ((s = device_ok()) != STEEPGS_OK) return s;
+  if (n < 0 || ld < n || n >= (1ll << 31) || !n_keep || !workspace || (n > 0 && (!params || !new_index)))
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "bad prune arguments");
+  if (ws_bytes < prune_ws_bytes(n)) return fail(STEEPGS_ERR_WORKSPACE_TOO_SMALL, "prune workspace too small");
+  const cudaError_t e = launch_prune_decide(params + 10 * ld, n, logit_min, new_index, n_keep, workspace, ws_bytes,
+                                            (cudaStream_t)stream);
+  return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_prune_decide");
+}
+
+steepgs_status steepgs_compact_planes(const float* src, int64_t ld_src, float* dst, int64_t ld_dst, int32_t planes,
+                                      int64_t n, const int32_t* new_index, void* stream) {
+  steepgs_status s;
+  if ((s = device_ok()) != STEEPGS_OK) return s;
+  if (n < 0 || planes < 0 || ld_src < n || ld_dst < n || (n > 0 && planes > 0 && (!src || !dst || !new_index)) ||
+      (src == dst && planes > 0 && n > 0))
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "bad compact_planes arguments (out of place only)");
+  const cudaError_t e = launch_compact_planes(src, ld_src, dst, ld_dst, planes, n, new_index, (cudaStream_t)stream);
+  return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_compact_planes");
+}
+
 steepgs_status steepgs_copy_offspring(float* arr, int64_t ld, int32_t planes, int64_t n, const int32_t* dest_index,
                                       void* stream) {
   steepgs_status s;

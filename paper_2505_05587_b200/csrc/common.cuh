@@ -45,6 +45,11 @@ cudaError_t launch_adam_planes(float* params, int64_t ld, int planes, int64_t n,
 size_t loss_ws_bytes(int V, int H, int W);
 cudaError_t launch_ssim_loss(const float* image, const float* target, int V, int H, int W, float lam, float scale,
                              float* dL, float* loss, void* ws, cudaStream_t st);
+size_t prune_ws_bytes(int64_t n);
+cudaError_t launch_prune_decide(const float* logit, int64_t n, float logit_min, int32_t* new_index, int64_t* n_keep,
+                                void* ws, size_t ws_bytes, cudaStream_t st);
+cudaError_t launch_compact_planes(const float* src, int64_t ld_src, float* dst, int64_t ld_dst, int planes, int64_t n,
+                                  const int32_t* new_index, cudaStream_t st);
 cudaError_t launch_copy_offspring(float* arr, int64_t ld, int planes, int64_t n, const int32_t* dest,
                                   cudaStream_t st);
 

@@ -230,6 +230,7 @@ class Schedule:
     tau_adc: float = 2e-3           # ADC clone/split boundary on ||Sigma||_2 = (0.01 x scene extent ~4.4)^2
     clone_step: float = 0.0         # ADC clone displacement along -G / T_split
     scale_factor: float = 0.8       # ADC split offspring scale
+    min_opacity: float | None = None  # prune Gaussians below this opacity after each densify (3DGS: 0.005)
 
     def densify_at(self, t: int) -> bool:
         return t >= self.t_start and (t - self.t_start) % self.t_split == 0
@@ -380,9 +381,37 @@ class Trainer:
             _lib.copy_offspring(self.sh_rest, n, rz.dest_index)          # offspring inherit the SH rest
             _lib.reset_moments(self.m_sh, self.v_sh, n, reset_mask, rz.n_split, reset_value)
         self.n = n + ns
-        info = dict(t=t, kind="densify", n_before=n, n_split=ns)
+        n_pruned = self._prune() if s.min_opacity is not None else 0
+        info = dict(t=t, kind="densify", n_before=n, n_split=ns, n_pruned=n_pruned)
         self.history.append(info)
         return info
+
+    def _prune(self) -> int:
+        """Opacity pruning after a densify (kept from 3DGS's density control): keep iff the
+        opacity logit >= logit(min_opacity) (an exact fp32 comparison), compact every per-Gaussian
+        buffer (params, Adam moments, SH rest and its moments) out of place, stable order."""
+        import math
+        n = self.n
+        if not hasattr(self, "_prune_ws"):
+            self._prune_ws = torch.empty(_lib.prune_workspace_size(self.cap), dtype=torch.uint8,
+                                         device=self.params.device)
+            self._new_index = torch.empty(self.cap, dtype=torch.int32, device=self.params.device)
+            self._n_keep = torch.zeros(1, dtype=torch.int64, device=self.params.device)
+        m = self.sched.min_opacity
+        logit_min = float(torch.tensor(math.log(m / (1.0 - m)), dtype=torch.float32))
+        _lib.prune_decide(self.params, n, logit_min, self._new_index, self._n_keep, self._prune_ws)
+        keep = int(self._n_keep.item())
+        if keep == n:
+            return 0
+        names = ["params", "m", "v"] + (["sh_rest", "m_sh", "v_sh"] if self.sh_rest is not None
+                                        and self.sh_rest.shape[0] > 0 else [])
+        for name in names:
+            src = getattr(self, name)
+            dst = torch.empty_like(src)
+            _lib.compact_planes(src, dst, n, self._new_index)
+            setattr(self, name, dst)
+        self.n = keep
+        return n - keep
 
     def loss(self) -> torch.Tensor:
         """Per-view losses of the last gradient step ([V], device)."""

@@ -66,7 +66,7 @@ def main():
             ("SDC + 3DGS gradient condition (C24)", dict(density="sdc", grad_gate=g3dgs)),
             ("ADC (3DGS)", dict(density="adc", eps_adc=g3dgs))]
     for name, kw in arms:
-        kw = dict(dict(t_start=500, t_split=100, tau_adc=(0.01 * 4.4) ** 2), **kw)
+        kw = dict(dict(t_start=500, t_split=100, tau_adc=(0.01 * 4.4) ** 2, min_opacity=0.005), **kw)
         sched = Schedule(**kw)
         tr = Trainer(init, n0, cap, 1, W, H, Raster(), adam, sched, seed=1)
         order = np.random.default_rng(3).permutation(np.arange(args.steps) % len(cams))

@@ -148,3 +148,29 @@ def test_fuzz_densify(orc, seed):
     assert int(rz.dens_status.item()) == 0 and int(rz.n_split.item()) == r["n_split"] == ns
     assert np.array_equal(rz.split_mask[:n].cpu().numpy(), r["mask"])
     assert np.array_equal(rz.dest_index[:n].cpu().numpy(), r["dest"])
+
+
+@pytest.mark.parametrize("n", [1, 255, 2048, 2049, 100_003])
+def test_prune_kernels(n):
+    """steepgs_prune_decide / steepgs_compact_planes against numpy: keep iff logit >= logit_min,
+    stable order, every plane moved."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2505_05587_b200 import _lib
+    rng = np.random.default_rng(n)
+    P = rng.normal(size=(14, n + 7)).astype(np.float32)
+    P[10] = rng.uniform(-8, 2, size=n + 7).astype(np.float32)
+    thr = np.float32(-5.29)
+    P[10, : n // 3] = thr                                   # exact ties are kept (>=)
+    dP = torch.from_numpy(P).cuda()
+    new_index = torch.empty(n, dtype=torch.int32, device="cuda")
+    n_keep = torch.zeros(1, dtype=torch.int64, device="cuda")
+    ws = torch.empty(_lib.prune_workspace_size(n), dtype=torch.uint8, device="cuda")
+    _lib.prune_decide(dP, n, float(thr), new_index, n_keep, ws)
+    keep = np.flatnonzero(P[10, :n] >= thr)
+    ref = np.full(n, -1); ref[keep] = np.arange(keep.size)
+    assert int(n_keep.item()) == keep.size
+    assert np.array_equal(new_index.cpu().numpy(), ref)
+    dst = torch.zeros_like(dP)
+    _lib.compact_planes(dP, dst, n, new_index)
+    assert np.array_equal(dst[:, :keep.size].cpu().numpy(), P[:, keep])

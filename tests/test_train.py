@@ -221,3 +221,56 @@ def test_product_schedule_matches_oracle_schedule():
         for t in range(1, 1200):
             assert s.densify_at(t) == is_densify_step(t, t_start, t_split)
             assert s.window_restarts_after(t) == window_restarts_after(t, t_start, t_split)
+
+
+def test_oracle_pruning_keeps_order(orc):
+    """min_opacity: with no learning and no splits, the loop's densify step removes exactly the
+    Gaussians whose opacity logit is below logit(min_opacity) and keeps the others in order."""
+    from oracle.train import train
+    cfg = synth.CONFIGS["C1"]
+    p = synth.scene_for(cfg).astype(np.float64)
+    p[10, ::5] = np.log(0.002 / 0.998)                     # every fifth Gaussian nearly transparent
+    cams = synth.ring_cameras(2, 32, 32, 3)
+    tg = synth.target_images(2, 32, 32, 4)
+    r = train(p.astype(np.float32), 64, 128, lambda t: (cams, tg), T=3, t_start=3, t_split=2, lr=(0, 0, 0, 0, 0),
+              rp=SMOOTH, eps_split=-1e30, min_opacity=0.005)
+    keep = np.flatnonzero(p[10] >= np.float32(np.log(0.005 / 0.995)))
+    assert r["n_split"] == [0] and r["n_pruned"] == [64 - keep.size] and r["n"] == keep.size
+    assert np.array_equal(r["params"], p.astype(np.float32).astype(np.float64)[:, keep])
+
+
+@pytest.mark.gpu
+def test_training_loop_with_pruning_parity(orc):
+    """Trainer with min_opacity (3DGS pruning after each densify) against oracle/train.py."""
+    _gpu()
+    from oracle.train import train
+    from gpu_run import raster_of
+    from paper_2505_05587_b200 import Adam, Schedule, Trainer
+    p, cams, tg = _scene()
+    p = p.copy()
+    p[10, ::6] = np.float32(np.log(0.002 / 0.998))
+    thr = float(np.float32(np.log(0.005 / 0.995)))
+    # the nearly transparent Gaussians have S ~ 0, i.e. lambda_min within noise of -1e-6: a larger
+    # |eps_split| keeps every split decision decisive
+    es = -1e-4
+    ora = train(p, 64, 512, _batches(cams, tg), T=10, t_start=4, t_split=3, lr=LR, eps=1e-15, rp=SMOOTH,
+                min_opacity=0.005, eps_split=es)
+    assert sum(ora["n_pruned"]) > 0
+    for lg in ora["logits_at_prune"]:
+        assert np.abs(lg - thr).min() > 1e-3                # no logit within fp32 noise of the threshold
+    for lam in ora["lambda_min"]:
+        assert np.abs(lam - es).min() > 1e-4 * np.abs(lam).max()
+    tr = Trainer(torch.from_numpy(p).cuda(), 64, 512, 2, 64, 64, raster_of(SMOOTH), Adam(LR, 0.9, 0.999, 1e-15),
+                 Schedule(4, 3, eps_split=es, min_opacity=0.005))
+    b = _batches(cams, tg)
+    for t in range(1, 11):
+        c, y = b(t)
+        tr.step(c, torch.from_numpy(np.ascontiguousarray(y)).cuda())
+    torch.cuda.synchronize()
+    assert [h["n_pruned"] for h in tr.history] == ora["n_pruned"]
+    assert [h["n_split"] for h in tr.history] == ora["n_split"] and tr.n == ora["n"]
+    got = tr.params[:, :tr.n].double().cpu().numpy()
+    lr = np.asarray(LR)[GROUP][:, None]
+    tol = 5e-3 * lr + 1e-6 * np.abs(ora["params"])
+    tol[0:3] = 2e-2 * lr[0:3] + 1e-6 * np.abs(ora["params"][0:3])
+    assert (np.abs(got - ora["params"]) <= tol).all()

@@ -244,8 +244,10 @@ class Trainer:
     allreduced every step so the Adam update stays replicated, the 6 S planes only before densify).
 
     Device state, all [plane][capacity] fp32: params (14), grad_S (20: per-step gradients + the
-    window's S), adam m/v (14 each), gacc (3: the window's position-gradient sum G).  One host sync
-    per densify step (the new Gaussian count)."""
+    window's S), adam m/v (14 each), gacc (3: the window's position-gradient sum G); optionally the
+    ADC statistic (2), SH rest coefficients with their gradients and Adam moments.  Host syncs: the
+    tile-instance count after each bin_sort (`check_overflow`, grows the buffers when a scene's
+    footprint outgrows them) and the new Gaussian count at each densify step."""
 
     def __init__(self, params0: torch.Tensor, n: int, capacity: int, V: int, width: int, height: int,
                  raster: Raster | None = None, adam: Adam | None = None, schedule: Schedule | None = None,
@@ -284,8 +286,7 @@ class Trainer:
         if ssim_lambda is not None:
             self.loss_ws = torch.empty(_lib.loss_workspace_size(V, height, width), dtype=torch.uint8, device=d)
         self.adam = adam or Adam()
-        self.ap_sh = _lib.adam_params((sh_lr,) * 5, (adam or Adam()).beta1, (adam or Adam()).beta2,
-                                      (adam or Adam()).eps)
+        self.ap_sh = _lib.adam_params((sh_lr,) * 5, self.adam.beta1, self.adam.beta2, self.adam.eps)
         self.ap = _lib.adam_params(self.adam.lr, self.adam.beta1, self.adam.beta2, self.adam.eps)
         self.sched = schedule or Schedule()
         self.group = group

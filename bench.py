@@ -171,6 +171,8 @@ def main():
     ap.add_argument("--views", type=int, default=8, help="views per GPU per step")
     ap.add_argument("--sh-degree", type=int, default=None, help="f3: view-dependent SH colour of this degree")
     ap.add_argument("--ssim", type=float, default=None, help="f3: loss (1 - l) l1 + l (1 - SSIM) with l = this")
+    ap.add_argument("--budget-frac", type=float, default=None,
+                    help="densify with the increment budget K = frac * n (App. A.2; SURVEY C4's ~10% split)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -252,7 +254,8 @@ def main():
         if ws > 1:
             allreduce_accumulators(grad_S, n=n)          # 20 row slices [k, :n], NCCL
         mark(8)
-        rz.densify(params, grad_S, n, cap, denom=float(V * ws), want_lambda=False)
+        rz.densify(params, grad_S, n, cap, denom=float(V * ws), want_lambda=False,
+                   budget=None if args.budget_frac is None else int(args.budget_frac * n))
         mark(9)
 
     def barrier():
@@ -434,7 +437,8 @@ def main():
             ms_per_step=round(ms_step, 4), higher_is_better=False, scaling="weak", vs_baseline=None, dtype="f32",
             data="synthetic",
             config=dict(workload=f"{cfg.name}: {cfg.cite}" + (f" + SH degree {shd}" if shd is not None else "")
-                        + (f" + SSIM loss (lambda {args.ssim})" if args.ssim is not None else ""),
+                        + (f" + SSIM loss (lambda {args.ssim})" if args.ssim is not None else "")
+                        + (f" + densify budget {args.budget_frac:g} n" if args.budget_frac is not None else ""),
                         n=n, width=cfg.width, height=cfg.height,
                         views_per_gpu_per_step=V, views_per_step=V * ws, capacity=cap,
                         parallelism=f"view-sharded dp{ws}" + (" + NCCL allreduce(grads+S)" if ws > 1 else ""),

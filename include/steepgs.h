@@ -320,7 +320,7 @@ steepgs_status steepgs_compact_planes(const float* src, int64_t ld_src, float* d
                                       int64_t n, const int32_t* new_index, void* stream);
 
 /* Copy planes [first, first + count) of a planar [*][ld] fp32 array, columns [0, n), device to
- * device (cudaMemcpy2DAsync; no kernel).  Used to checkpoint / restore Gaussian sets. */
+ * device (one vectorised copy kernel).  Used to checkpoint / restore Gaussian sets. */
 steepgs_status steepgs_copy_planes(float* dst, int64_t ld_dst, const float* src, int64_t ld_src, int64_t n,
                                    int32_t first, int32_t count, void* stream);
 

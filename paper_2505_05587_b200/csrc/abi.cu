@@ -435,9 +435,7 @@ steepgs_status steepgs_copy_planes(float* dst, int64_t ld_dst, const float* src,
   if (!dst || !src || n < 0 || ld_dst < n || ld_src < n || first < 0 || count < 0)
     return fail(STEEPGS_ERR_INVALID_ARGUMENT, "bad copy_planes arguments");
   if (n == 0 || count == 0) return STEEPGS_OK;
-  const cudaError_t e = cudaMemcpy2DAsync(dst + first * ld_dst, (size_t)ld_dst * 4, src + first * ld_src,
-                                          (size_t)ld_src * 4, (size_t)n * 4, (size_t)count, cudaMemcpyDeviceToDevice,
-                                          (cudaStream_t)stream);
+  const cudaError_t e = launch_copy_planes(dst, ld_dst, src, ld_src, n, first, count, (cudaStream_t)stream);
   return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_copy_planes");
 }
 

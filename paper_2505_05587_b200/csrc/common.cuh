@@ -50,6 +50,8 @@ cudaError_t launch_prune_decide(const float* logit, int64_t n, float logit_min, 
                                 void* ws, size_t ws_bytes, cudaStream_t st);
 cudaError_t launch_compact_planes(const float* src, int64_t ld_src, float* dst, int64_t ld_dst, int planes, int64_t n,
                                   const int32_t* new_index, cudaStream_t st);
+cudaError_t launch_copy_planes(float* dst, int64_t ld_dst, const float* src, int64_t ld_src, int64_t n, int first,
+                               int count, cudaStream_t st);
 cudaError_t launch_copy_offspring(float* arr, int64_t ld, int planes, int64_t n, const int32_t* dest,
                                   cudaStream_t st);
 

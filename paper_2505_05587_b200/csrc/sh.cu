@@ -8,6 +8,7 @@
 //                    into dL/dp (-> grad_S planes 0-2; k_gauss_bwd then adds the splat terms).
 //   k_adam_planes    Adam over `planes` dense planes with one learning rate (the SH rest coefficients).
 //   k_copy_offspring arr[:, dest[i]] = arr[:, i] for densified parents (extra planes follow the parent).
+//   k_copy_planes    plane-range copies (checkpoint / restore of Gaussian sets, steepgs_copy_planes).
 // Bound: HBM.
 #include <math.h>
 
@@ -155,7 +156,41 @@ __global__ void __launch_bounds__(256) k_copy_offspring(float* __restrict__ arr,
   for (int k = 0; k < planes; ++k) arr[k * ld + b] = arr[k * ld + i];
 }
 
+// dst[first + k][i] = src[first + k][i] for k < count, i < n: 16-B vector copies when both row
+// pitches and bases allow it (the planar arrays here are 256-B aligned with ld % 4 == 0)
+__global__ void __launch_bounds__(256) k_copy_planes(float* __restrict__ dst, int64_t ld_dst,
+                                                     const float* __restrict__ src, int64_t ld_src, int64_t n,
+                                                     int count, bool vec) {
+  const int k = blockIdx.y;
+  float* d = dst + k * ld_dst;
+  const float* s = src + k * ld_src;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (vec) {
+    const int64_t n4 = n / 4;
+    for (int64_t q = i; q < n4; q += stride)
+      reinterpret_cast<float4*>(d)[q] = __ldg(reinterpret_cast<const float4*>(s) + q);
+    for (int64_t q = 4 * n4 + i; q < n; q += stride) d[q] = s[q];
+  } else {
+    for (; i < n; i += stride) d[i] = s[i];
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_copy_planes(float* dst, int64_t ld_dst, const float* src, int64_t ld_src, int64_t n, int first,
+                               int count, cudaStream_t st) {
+  if (n == 0 || count == 0) return cudaSuccess;
+  float* d = dst + first * ld_dst;
+  const float* s = src + first * ld_src;
+  const bool vec = (ld_dst % 4 == 0) && (ld_src % 4 == 0) && ((uintptr_t)d % 16 == 0) && ((uintptr_t)s % 16 == 0);
+  int64_t blocks = (n / (vec ? 4 : 1) + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_copy_planes<<<dim3((unsigned)(blocks > 0 ? blocks : 1), (unsigned)count), 256, 0, st>>>(d, ld_dst, s, ld_src, n,
+                                                                                            count, vec);
+  note_launch();
+  return check_launch("k_copy_planes");
+}
 
 cudaError_t launch_sh_bwd(const float* params, int64_t ld, int64_t n, const float* sh_rest, int64_t ld_sh,
                           int sh_degree, const CamPack& cams, int V, const float* moments, float* grad_S,

@@ -24,6 +24,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kItems = 8;
 constexpr int kTileItems = kThreads * kItems;
+static_assert(kItems * (kThreads / 32) == 64, "the block scan gives each of 32 lanes two (item, warp) counts");
 
 __global__ void __launch_bounds__(kThreads) k_adc_decide(const float* __restrict__ params, int64_t ld, int64_t n,
                                                          const float* __restrict__ stats, int64_t lds,

@@ -16,6 +16,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kItems = 8;
 constexpr int kPTile = kThreads * kItems;
+static_assert(kItems * (kThreads / 32) == 64, "the block scan gives each of 32 lanes two (item, warp) counts");
 
 __global__ void __launch_bounds__(kThreads) k_prune_decide(const float* __restrict__ logit, int64_t n, float logit_min,
                                                            int32_t* __restrict__ new_index, uint64_t* status,

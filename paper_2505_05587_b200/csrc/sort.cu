@@ -24,6 +24,7 @@ namespace {
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 8;                      // items per thread per scan tile
 constexpr int kScanTile = kScanThreads * kScanItems;  // 2048
+static_assert(kScanItems * (kScanThreads / 32) == 64, "the block scan gives each of 32 lanes two (item, warp) counts");
 constexpr int kRadixThreads = 256;
 constexpr int kRadixItems = 12;
 constexpr int kRadixTile = kRadixThreads * kRadixItems;  // 3072

@@ -45,6 +45,7 @@ constexpr int kFwdProducers = 2;                    // the forward's consumers a
 constexpr int kThreadsFwd = 32 * (kConsumers + kFwdProducers);
 constexpr int kBatch = 128;                         // splats per staged batch
 constexpr int kStages = 3;                          // ring depth
+constexpr uint32_t kSuspendNs = 1000000;            // mbarrier try_wait suspend-time hint
 
 struct Buffer {
   float4 geo[kBatch];            // (mu_x - ox, mu_y - oy, Qxx', 2 Qxy')   Q' = Q log2(e)/2
@@ -72,22 +73,18 @@ __device__ __forceinline__ void mbar_init(unsigned long long* b, uint32_t count)
 __device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
 }
-// Wait for the phase with the given parity to complete.  A failed probe backs off with
-// __nanosleep(backoff_ns) so a waiting warp does not steal issue slots from working warps.
-__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity, uint32_t backoff_ns) {
-  uint32_t ok = 0;
-  const uint32_t a = saddr(b);
-  while (true) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(a), "r"(parity)
-        : "memory");
-    if (ok) break;
-    __nanosleep(backoff_ns);
-  }
+// Wait for the phase with the given parity to complete.  try_wait with a suspend-time hint parks
+// the warp in hardware until the phase completes (or the hint elapses, then it retries): a waiting
+// warp issues no polling instructions and resumes as soon as the barrier flips.
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity, uint32_t suspend_ns) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT_%=;\n}"
+      :
+      : "r"(saddr(b)), "r"(parity), "r"(suspend_ns)
+      : "memory");
 }
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -159,7 +156,7 @@ __device__ __forceinline__ void run_producer(Smem& sm, const uint32_t* __restric
   load_ids(1, gnext);
   for (int k = 0; k < nb; ++k) {
     const int s = k % kStages;
-    if (k >= kStages) mbar_wait(&sm.empty[s], ((k / kStages) & 1) ^ 1, 256);
+    if (k >= kStages) mbar_wait(&sm.empty[s], ((k / kStages) & 1) ^ 1, kSuspendNs);
     Buffer& B = sm.buf[s];
     int stop = 0;
     if (kFwd) {   // one decision per batch for all producer warps (a split decision would deadlock)
@@ -300,7 +297,7 @@ __global__ void __launch_bounds__(kThreadsFwd, 4) k_render_fwd(const steepgs_spl
   bool done = !inside, warp_done = false;
   for (int k = 0; k < nb; ++k) {
     const int s = k % kStages;
-    mbar_wait(&sm.full[s], (k / kStages) & 1, 32);
+    mbar_wait(&sm.full[s], (k / kStages) & 1, kSuspendNs);
     const Buffer& B = sm.buf[s];
     if (B.stop) break;
     if (!warp_done) {
@@ -483,7 +480,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
   const int e2 = lane & (kChunk - 1), half = lane >> 4;
   for (int k = 0; k < nb; ++k) {
     const int s = k % kStages;
-    mbar_wait(&sm.full[s], (k / kStages) & 1, 32);
+    mbar_wait(&sm.full[s], (k / kStages) & 1, kSuspendNs);
     const Buffer& B = sm.buf[s];
     uint8_t* lst = sm.buf[s].list[warp];
     const int nl = build_list(B, lst, warp, lane, wmax - B.base);   // only entries before the warp's prefix end

@@ -396,20 +396,27 @@ constexpr int kChunk = 16;   // list entries per backward chunk (phase 1 -> phas
 struct BwdScratch {
   float2 wat[kConsumers][kChunk][33];  // (dL/dsigma * sigma, alpha T) per (entry, pixel); padded rows
   uint32_t cmask[kConsumers][kChunk];  // contributing pixels of each entry (ballot)
-  float4 pix[kConsumers][32];          // per pixel: tile-relative centre (x, y), dL/dC_r, dL/dC_g
+  float4 pix[kConsumers][32];          // per pixel: centre relative to the warp's 8x4 sub-block
+                                       // centre (x', y'), dL/dC_r, dL/dC_g
   float pdl2[kConsumers][32];          // per pixel: dL/dC_b
+  float2 emean[kConsumers][kChunk];    // per chunk entry: the splat mean (tile-relative)
+  float* eptr[kConsumers][kChunk];     // per chunk entry: &moments[view][gid][0]
 };
 
 __device__ __forceinline__ void red_v4(float* p, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
 }
 
-// Backward.  Per consumer warp and chunk of <= 16 list entries (back to front):
-//   phase 1 (pixel-parallel): each lane runs its pixel's recursion over the chunk and leaves
+// Backward.  Per consumer warp and chunk of 16 list entries (back to front; a chunk continues
+// across batch boundaries, so only the tile's last chunk is partial):
+//   phase 1 (pixel-parallel): each lane runs its pixel's recursion over the entries and leaves
 //     w = dL/dsigma * sigma and alpha T in shared memory, plus a ballot of contributing pixels;
-//   phase 2 (splat-parallel): lanes e and e + 16 own entry e and sum its 9 moments over the
-//     contributing pixels (even / odd rank), combine with one xor-16 shuffle per value, and
-//     add them with two 16-B + one 4-B vector REDs.
+//     the entry's splat mean and moment address are kept beside the chunk (the batch buffer may
+//     be released before the chunk is reduced);
+//   phase 2 (splat-parallel): lanes e and e + 16 own entry e and sum its raw moments over the
+//     contributing pixels (even / odd rank) in the sub-block frame (x', y'), combine with one
+//     xor-16 shuffle per value, recentre on the splat mean (d = (x', y') + (u, v)) and add the 9
+//     moments with two 16-B + one 4-B vector REDs.
 // No per-(warp, splat) cross-lane reduction tree: the reduction costs O(contributing pairs).
 __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat* __restrict__ splats,
                                                          const uint32_t* __restrict__ ids,
@@ -442,7 +449,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
     dl0 = dl[pix]; dl1 = dl[HW + pix]; dl2 = dl[2 * HW + pix];
   }
   if (warp < kConsumers) {
-    sc.pix[warp][lane] = make_float4((float)lx + 0.5f, (float)ly + 0.5f, dl0, dl1);
+    sc.pix[warp][lane] = make_float4((float)(lane & 7) - 3.5f, (float)(lane >> 3) - 1.5f, dl0, dl1);
     sc.pdl2[warp][lane] = dl2;
   }
   // list prefix any pixel of the tile composited (stored by the forward), so the producer starts at
@@ -477,7 +484,69 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
   uint32_t* scm = sc.cmask[warp];
   const float4* spix = sc.pix[warp];
   const float* sdl2 = sc.pdl2[warp];
+  float2* smean = sc.emean[warp];
+  float** sptr = sc.eptr[warp];
   const int e2 = lane & (kChunk - 1), half = lane >> 4;
+  const float cxw = (float)(8 * (warp & 1) + 4), cyw = (float)(4 * (warp >> 1) + 2);   // sub-block centre
+  // ---- phase 2 over the chunk's first `ne` rows ----
+  auto reduce_chunk = [&](int ne) {
+    __syncwarp();
+    float acc[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) acc[q] = 0.0f;
+    const bool valid = e2 < ne;
+    uint32_t full_bits = 0u;
+    if (valid) {
+      full_bits = scm[e2];
+      // the two lanes of an entry take the contributing pixels of even / odd rank (prefix parity)
+      uint32_t x = full_bits;
+      x ^= x << 1; x ^= x << 2; x ^= x << 4; x ^= x << 8; x ^= x << 16;
+      const uint32_t odd = full_bits & (x << 1);
+      uint32_t bits = half ? odd : (full_bits & ~odd);
+      const float2* row = swat[e2];
+      auto add = [&](float w, float at, float4 d, float dl2p) {   // raw moments in the sub-block frame
+        const float wx = w * d.x, wy = w * d.y;
+        acc[0] += w;
+        acc[1] += wx;
+        acc[2] += wy;
+        acc[3] = fmaf(wx, d.x, acc[3]);
+        acc[4] = fmaf(wx, d.y, acc[4]);
+        acc[5] = fmaf(wy, d.y, acc[5]);
+        acc[6] = fmaf(at, d.z, acc[6]);
+        acc[7] = fmaf(at, d.w, acc[7]);
+        acc[8] = fmaf(at, dl2p, acc[8]);
+      };
+      while (bits) {        // two pixels per iteration; a missing second one adds zeros
+        const int pa = 31 - __clz(bits);
+        bits ^= 1u << pa;
+        const bool two = bits != 0u;
+        const int pb = two ? 31 - __clz(bits) : pa;
+        bits &= ~(two ? (1u << pb) : 0u);
+        const float2 wa = row[pa], wb = row[pb];
+        const float4 da = spix[pa], db = spix[pb];
+        const float la = sdl2[pa], lb = sdl2[pb];
+        add(wa.x, wa.y, da, la);
+        add(two ? wb.x : 0.0f, two ? wb.y : 0.0f, db, lb);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 9; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], 16);
+    if (valid && half == 0 && full_bits) {
+      const float2 gm = smean[e2];
+      const float u = cxw - gm.x, v = cyw - gm.y;   // d = (x', y') + (u, v)
+      const float S0 = acc[0], Sx = acc[1], Sy = acc[2];
+      const float m1x = fmaf(u, S0, Sx), m1y = fmaf(v, S0, Sy);
+      const float Mxx = fmaf(u, fmaf(u, S0, 2.0f * Sx), acc[3]);
+      const float Mxy = fmaf(u, m1y, fmaf(v, Sx, acc[4]));
+      const float Myy = fmaf(v, fmaf(v, S0, 2.0f * Sy), acc[5]);
+      float* mp = sptr[e2];
+      red_v4(mp, S0, m1x, m1y, Mxx);
+      red_v4(mp + 4, Mxy, Myy, acc[6], acc[7]);
+      atomicAdd(mp + 8, acc[8]);
+    }
+    __syncwarp();
+  };
+  int fill = 0;   // rows of the current chunk already filled
   for (int k = 0; k < nb; ++k) {
     const int s = k % kStages;
     mbar_wait(&sm.full[s], (k / kStages) & 1, kSuspendNs);
@@ -485,10 +554,17 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
     uint8_t* lst = sm.buf[s].list[warp];
     const int nl = build_list(B, lst, warp, lane, wmax - B.base);   // only entries before the warp's prefix end
     const int lim = last - B.base;                          // this pixel composited list positions < last
-    for (int t_hi = nl; t_hi > 0; t_hi -= kChunk) {
-      const int t_lo = max(0, t_hi - kChunk);
+    for (int t_hi = nl; t_hi > 0;) {
+      const int m = min(t_hi, kChunk - fill);
+      const int t_lo = t_hi - m;
+      const int r0 = fill - t_lo;                           // row of list entry t = r0 + t
+      if (lane < m) {
+        const int j = lst[t_lo + lane];
+        smean[fill + lane] = *reinterpret_cast<const float2*>(&B.geo[j]);
+        sptr[fill + lane] = B.mptr[j];
+      }
       // ---- phase 1: pixel-parallel recursion over entries t_hi-1 .. t_lo ----
-      // Two entries per iteration: both pair tests are evaluated before the (serial) recursion, so
+      // Four entries per iteration: the pair tests are evaluated before the (serial) recursion, so
       // their shared-memory loads and arithmetic overlap.
       auto recurse = [&](bool hit, float ee, int j, int e) {
         if (hit) {
@@ -518,72 +594,26 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
           ee[u] = pair_e(__fsub_rn(fx, g.x), __fsub_rn(fy, g.y), g, p);
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) recurse(jj[u] < lim && ee[u] >= lmin, ee[u], jj[u], t - u - t_lo);
+        for (int u = 0; u < 4; ++u) recurse(jj[u] < lim && ee[u] >= lmin, ee[u], jj[u], r0 + t - u);
       }
       for (; t >= t_lo; --t) {
         const int ja = lst[t];
         const float4 ga = B.geo[ja];
         const float4 pa = B.par[ja];
         const float ea = pair_e(__fsub_rn(fx, ga.x), __fsub_rn(fy, ga.y), ga, pa);
-        recurse(ja < lim && ea >= lmin, ea, ja, t - t_lo);
+        recurse(ja < lim && ea >= lmin, ea, ja, r0 + t);
       }
-      __syncwarp();
-      // ---- phase 2: splat-parallel sums (lanes e2 and e2 + 16 own entry e2) ----
-      const int ne = t_hi - t_lo;
-      float acc[9];
-#pragma unroll
-      for (int q = 0; q < 9; ++q) acc[q] = 0.0f;
-      const bool valid = e2 < ne;
-      int j2 = 0;
-      uint32_t full_bits = 0u;
-      if (valid) {
-        j2 = lst[t_lo + e2];
-        full_bits = scm[e2];
-        // the two lanes of an entry take the contributing pixels of even / odd rank (prefix parity)
-        uint32_t x = full_bits;
-        x ^= x << 1; x ^= x << 2; x ^= x << 4; x ^= x << 8; x ^= x << 16;
-        const uint32_t odd = full_bits & (x << 1);
-        uint32_t bits = half ? odd : (full_bits & ~odd);
-        const float2 gm = *reinterpret_cast<const float2*>(&B.geo[j2]);
-        const float2* row = swat[e2];
-        auto add = [&](float w, float at, float4 d, float dl2p) {
-          const float dx = d.x - gm.x, dy = d.y - gm.y;
-          const float wdx = w * dx, wdy = w * dy;
-          acc[0] += w;
-          acc[1] += wdx;
-          acc[2] += wdy;
-          acc[3] = fmaf(wdx, dx, acc[3]);
-          acc[4] = fmaf(wdx, dy, acc[4]);
-          acc[5] = fmaf(wdy, dy, acc[5]);
-          acc[6] = fmaf(at, d.z, acc[6]);
-          acc[7] = fmaf(at, d.w, acc[7]);
-          acc[8] = fmaf(at, dl2p, acc[8]);
-        };
-        while (bits) {        // two pixels per iteration; a missing second one adds zeros
-          const int pa = 31 - __clz(bits);
-          bits ^= 1u << pa;
-          const bool two = bits != 0u;
-          const int pb = two ? 31 - __clz(bits) : pa;
-          bits &= ~(two ? (1u << pb) : 0u);
-          const float2 wa = row[pa], wb = row[pb];
-          const float4 da = spix[pa], db = spix[pb];
-          const float la = sdl2[pa], lb = sdl2[pb];
-          add(wa.x, wa.y, da, la);
-          add(two ? wb.x : 0.0f, two ? wb.y : 0.0f, db, lb);
-        }
+      fill += m;
+      t_hi = t_lo;
+      if (fill == kChunk) {
+        reduce_chunk(kChunk);
+        fill = 0;
       }
-#pragma unroll
-      for (int q = 0; q < 9; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], 16);
-      if (valid && half == 0 && full_bits) {
-        float* mp = B.mptr[j2];
-        red_v4(mp, acc[0], acc[1], acc[2], acc[3]);
-        red_v4(mp + 4, acc[4], acc[5], acc[6], acc[7]);
-        atomicAdd(mp + 8, acc[8]);
-      }
-      __syncwarp();
     }
+    __syncwarp();
     mbar_arrive(&sm.empty[s]);
   }
+  if (fill > 0) reduce_chunk(fill);
 }
 
 __global__ void k_l1_grad(const float* __restrict__ image, const float* __restrict__ target, int64_t count,

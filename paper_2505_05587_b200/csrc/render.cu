@@ -573,10 +573,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
           const float4 c = B.col[j];
           const float om = 1.0f - alpha;
           T = T * rcp_approx(om);                           // T_i (before this splat)
-          const float gsum = dl0 * (c.x - B0) + dl1 * (c.y - B1) + dl2 * (c.z - B2);
-          B0 = alpha * c.x + om * B0;
-          B1 = alpha * c.y + om * B1;
-          B2 = alpha * c.z + om * B2;
+          const float d0 = c.x - B0, d1 = c.y - B1, d2 = c.z - B2;   // colour minus the colour behind
+          const float gsum = fmaf(dl2, d2, fmaf(dl1, d1, dl0 * d0));
+          B0 = fmaf(alpha, d0, B0);                         // B <- alpha c + (1 - alpha) B
+          B1 = fmaf(alpha, d1, B1);
+          B2 = fmaf(alpha, d2, B2);
           swat[e][lane] = make_float2(T * gsum * sigma, alpha * T);  // dL/dalpha * sigma (Z3), alpha T
         }
         const uint32_t bal = __ballot_sync(0xffffffffu, hit);

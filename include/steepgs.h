@@ -114,6 +114,9 @@ typedef struct {
   uint32_t* tile_last;          /* [V * tiles_x * tiles_y]: zeroed by bin_sort; render_fwd stores the
                                    tile's composited list prefix (max over its pixels of n_contrib),
                                    which render_bwd reads: the backward needs the forward's binning */
+  uint8_t* inst_mask;           /* [max_instances]: render_fwd stores, per tile instance it stages,
+                                   the 8-bit mask of the tile's 8x4 sub-blocks the splat's alpha
+                                   support reaches; render_bwd reads it instead of recomputing */
   int64_t max_instances;
   int32_t tiles_x, tiles_y, V;
 } steepgs_binning;

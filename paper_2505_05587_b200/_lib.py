@@ -50,6 +50,7 @@ class AdamParams(C.Structure):
 class Binning(C.Structure):
     _fields_ = [("ids", C.c_void_p), ("ranges", C.c_void_p), ("n_instances", C.c_void_p),
                 ("n_visible", C.c_void_p), ("overflow", C.c_void_p), ("tile_last", C.c_void_p),
+                ("inst_mask", C.c_void_p),
                 ("max_instances", C.c_int64),
                 ("tiles_x", C.c_int32), ("tiles_y", C.c_int32), ("V", C.c_int32)]
 

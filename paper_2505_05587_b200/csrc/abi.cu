@@ -76,7 +76,8 @@ static steepgs_status check_raster(const steepgs_raster_params* rp) {
 static bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
 static steepgs_status check_binning(const steepgs_binning* b, int32_t V, const steepgs_camera* cams) {
-  if (!b || !b->ids || !b->ranges || !b->n_instances) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "binning null");
+  if (!b || !b->ids || !b->ranges || !b->n_instances || !b->tile_last || !b->inst_mask)
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "binning null");
   const int tx = (cams[0].width + kTile - 1) / kTile, ty = (cams[0].height + kTile - 1) / kTile;
   if (b->V != V || b->tiles_x != tx || b->tiles_y != ty)
     return fail(STEEPGS_ERR_INVALID_ARGUMENT, "binning does not match the views of this call");

@@ -122,17 +122,19 @@ template <bool kFwd, int kProd, class BatchOf>
 __device__ __forceinline__ void run_producer(Smem& sm, const uint32_t* __restrict__ ids,
                                              const steepgs_splat* __restrict__ vs, uint32_t first, int nb,
                                              BatchOf batch_of, double ox, double oy, float* mom_view, float lmin,
-                                             int pw, int lane) {
+                                             uint8_t* __restrict__ inst_mask, int pw, int lane) {
   // producer warp pw of kProd stages the batch slots kk = (q kProd + pw) * 32 + lane
   constexpr int kQ = kBatch / 32 / kProd;
   uint32_t gcur[kQ], gnext[kQ];
-  auto load_ids = [&](int k, uint32_t* g) {
+  uint32_t mcur[kQ], mnext[kQ];   // backward: the forward's sub-block masks, prefetched with the ids
+  auto load_ids = [&](int k, uint32_t* g, uint32_t* mk) {
     int rel = 0, cnt = 0;
     if (k < nb) batch_of(k, rel, cnt);
 #pragma unroll
     for (int q = 0; q < kQ; ++q) {
       const int kk = (q * kProd + pw) * 32 + lane;
       g[q] = kk < cnt ? __ldg(ids + first + rel + kk) : 0u;
+      if (!kFwd) mk[q] = kk < cnt ? (uint32_t)__ldg(inst_mask + first + rel + kk) : 0u;
     }
   };
   auto issue = [&](int k, const uint32_t* g) {
@@ -145,15 +147,15 @@ __device__ __forceinline__ void run_producer(Smem& sm, const uint32_t* __restric
         if (kk < cnt) {
           const uint4* src = reinterpret_cast<const uint4*>(vs + g[q]);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) cp_async16(&sm.raw[j][kk], src + j);
+          for (int j = 0; j < (kFwd ? 4 : 3); ++j) cp_async16(&sm.raw[j][kk], src + j);   // bwd: no extents
         }
       }
     }
     cp_async_commit();
   };
-  load_ids(0, gcur);
+  load_ids(0, gcur, mcur);
   issue(0, gcur);
-  load_ids(1, gnext);
+  load_ids(1, gnext, mnext);
   for (int k = 0; k < nb; ++k) {
     const int s = k % kStages;
     if (k >= kStages) mbar_wait(&sm.empty[s], ((k / kStages) & 1) ^ 1, kSuspendNs);
@@ -180,12 +182,16 @@ __device__ __forceinline__ void run_producer(Smem& sm, const uint32_t* __restric
         const double2 mean = *reinterpret_cast<const double2*>(&sm.raw[0][kk]);
         const float4 a = *reinterpret_cast<const float4*>(&sm.raw[1][kk]);   // conic', log2 o
         const float4 b = *reinterpret_cast<const float4*>(&sm.raw[2][kk]);   // rgb, o
-        const float4 c = *reinterpret_cast<const float4*>(&sm.raw[3][kk]);   // extents, tau
         const float gx = (float)(mean.x - ox), gy = (float)(mean.y - oy);
         B.geo[kk] = make_float4(gx, gy, a.x, a.y);
         B.par[kk] = make_float4(a.z, a.w, 0.0f, 0.0f);
         B.col[kk] = make_float4(b.x, b.y, b.z, 0.0f);
         if (mom_view) B.mptr[kk] = mom_view + (size_t)gcur[q] * 12;
+        if (!kFwd) {   // the backward reuses the forward's masks (same splat, same tile)
+          B.mask[kk] = mcur[q];
+          continue;
+        }
+        const float4 c = *reinterpret_cast<const float4*>(&sm.raw[3][kk]);   // extents, tau
         uint32_t xb = 0u;
 #pragma unroll
         for (int t = 0; t < 2; ++t)
@@ -217,6 +223,7 @@ __device__ __forceinline__ void run_producer(Smem& sm, const uint32_t* __restric
           m |= (xs & xb) << (2 * t);
         }
         B.mask[kk] = m;
+        inst_mask[first + rel + kk] = (uint8_t)m;   // for the backward's producer
       }
     }
     if (pw == 0 && lane == 0) {
@@ -227,9 +234,12 @@ __device__ __forceinline__ void run_producer(Smem& sm, const uint32_t* __restric
     mbar_arrive(&sm.full[s]);
     if (stop) break;
 #pragma unroll
-    for (int q = 0; q < kQ; ++q) gcur[q] = gnext[q];
+    for (int q = 0; q < kQ; ++q) {
+      gcur[q] = gnext[q];
+      mcur[q] = mnext[q];
+    }
     issue(k + 1, gcur);
-    load_ids(k + 2, gnext);
+    load_ids(k + 2, gnext, mnext);
   }
   cp_async_wait_all();
 }
@@ -259,6 +269,7 @@ __global__ void __launch_bounds__(kThreadsFwd, 4) k_render_fwd(const steepgs_spl
                                                          float* __restrict__ image, float* __restrict__ final_T,
                                                          int32_t* __restrict__ n_contrib,
                                                          uint32_t* __restrict__ tile_last,
+                                                         uint8_t* __restrict__ inst_mask,
                                                          unsigned long long* __restrict__ pair_counts,
                                                          const L1Fused l1) {
   __shared__ Smem sm;
@@ -281,7 +292,7 @@ __global__ void __launch_bounds__(kThreadsFwd, 4) k_render_fwd(const steepgs_spl
     const int len = (int)(rg.y - rg.x);
     run_producer<true, kFwdProducers>(sm, ids, splats + (int64_t)view * n, rg.x, nb,
                                       [len](int k, int& rel, int& cnt) { rel = k * kBatch; cnt = min(len - rel, kBatch); },
-                                      ox, oy, nullptr, __log2f(rk.alpha_min), warp - kConsumers, lane);
+                                      ox, oy, nullptr, __log2f(rk.alpha_min), inst_mask, warp - kConsumers, lane);
     return;
   }
 
@@ -426,6 +437,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
                                                          const int32_t* __restrict__ n_contrib,
                                                          const float* __restrict__ dL_dimage,
                                                          const uint32_t* __restrict__ tile_last,
+                                                         uint8_t* __restrict__ inst_mask,
                                                          float* __restrict__ moments) {
   extern __shared__ __align__(16) unsigned char dsmem[];
   Smem& sm = *reinterpret_cast<Smem*>(dsmem);
@@ -471,7 +483,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
                           rel = (nb - 1 - k) * kBatch;
                           cnt = min(L - rel, kBatch);
                         },
-                        ox, oy, moments + (int64_t)view * n * 12, __log2f(rk.alpha_min), 0, lane);
+                        ox, oy, moments + (int64_t)view * n * 12, __log2f(rk.alpha_min), inst_mask, 0, lane);
     return;
   }
 
@@ -657,11 +669,11 @@ cudaError_t launch_render_fwd(const steepgs_splat* splats, int64_t n, const stee
   }
   if (pair_counts)
     k_render_fwd<true><<<grid, kThreadsFwd, 0, st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
-                                                  b.tiles_x, tpv, rk, image, final_T, n_contrib, b.tile_last,
+                                                  b.tiles_x, tpv, rk, image, final_T, n_contrib, b.tile_last, b.inst_mask,
                                                   reinterpret_cast<unsigned long long*>(pair_counts), l1);
   else
     k_render_fwd<false><<<grid, kThreadsFwd, 0, st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
-                                                   b.tiles_x, tpv, rk, image, final_T, n_contrib, b.tile_last, nullptr,
+                                                   b.tiles_x, tpv, rk, image, final_T, n_contrib, b.tile_last, b.inst_mask, nullptr,
                                                    l1);
   note_launch();
   return check_launch("k_render_fwd");
@@ -695,7 +707,7 @@ cudaError_t launch_render_bwd(const steepgs_splat* splats, const steepgs_binning
     attr_set = true;
   }
   k_render_bwd<<<grid, kThreads, smem, st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
-                                          b.tiles_x, tpv, rk, final_T, n_contrib, dL_dimage, b.tile_last, moments);
+                                          b.tiles_x, tpv, rk, final_T, n_contrib, dL_dimage, b.tile_last, b.inst_mask, moments);
   note_launch();
   return check_launch("k_render_bwd");
 }

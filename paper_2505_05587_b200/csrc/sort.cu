@@ -376,7 +376,7 @@ __global__ void k_ranges(const uint32_t* __restrict__ keys, const int64_t* n_ins
 inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
-  size_t keysA, valsA, keysB, valsB, recs, keysC, valsC, keysD, valsD, ranges, tile_last;
+  size_t keysA, valsA, keysB, valsB, recs, keysC, valsC, keysD, valsD, ranges, tile_last, inst_mask;
   size_t st_compact, st_dup, st_depth, st_tile, counters, hist, scalars, end;
   size_t zero_begin, zero_end;
   int64_t items;
@@ -402,6 +402,7 @@ Layout layout(int64_t n, int V, int tiles_total, int64_t max_instances) {
   L.keysD = take(4 * (size_t)max_instances);
   L.valsD = take(4 * (size_t)max_instances);
   L.ranges = take(8 * (size_t)tiles_total);
+  L.inst_mask = take((size_t)max_instances);
   L.zero_begin = o;
   L.tile_last = take(4 * (size_t)tiles_total);
   L.st_compact = take(8 * (size_t)L.compact_tiles);
@@ -462,6 +463,7 @@ cudaError_t launch_bin_sort(const uint32_t* depth_key, const uint32_t* tile_rect
   out->n_visible = n_visible;
   out->overflow = overflow;
   out->tile_last = U32(L.tile_last);
+  out->inst_mask = reinterpret_cast<uint8_t*>(w + L.inst_mask);
   out->max_instances = max_instances;
   out->tiles_x = tiles_x;
   out->tiles_y = tiles_y;

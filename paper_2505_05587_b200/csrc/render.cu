@@ -44,7 +44,8 @@ constexpr int kThreads = 32 * (kConsumers + 1);     // + 1 producer warp (backwa
 constexpr int kFwdProducers = 2;                    // the forward's consumers are faster: 2 producer warps
 constexpr int kThreadsFwd = 32 * (kConsumers + kFwdProducers);
 constexpr int kBatch = 128;                         // splats per staged batch
-constexpr int kStages = 3;                          // ring depth
+constexpr int kStages = 3;                          // ring depth (backward: bounded by shared memory)
+constexpr int kFwdStages = 4;                       // forward ring depth (slack for unequal consumer warps)
 constexpr uint32_t kSuspendNs = 1000000;            // mbarrier try_wait suspend-time hint
 
 struct Buffer {
@@ -58,13 +59,16 @@ struct Buffer {
   int stop;                      // 1: no more batches (forward early termination)
 };
 
-struct Smem {
-  Buffer buf[kStages];
+template <int kS>
+struct SmemT {
+  Buffer buf[kS];
   uint4 raw[4][kBatch];          // producer staging: the next batch's 64-B records (cp.async), SoA by 16 B
-  unsigned long long full[kStages], empty[kStages];
+  unsigned long long full[kS], empty[kS];
   int done_warps;
   int stop_flag[2];              // forward: the producers' shared early-exit decision (double-buffered)
 };
+using Smem = SmemT<kStages>;
+using SmemFwd = SmemT<kFwdStages>;
 
 __device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long* b, uint32_t count) {
@@ -118,8 +122,8 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // round trip once it runs ahead.  Staging a record is then two fp64 subtractions and eight
 // interval tests of the padded extents against the 8x4 sub-blocks.
 // kFwd: stop early once every consumer warp has terminated (forward early exit).
-template <bool kFwd, int kProd, class BatchOf>
-__device__ __forceinline__ void run_producer(Smem& sm, const uint32_t* __restrict__ ids,
+template <bool kFwd, int kProd, int kS, class BatchOf>
+__device__ __forceinline__ void run_producer(SmemT<kS>& sm, const uint32_t* __restrict__ ids,
                                              const steepgs_splat* __restrict__ vs, uint32_t first, int nb,
                                              BatchOf batch_of, double ox, double oy, float* mom_view, float lmin,
                                              uint8_t* __restrict__ inst_mask, int pw, int lane) {
@@ -157,8 +161,8 @@ __device__ __forceinline__ void run_producer(Smem& sm, const uint32_t* __restric
   issue(0, gcur);
   load_ids(1, gnext, mnext);
   for (int k = 0; k < nb; ++k) {
-    const int s = k % kStages;
-    if (k >= kStages) mbar_wait(&sm.empty[s], ((k / kStages) & 1) ^ 1, kSuspendNs);
+    const int s = k % kS;
+    if (k >= kS) mbar_wait(&sm.empty[s], ((k / kS) & 1) ^ 1, kSuspendNs);
     Buffer& B = sm.buf[s];
     int stop = 0;
     if (kFwd) {   // one decision per batch for all producer warps (a split decision would deadlock)
@@ -272,7 +276,7 @@ __global__ void __launch_bounds__(kThreadsFwd, 4) k_render_fwd(const steepgs_spl
                                                          uint8_t* __restrict__ inst_mask,
                                                          unsigned long long* __restrict__ pair_counts,
                                                          const L1Fused l1) {
-  __shared__ Smem sm;
+  __shared__ SmemFwd sm;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int tile = blockIdx.x, view = blockIdx.y;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
@@ -280,7 +284,7 @@ __global__ void __launch_bounds__(kThreadsFwd, 4) k_render_fwd(const steepgs_spl
   const uint2 rg = ranges[(int64_t)view * tiles_per_view + tile];
   const int nb = (int)((rg.y - rg.x + kBatch - 1) / kBatch);
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kFwdStages; ++s) {
       mbar_init(&sm.full[s], 32 * kFwdProducers);
       mbar_init(&sm.empty[s], 32 * kConsumers);
     }
@@ -290,7 +294,7 @@ __global__ void __launch_bounds__(kThreadsFwd, 4) k_render_fwd(const steepgs_spl
 
   if (warp >= kConsumers) {  // ---------------- producers ----------------
     const int len = (int)(rg.y - rg.x);
-    run_producer<true, kFwdProducers>(sm, ids, splats + (int64_t)view * n, rg.x, nb,
+    run_producer<true, kFwdProducers, kFwdStages>(sm, ids, splats + (int64_t)view * n, rg.x, nb,
                                       [len](int k, int& rel, int& cnt) { rel = k * kBatch; cnt = min(len - rel, kBatch); },
                                       ox, oy, nullptr, __log2f(rk.alpha_min), inst_mask, warp - kConsumers, lane);
     return;
@@ -307,8 +311,8 @@ __global__ void __launch_bounds__(kThreadsFwd, 4) k_render_fwd(const steepgs_spl
   int last = 0, ncomp = 0, neval = 0;
   bool done = !inside, warp_done = false;
   for (int k = 0; k < nb; ++k) {
-    const int s = k % kStages;
-    mbar_wait(&sm.full[s], (k / kStages) & 1, kSuspendNs);
+    const int s = k % kFwdStages;
+    mbar_wait(&sm.full[s], (k / kFwdStages) & 1, kSuspendNs);
     const Buffer& B = sm.buf[s];
     if (B.stop) break;
     if (!warp_done) {
@@ -478,7 +482,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
   const int wmax = __reduce_max_sync(0xffffffffu, last);
 
   if (warp == kConsumers) {  // ---------------- producer: batches from the back ----------------
-    run_producer<false, 1>(sm, ids, splats + (int64_t)view * n, rg.x, nb,
+    run_producer<false, 1, kStages>(sm, ids, splats + (int64_t)view * n, rg.x, nb,
                         [nb, L](int k, int& rel, int& cnt) {
                           rel = (nb - 1 - k) * kBatch;
                           cnt = min(L - rel, kBatch);

@@ -2,8 +2,9 @@
 // order C7 = ascending (depth key, index) within each (view, tile)).
 //
 // B200 design (no host synchronisation, graph-capturable):
-//   1. k_compact        visible (view, Gaussian) pairs -> (depth key, slot) + 16-B record; builds the
-//                       4 depth-digit histograms on the fly; decoupled look-back scan.
+//   1. k_count_visible + k_scan_tile_counts + k_compact: visible (view, Gaussian) pairs -> (depth
+//                       key, slot) + 16-B record at offsets from a reduce-then-scan of per-tile
+//                       counts; builds the 4 depth-digit histograms on the fly.
 //   2. 4 x k_radix_pass  stable LSD radix sort of the 32-bit depth keys (8-bit digits, onesweep-style:
 //                       warp match-based ranking, per-digit decoupled look-back, smem-staged coalesced
 //                       scatter).  Ties keep (view, index) order because the input is in that order.
@@ -37,22 +38,79 @@ constexpr uint32_t kRadValMask = (1u << 30) - 1;
 // ------------------------------------------------------------------------------------------------
 // 1. compaction of visible pairs + depth-digit histograms
 // ------------------------------------------------------------------------------------------------
+// Visible items per compaction tile (tiles_touched > 0), then one exclusive scan of the tile counts:
+// k_compact then knows its output offset at once (a decoupled look-back here walks back over most of
+// the first wave's tiles, whose aggregates appear together but whose prefixes resolve one by one).
+__global__ void __launch_bounds__(kScanThreads) k_count_visible(const int32_t* __restrict__ tiles_touched,
+                                                                int64_t total, uint64_t* __restrict__ tile_count) {
+  __shared__ uint32_t s_w[kScanThreads / 32];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t base = (int64_t)blockIdx.x * kScanTile;
+  uint32_t c = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    const int64_t idx = base + (int64_t)j * kScanThreads + tid;
+    c += (idx < total && __ldg(tiles_touched + idx) > 0) ? 1u : 0u;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) s_w[warp] = c;
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t t = 0;
+#pragma unroll
+    for (int w = 0; w < kScanThreads / 32; ++w) t += s_w[w];
+    tile_count[blockIdx.x] = t;
+  }
+}
+
+// In-place exclusive scan of the tile counts (one block of 1024 threads, contiguous chunks).
+__global__ void __launch_bounds__(1024) k_scan_tile_counts(uint64_t* __restrict__ v, int m, int64_t* total_out) {
+  __shared__ uint64_t s_w[32];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int per = (m + 1023) / 1024;
+  const int a = min(m, tid * per), b = min(m, a + per);
+  uint64_t sum = 0;
+  for (int i = a; i < b; ++i) sum += v[i];
+  uint64_t inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) s_w[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const uint64_t x = s_w[lane];
+    uint64_t y = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t t = __shfl_up_sync(0xffffffffu, y, o);
+      if (lane >= o) y += t;
+    }
+    s_w[lane] = y - x;
+    if (lane == 31) *total_out = (int64_t)y;
+  }
+  __syncthreads();
+  uint64_t run = s_w[warp] + inc - sum;
+  for (int i = a; i < b; ++i) {
+    const uint64_t c = v[i];
+    v[i] = run;
+    run += c;
+  }
+}
+
 __global__ void __launch_bounds__(kScanThreads) k_compact(const uint32_t* __restrict__ depth_key,
                                                           const uint2* __restrict__ tile_rect,
                                                           const int32_t* __restrict__ tiles_touched, int64_t n,
                                                           int64_t total, uint32_t* __restrict__ keys_out,
                                                           uint32_t* __restrict__ vals_out, uint4* __restrict__ recs,
-                                                          uint64_t* status, int* tile_counter, uint32_t* hist4,
-                                                          int64_t* n_visible) {
-  __shared__ int s_tile;
+                                                          const uint64_t* __restrict__ tile_offset, uint32_t* hist4) {
   __shared__ uint32_t s_cnt[kScanItems][kScanThreads / 32];
   __shared__ uint32_t s_hist[4][256];
-  __shared__ uint64_t s_excl;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) s_tile = atomicAdd(tile_counter, 1);
   for (int k = tid; k < 4 * 256; k += kScanThreads) (&s_hist[0][0])[k] = 0;
-  __syncthreads();
-  const int tile = s_tile;
+  const int tile = blockIdx.x;
   const int64_t base = (int64_t)tile * kScanTile;
   bool flag[kScanItems];
   uint32_t pos_in_warp[kScanItems];
@@ -65,9 +123,7 @@ __global__ void __launch_bounds__(kScanThreads) k_compact(const uint32_t* __rest
     if (lane == 0) s_cnt[j][warp] = __popc(b);
   }
   __syncthreads();
-  // exclusive scan of the 64 warp counts in (j, warp) order by warp 0; the aggregate is published
-  // before the visible items' records are gathered, so the look-back overlaps those loads
-  __shared__ uint32_t s_agg;
+  // exclusive scan of the 64 warp counts in (j, warp) order by warp 0
   if (warp == 0) {
     const int nw = kScanThreads / 32;
     uint32_t a = s_cnt[(2 * lane) / nw][(2 * lane) % nw], b = s_cnt[(2 * lane + 1) / nw][(2 * lane + 1) % nw];
@@ -80,8 +136,6 @@ __global__ void __launch_bounds__(kScanThreads) k_compact(const uint32_t* __rest
     const uint32_t ex = inc - sum;
     s_cnt[(2 * lane) / nw][(2 * lane) % nw] = ex;
     s_cnt[(2 * lane + 1) / nw][(2 * lane + 1) % nw] = ex + a;
-    const uint32_t agg = __shfl_sync(0xffffffffu, inc, 31);
-    if (lane == 0) { publish_aggregate(status, tile, agg); s_agg = agg; }
   }
   uint32_t key[kScanItems];
   uint2 rect[kScanItems];
@@ -91,16 +145,8 @@ __global__ void __launch_bounds__(kScanThreads) k_compact(const uint32_t* __rest
     const int64_t idx = base + (int64_t)j * kScanThreads + tid;
     if (flag[j]) { key[j] = depth_key[idx]; rect[j] = tile_rect[idx]; tt[j] = tiles_touched[idx]; }
   }
-  if (warp == 0) {
-    const uint32_t agg = __shfl_sync(0xffffffffu, s_agg, 0);
-    const uint64_t excl = lookback_published(status, tile, agg);
-    if (lane == 0) {
-      s_excl = excl;
-      if ((base + kScanTile >= total)) *n_visible = (int64_t)(excl + agg);  // last tile
-    }
-  }
   __syncthreads();
-  const uint64_t bex = s_excl;
+  const uint64_t bex = tile_offset[tile];
 #pragma unroll
   for (int j = 0; j < kScanItems; ++j) {
     if (!flag[j]) continue;
@@ -470,9 +516,15 @@ cudaError_t launch_bin_sort(const uint32_t* depth_key, const uint32_t* tile_rect
   out->V = V;
   if (L.items == 0) return cudaSuccess;
 
+  k_count_visible<<<L.compact_tiles, kScanThreads, 0, st>>>(tiles_touched, L.items, st_compact);
+  note_launch();
+  if ((e = check_launch("k_count_visible")) != cudaSuccess) return e;
+  k_scan_tile_counts<<<1, 1024, 0, st>>>(st_compact, L.compact_tiles, n_visible);
+  note_launch();
+  if ((e = check_launch("k_scan_tile_counts")) != cudaSuccess) return e;
   k_compact<<<L.compact_tiles, kScanThreads, 0, st>>>(depth_key, reinterpret_cast<const uint2*>(tile_rect),
                                                       tiles_touched, n, L.items, keysA, valsA, recs, st_compact,
-                                                      counters + 0, hist, n_visible);
+                                                      hist);
   note_launch();
   if ((e = check_launch("k_compact")) != cudaSuccess) return e;
   // depth sort: A -> B -> A -> B -> A

@@ -40,7 +40,7 @@ __device__ __forceinline__ double drcp(double x) {
 // (NEXT f3): colour = max(0, sum_k Y_k(dir) f_k + 1/2), DC f_0 = planes 11-13, the rest from
 // sh_rest (plane 3 (k - 1) + ch), dir = (p - o)/|p - o| with o = -R^T t (pinhole) or R^T e_z (affine).
 template <int kSH>
-__global__ void __launch_bounds__(256) k_project(const float* __restrict__ params, int64_t ld, int64_t n,
+__global__ void __launch_bounds__(256, kSH < 0 ? 4 : 1) k_project(const float* __restrict__ params, int64_t ld, int64_t n,
                                                  const float* __restrict__ sh_rest, int64_t ld_sh,
                                                  const CamPack cams, int V, const RasterK rk,
                                                  steepgs_splat* __restrict__ splats,

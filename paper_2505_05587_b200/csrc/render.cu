@@ -46,7 +46,7 @@ constexpr int kThreadsFwd = 32 * (kConsumers + kFwdProducers);
 constexpr int kBatch = 128;                         // splats per staged batch
 constexpr int kStages = 3;                          // ring depth (backward: bounded by shared memory)
 constexpr int kFwdStages = 4;                       // forward ring depth (slack for unequal consumer warps)
-constexpr uint32_t kSuspendNs = 1000000;            // mbarrier try_wait suspend-time hint
+constexpr uint32_t kSuspendNs = 4096;               // longest mbarrier back-off (ns)
 
 struct Buffer {
   float4 geo[kBatch];            // (mu_x - ox, mu_y - oy, Qxx', 2 Qxy')   Q' = Q log2(e)/2
@@ -77,18 +77,25 @@ __device__ __forceinline__ void mbar_init(unsigned long long* b, uint32_t count)
 __device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
 }
-// Wait for the phase with the given parity to complete.  try_wait with a suspend-time hint parks
-// the warp in hardware until the phase completes (or the hint elapses, then it retries): a waiting
-// warp issues no polling instructions and resumes as soon as the barrier flips.
-__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity, uint32_t suspend_ns) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1, %2;\n\t"
-      "@!p bra WAIT_%=;\n}"
-      :
-      : "r"(saddr(b)), "r"(parity), "r"(suspend_ns)
-      : "memory");
+// Wait for the phase with the given parity to complete: try_wait (which may park the warp for a
+// hardware-chosen time), then exponential back-off with __nanosleep up to max_ns, so a warp that
+// runs far ahead of its block (or a producer ahead of the slowest consumer) polls rarely.
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity, uint32_t max_ns) {
+  const uint32_t a = saddr(b);
+  uint32_t ns = 64;
+  while (true) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (ok) break;
+    __nanosleep(ns);
+    ns = min(2 * ns, max_ns);
+  }
 }
 
 __device__ __forceinline__ float ex2_approx(float x) {

@@ -328,19 +328,23 @@ __global__ void __launch_bounds__(kThreadsFwd, 4) k_render_fwd(const steepgs_spl
       const int base1 = B.base + 1;
       if (kCount && !done) neval += nl;
       // Two entries per iteration: both pair tests ahead of the serial compositing (as in the bwd).
+      // Branch-free (predicated) so the four calls need no divergence bookkeeping; the values are
+      // those of the plain C8 loop.
       auto blend = [&](float e, int j) {
-        if (done || e < lmin) return;                     // sigma < alpha_min: C8 skip
+        const bool live = !done && e >= lmin;             // sigma < alpha_min: C8 skip
         const float alpha = fminf(amax, ex2_approx(e));
         const float Tn = __fmul_rn(T, __fsub_rn(1.0f, alpha));
-        if (Tn < tmin) { done = true; return; }           // C8 termination
+        const bool term = live && Tn < tmin;              // C8 termination
+        const bool comp = live && !term;
+        done = done || term;
         const float4 c = B.col[j];
         const float aT = __fmul_rn(alpha, T);
-        C0 = __fmaf_rn(aT, c.x, C0);
-        C1 = __fmaf_rn(aT, c.y, C1);
-        C2 = __fmaf_rn(aT, c.z, C2);
-        T = Tn;
-        last = base1 + j;
-        if (kCount) ++ncomp;
+        C0 = comp ? __fmaf_rn(aT, c.x, C0) : C0;
+        C1 = comp ? __fmaf_rn(aT, c.y, C1) : C1;
+        C2 = comp ? __fmaf_rn(aT, c.z, C2) : C2;
+        T = comp ? Tn : T;
+        last = comp ? base1 + j : last;
+        if (kCount) ncomp += comp ? 1 : 0;
       };
       int t = 0;
       for (; t + 3 < nl; t += 4) {

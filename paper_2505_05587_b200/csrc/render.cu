@@ -593,20 +593,21 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
       // ---- phase 1: pixel-parallel recursion over entries t_hi-1 .. t_lo ----
       // Four entries per iteration: the pair tests are evaluated before the (serial) recursion, so
       // their shared-memory loads and arithmetic overlap.
+      // Branch-free (predicated): a lane that does not composite the entry takes alpha = 0, which
+      // leaves B unchanged exactly, and keeps its T; the hit lanes' values are those of the plain
+      // C10 recursion.
       auto recurse = [&](bool hit, float ee, int j, int e) {
-        if (hit) {
-          const float sigma = ex2_approx(ee);
-          const float alpha = fminf(amax, sigma);
-          const float4 c = B.col[j];
-          const float om = 1.0f - alpha;
-          T = T * rcp_approx(om);                           // T_i (before this splat)
-          const float d0 = c.x - B0, d1 = c.y - B1, d2 = c.z - B2;   // colour minus the colour behind
-          const float gsum = fmaf(dl2, d2, fmaf(dl1, d1, dl0 * d0));
-          B0 = fmaf(alpha, d0, B0);                         // B <- alpha c + (1 - alpha) B
-          B1 = fmaf(alpha, d1, B1);
-          B2 = fmaf(alpha, d2, B2);
-          swat[e][lane] = make_float2(T * gsum * sigma, alpha * T);  // dL/dalpha * sigma (Z3), alpha T
-        }
+        const float sigma = ex2_approx(ee);
+        const float alpha = hit ? fminf(amax, sigma) : 0.0f;
+        const float4 c = B.col[j];
+        const float om = 1.0f - alpha;
+        T = hit ? T * rcp_approx(om) : T;                  // T_i (before this splat)
+        const float d0 = c.x - B0, d1 = c.y - B1, d2 = c.z - B2;   // colour minus the colour behind
+        const float gsum = fmaf(dl2, d2, fmaf(dl1, d1, dl0 * d0));
+        B0 = fmaf(alpha, d0, B0);                           // B <- alpha c + (1 - alpha) B
+        B1 = fmaf(alpha, d1, B1);
+        B2 = fmaf(alpha, d2, B2);
+        if (hit) swat[e][lane] = make_float2(T * gsum * sigma, alpha * T);  // dL/dalpha * sigma (Z3), alpha T
         const uint32_t bal = __ballot_sync(0xffffffffu, hit);
         if (lane == 0) scm[e] = bal;
       };

@@ -217,12 +217,12 @@ __device__ __forceinline__ void run_producer(SmemT<kS>& sm, const uint32_t* __re
         const float inv2a = __fdividef(0.5f, qa), slope = -qb * inv2a;   // approximate: covered by the padding
         uint32_t m = 0u;
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          if (!(gy - c.y <= 4.0f * t + 3.5f && gy + c.y >= 4.0f * t + 0.5f)) continue;
+        for (int t = 0; t < 4; ++t) {   // branch-free: the four strips' tests are predicated
+          const bool inb = gy - c.y <= 4.0f * t + 3.5f && gy + c.y >= 4.0f * t + 0.5f;
           const float dy0 = 4.0f * t + 0.5f - gy, dy1 = dy0 + 3.0f;
           const float dym = fminf(fmaxf(0.0f, dy0), dy1);
           const float D = 4.0f * qa * tq - delta * dym * dym;
-          if (D < 0.0f) continue;
+          const bool ok = inb && D >= 0.0f;
           float sq;
           asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(D));          // inf stays inf (smooth mode)
           const float hw = sq * inv2a * 1.0001f + 0.01f;
@@ -231,7 +231,7 @@ __device__ __forceinline__ void run_producer(SmemT<kS>& sm, const uint32_t* __re
           uint32_t xs = 0u;
           if (hi >= 0.5f && lo <= 7.5f) xs |= 1u;
           if (hi >= 8.5f && lo <= 15.5f) xs |= 2u;
-          m |= (xs & xb) << (2 * t);
+          m |= ok ? (xs & xb) << (2 * t) : 0u;
         }
         B.mask[kk] = m;
         inst_mask[first + rel + kk] = (uint8_t)m;   // for the backward's producer

@@ -49,4 +49,4 @@ tot, stt = sum(acc.values()), sum(st.values())
 src = open(srcp).read().split("\n")
 print(f"{len(out)} local / {len(recs)} profiled instructions; {tot:.3g} warp instructions")
 for ln, v in sorted(acc.items(), key=lambda x: -x[1] - 1e3 * st[x[0]])[:top]:
-    print(f"{ln}: {100 * v / tot:5.1f}% instr {100 * st[ln] / stt:5.1f}% stall  {src[ln - 1].strip()[:90] if ln else ''}")
+    print(f"{ln}: {100 * v / tot:5.1f}% instr {100 * st[ln] / stt:5.1f}% stall  {src[ln - 1].strip()[:90] if ln and ln <= len(src) else ''}")

@@ -201,7 +201,10 @@ steepgs_status steepgs_l1_ssim_grad(const float* image, const float* target, int
  * view_grad_stats [2][ldg] fp32 or NULL (NEXT f4, the ADC statistic of P:L154): plane 0 gets the sum
  * over this call's views v with tiles_touched[v][i] > 0 of ||dL/dPi(p_i)||_2 (pixel units), plane 1
  * the number of such views; written (accumulate = 0) or added (1, 2) like the S planes.
- * tiles_touched ([V][n], from steepgs_project) is read only then. */
+ * tiles_touched ([V][n], from steepgs_project) is read only then.
+ * Precondition: splats, b, cams and rp are those of the steepgs_render_fwd call that produced
+ * final_T and n_contrib (the replay also reads b->tile_last and b->inst_mask, which that forward
+ * wrote); otherwise the result is unspecified. */
 steepgs_status steepgs_render_bwd_split(const float* params, int64_t ld, int64_t n,
                                         const steepgs_splat* splats, const steepgs_binning* b,
                                         const steepgs_camera* cams, int32_t V,

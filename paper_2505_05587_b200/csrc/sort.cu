@@ -408,14 +408,33 @@ __global__ void __launch_bounds__(kScanThreads) k_duplicate(const uint32_t* __re
 // ------------------------------------------------------------------------------------------------
 // 5. tile ranges
 // ------------------------------------------------------------------------------------------------
+// Four consecutive keys per thread (one 16-B load; the neighbours across the group boundary come
+// from the adjacent lanes or one extra load).
 __global__ void k_ranges(const uint32_t* __restrict__ keys, const int64_t* n_inst, int64_t max_instances,
                          uint2* __restrict__ ranges) {
   int64_t I = *n_inst;
   if (I > max_instances) I = max_instances;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < I; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t k = keys[i];
-    if (i == 0 || keys[i - 1] != k) ranges[k].x = (uint32_t)i;
-    if (i == I - 1 || keys[i + 1] != k) ranges[k].y = (uint32_t)(i + 1);
+  const int64_t groups = (I + 3) / 4;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i0 = 4 * g;
+    uint32_t k[6];   // keys i0 - 1 .. i0 + 4
+    if (i0 + 4 <= I) {
+      const uint4 q = *reinterpret_cast<const uint4*>(keys + i0);   // keys buffer is 256-B aligned
+      k[1] = q.x; k[2] = q.y; k[3] = q.z; k[4] = q.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) k[1 + j] = i0 + j < I ? keys[i0 + j] : 0u;
+    }
+    k[0] = i0 > 0 ? __ldg(keys + i0 - 1) : ~0u;
+    k[5] = i0 + 4 < I ? __ldg(keys + i0 + 4) : ~0u;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t i = i0 + j;
+      if (i >= I) break;
+      const uint32_t kk = k[1 + j];
+      if (i == 0 || k[j] != kk) ranges[kk].x = (uint32_t)i;
+      if (i == I - 1 || k[2 + j] != kk) ranges[kk].y = (uint32_t)(i + 1);
+    }
   }
 }
 
@@ -559,7 +578,7 @@ cudaError_t launch_bin_sort(const uint32_t* depth_key, const uint32_t* tile_rect
     t = tvi; tvi = tvo; tvo = t;
   }
   out->ids = tvi;
-  int64_t rb = (max_instances + 255) / 256;
+  int64_t rb = (max_instances + 1023) / 1024;
   if (rb > 148 * 8) rb = 148 * 8;  // grid-stride: the true I is only known on the device
   k_ranges<<<(unsigned)(rb > 0 ? rb : 1), 256, 0, st>>>(tki, n_inst, max_instances, ranges);
   note_launch();

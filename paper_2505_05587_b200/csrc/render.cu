@@ -6,16 +6,19 @@
 //   * warps 0..7 (consumers) own one pixel per thread; warp w covers the 8x4 sub-block
 //     x in 8 (w & 1) .. +7, y in 4 (w >> 1) .. +3;
 //   * producer warps (2 in the forward, 1 in the backward) stage the tile's depth-ordered splats
-//     into a ring of kStages shared-memory buffers of kBatch splats: the 64-B records are copied
-//     with cp.async (ids prefetched a batch ahead), made tile-relative, and given the 8-bit mask of
-//     sub-blocks their alpha support {m <= tau} reaches (box test refined by an exact per-strip
-//     ellipse test); each consumer compacts a staged batch to its own sub-block's splats with 4
-//     ballots.
+//     into a ring of shared-memory buffers (4 in the forward, 3 in the backward) of kBatch splats:
+//     the 64-B records are copied with cp.async (ids prefetched two batches ahead), made
+//     tile-relative, and given the 8-bit mask of sub-blocks their alpha support {m <= tau} reaches
+//     (box test refined by an exact per-strip ellipse test).  The forward stores each instance's
+//     mask (binning.inst_mask); the backward's producer reads it back instead of recomputing it and
+//     copies only the 48 record bytes it needs.  Each consumer compacts a staged batch to its own
+//     sub-block's splats with 4 ballots.
 // Full/empty mbarriers per buffer replace block-wide barriers, so consumer warps with short lists
-// run ahead by up to kStages batches instead of waiting for the slowest warp, and a consumer
-// iterates only over the splats that can touch its 32 pixels.  Consumers take four list entries
-// per iteration: the four pair tests are independent and are issued before the serial
-// compositing / recursion.
+// run ahead by up to a ring's depth of batches instead of waiting for the slowest warp (waits:
+// try_wait + exponential __nanosleep back-off), and a consumer iterates only over the splats that
+// can touch its 32 pixels.  Consumers take four list entries per iteration: the four pair tests are
+// independent and are issued before the serial compositing / recursion, which is branch-free
+// (predicated) so the four steps need no divergence bookkeeping.
 //
 // Per-pair arithmetic: the mean is made tile-relative in fp64 before rounding (offsets
 // d = x - Pi(p) carry ~1e-7 px error); the conic arrives pre-scaled by log2(e)/2 (a1) so that
@@ -28,11 +31,12 @@
 // tile's longest prefix is stored by the forward), T_i recovered as T_{i+1} / (1 - alpha_i)
 // (approximate reciprocal; relative error ~1 ulp per step), dL/dalpha_i = T_i sum_ch dL/dC_ch
 // (c_ch - B_ch) with B the normalised colour behind (C10), w = dL/dsigma * sigma.  Two phases per
-// chunk of 16 list entries: the pixel-parallel recursion leaves (w, alpha T) in shared memory, then
-// the two lanes of each entry sum its 9 moments (w, w d, w d d^T, alpha T dL/dC) over the
-// contributing pixels and add them with vector REDs into moments[view][gid][12].  The splitting
-// matrix needs no per-pair work of its own: S_view = P^T (Q M Q - m0 Q) P is formed per Gaussian from
-// these moments (gauss_bwd.cu).
+// chunk of 16 list entries (a chunk continues across batch boundaries): the pixel-parallel
+// recursion leaves (w, alpha T) in shared memory, then the two lanes of each entry sum its raw
+// moments over the contributing pixels in the warp's sub-block frame, recentre them on the splat
+// mean and add the 9 moments (w, w d, w d d^T, alpha T dL/dC) with vector REDs into
+// moments[view][gid][12].  The splitting matrix needs no per-pair work of its own:
+// S_view = P^T (Q M Q - m0 Q) P is formed per Gaussian from these moments (gauss_bwd.cu).
 #include "common.cuh"
 
 namespace sgs {

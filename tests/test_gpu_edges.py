@@ -116,6 +116,13 @@ def test_argument_validation():
     assert e.value.status == 2
     with pytest.raises(_lib.SteepGSError):
         Rasterizer(64, 65, 64, 64)                                           # > 64 views
+    # a binning without the forward -> backward per-instance masks is rejected before any launch
+    rz.bin_sort()
+    b = _lib.Binning.from_buffer_copy(rz.binning)
+    b.inst_mask = None
+    with pytest.raises(_lib.SteepGSError) as e:
+        _lib.render_fwd(rz.splats, 64, b, rz.cams_arr, 1, rz.rp, rz.image, rz.final_T, rz.n_contrib)
+    assert e.value.status == 1
 
 
 def test_instance_overflow_auto_grow():

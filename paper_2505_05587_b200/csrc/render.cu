@@ -6,7 +6,7 @@
 //   * warps 0..7 (consumers) own one pixel per thread; warp w covers the 8x4 sub-block
 //     x in 8 (w & 1) .. +7, y in 4 (w >> 1) .. +3;
 //   * producer warps (2 in the forward, 1 in the backward) stage the tile's depth-ordered splats
-//     into a ring of shared-memory buffers (4 in the forward, 3 in the backward) of kBatch splats:
+//     into a ring of shared-memory buffers (5 in the forward, 3 in the backward) of kBatch splats:
 //     the 64-B records are copied with cp.async (ids prefetched two batches ahead), made
 //     tile-relative, and given the 8-bit mask of sub-blocks their alpha support {m <= tau} reaches
 //     (box test refined by an exact per-strip ellipse test).  The forward stores each instance's
@@ -49,7 +49,7 @@ constexpr int kFwdProducers = 2;                    // the forward's consumers a
 constexpr int kThreadsFwd = 32 * (kConsumers + kFwdProducers);
 constexpr int kBatch = 128;                         // splats per staged batch
 constexpr int kStages = 3;                          // ring depth (backward: bounded by shared memory)
-constexpr int kFwdStages = 4;                       // forward ring depth (slack for unequal consumer warps)
+constexpr int kFwdStages = 5;                       // forward ring depth (slack for unequal consumer warps)
 constexpr uint32_t kSuspendNs = 4096;               // longest mbarrier back-off (ns)
 
 struct Buffer {
@@ -287,7 +287,8 @@ __global__ void __launch_bounds__(kThreadsFwd, 4) k_render_fwd(const steepgs_spl
                                                          uint8_t* __restrict__ inst_mask,
                                                          unsigned long long* __restrict__ pair_counts,
                                                          const L1Fused l1) {
-  __shared__ SmemFwd sm;
+  extern __shared__ __align__(16) unsigned char fsmem[];
+  SmemFwd& sm = *reinterpret_cast<SmemFwd*>(fsmem);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int tile = blockIdx.x, view = blockIdx.y;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
@@ -687,12 +688,20 @@ cudaError_t launch_render_fwd(const steepgs_splat* splats, int64_t n, const stee
     const cudaError_t e = cudaMemsetAsync(l1.loss, 0, sizeof(float) * (size_t)b.V, st);
     if (e != cudaSuccess) return e;
   }
+  static bool attr_set = false;   // per process; the attribute is a property of the functions
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_render_fwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SmemFwd));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_render_fwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SmemFwd));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
   if (pair_counts)
-    k_render_fwd<true><<<grid, kThreadsFwd, 0, st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
+    k_render_fwd<true><<<grid, kThreadsFwd, sizeof(SmemFwd), st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
                                                   b.tiles_x, tpv, rk, image, final_T, n_contrib, b.tile_last, b.inst_mask,
                                                   reinterpret_cast<unsigned long long*>(pair_counts), l1);
   else
-    k_render_fwd<false><<<grid, kThreadsFwd, 0, st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
+    k_render_fwd<false><<<grid, kThreadsFwd, sizeof(SmemFwd), st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
                                                    b.tiles_x, tpv, rk, image, final_T, n_contrib, b.tile_last, b.inst_mask, nullptr,
                                                    l1);
   note_launch();

@@ -37,6 +37,8 @@
 // mean and add the 9 moments (w, w d, w d d^T, alpha T dL/dC) with vector REDs into
 // moments[view][gid][12].  The splitting matrix needs no per-pair work of its own:
 // S_view = P^T (Q M Q - m0 Q) P is formed per Gaussian from these moments (gauss_bwd.cu).
+#include <atomic>
+
 #include "common.cuh"
 
 namespace sgs {
@@ -679,6 +681,20 @@ __global__ void k_l1_grad(const float* __restrict__ image, const float* __restri
 
 }  // namespace
 
+// Opt a kernel into more than 48 KB of dynamic shared memory on the current device (the attribute is
+// per device); `done` records the devices already set (bit per device id < 64).  With mark = false
+// the bit is left for a following call on another function of the same group.
+static cudaError_t allow_dynamic_smem(std::atomic<uint64_t>& done, const void* fn, size_t bytes, bool mark = false) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = dev < 64 ? (1ull << dev) : 0ull;
+  if (bit && (done.load(std::memory_order_acquire) & bit)) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess && mark && bit) done.fetch_or(bit, std::memory_order_release);
+  return e;
+}
+
 cudaError_t launch_render_fwd(const steepgs_splat* splats, int64_t n, const steepgs_binning& b, int W, int H,
                               const RasterK& rk, float* image, float* final_T, int32_t* n_contrib,
                               int64_t* pair_counts, cudaStream_t st, const L1Fused& l1) {
@@ -688,13 +704,11 @@ cudaError_t launch_render_fwd(const steepgs_splat* splats, int64_t n, const stee
     const cudaError_t e = cudaMemsetAsync(l1.loss, 0, sizeof(float) * (size_t)b.V, st);
     if (e != cudaSuccess) return e;
   }
-  static bool attr_set = false;   // per process; the attribute is a property of the functions
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_render_fwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SmemFwd));
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_render_fwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SmemFwd));
+  {
+    static std::atomic<uint64_t> done{0};   // devices whose function attribute is set
+    cudaError_t e = allow_dynamic_smem(done, (const void*)k_render_fwd<true>, sizeof(SmemFwd));
+    if (e == cudaSuccess) e = allow_dynamic_smem(done, (const void*)k_render_fwd<false>, sizeof(SmemFwd), true);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   if (pair_counts)
     k_render_fwd<true><<<grid, kThreadsFwd, sizeof(SmemFwd), st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
@@ -729,11 +743,10 @@ cudaError_t launch_render_bwd(const steepgs_splat* splats, const steepgs_binning
   const int tpv = b.tiles_x * b.tiles_y;
   dim3 grid(tpv, b.V);
   const size_t smem = ((sizeof(Smem) + 15) & ~size_t(15)) + sizeof(BwdScratch);
-  static bool attr_set = false;  // per process; the attribute is a property of the function
-  if (!attr_set) {
-    const cudaError_t e = cudaFuncSetAttribute(k_render_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    static std::atomic<uint64_t> done{0};   // devices whose function attribute is set
+    const cudaError_t e = allow_dynamic_smem(done, (const void*)k_render_bwd, smem, true);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   k_render_bwd<<<grid, kThreads, smem, st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
                                           b.tiles_x, tpv, rk, final_T, n_contrib, dL_dimage, b.tile_last, b.inst_mask, moments);

@@ -59,6 +59,15 @@ def test_host_only_entry_points(libsteepgs):
         sizes = [int(x) for x in subprocess.check_output([os.path.join(d, "s")]).split()]
     assert sizes == [ctypes.sizeof(_lib.Camera), ctypes.sizeof(_lib.RasterParams), ctypes.sizeof(_lib.DensifyParams),
                      ctypes.sizeof(_lib.Binning), _lib.SPLAT_BYTES, ctypes.sizeof(_lib.AdamParams)]
+    # field offsets of the binning struct too (the render calls read fields the forward / backward share)
+    fields = [f for f, _ in _lib.Binning._fields_]
+    src2 = ('#include <stdio.h>\n#include <stddef.h>\n#include "steepgs.h"\nint main(void){'
+            + "".join(f'printf("%zu ", offsetof(steepgs_binning, {f}));' for f in fields) + "return 0;}")
+    with tempfile.TemporaryDirectory() as d:
+        open(os.path.join(d, "o.c"), "w").write(src2)
+        subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", os.path.join(d, "o"), os.path.join(d, "o.c")])
+        offs = [int(x) for x in subprocess.check_output([os.path.join(d, "o")]).split()]
+    assert offs == [getattr(_lib.Binning, f).offset for f in fields]
     assert _lib.version().startswith("steepgs-b200")
     assert _lib.bin_sort_workspace_size(1000, 2, 64, 48, 10000) > 0
     assert _lib.densify_workspace_size(5000) >= 8

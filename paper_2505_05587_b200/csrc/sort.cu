@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(kRadixThreads, 3) k_radix_pass(const uint32_t*
 // ------------------------------------------------------------------------------------------------
 // 3. duplication: scan of tiles_touched in depth order, one instance per touched tile
 // ------------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(kScanThreads) k_duplicate(const uint32_t* __restrict__ sorted_slots,
+__global__ void __launch_bounds__(kScanThreads, 4) k_duplicate(const uint32_t* __restrict__ sorted_slots,
                                                             const uint4* __restrict__ recs, const int64_t* n_vis_dev,
                                                             int tiles_x, int tiles_per_view, int64_t max_instances,
                                                             uint32_t* __restrict__ inst_keys,

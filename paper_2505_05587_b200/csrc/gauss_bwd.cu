@@ -19,7 +19,7 @@ namespace sgs {
 
 namespace {
 
-__global__ void __launch_bounds__(128) k_gauss_bwd(const float* __restrict__ params, int64_t ld, int64_t n,
+__global__ void __launch_bounds__(128, 5) k_gauss_bwd(const float* __restrict__ params, int64_t ld, int64_t n,
                                                    const CamPack cams, int V, const RasterK rk,
                                                    float* __restrict__ moments, float* __restrict__ grad_S,
                                                    int64_t ldg, int accumulate,

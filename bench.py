@@ -174,6 +174,7 @@ def main():
     ap.add_argument("--budget-frac", type=float, default=None,
                     help="densify with the increment budget K = frac * n (App. A.2; SURVEY C4's ~10% split)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch every kernel eagerly (no per-stage CUDA graphs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -222,41 +223,68 @@ def main():
     stage_names = ["restore", "project", "bin_sort", "render_fwd", "l1_grad", "render_bwd", "gauss_bwd_S",
                    "allreduce", "densify"]
 
+    def stage_fns(tgt):
+        """The step as (stage, callable or None) in stage_names order; None = nothing in this stage."""
+        def restore():
+            _lib.copy_planes(params, pristine, n, 0, 3)      # undo last step's densify (positions,
+            _lib.copy_planes(params, pristine, n, 10, 1)     # opacity) -- checkpoint restore, no kernel
+
+        def bwd():
+            if shd is not None:
+                rz.sh_bwd(params, grad_S, sh_rest, shd, grad_sh, 0)
+            rz.gauss_bwd(params, grad_S, accumulate=0 | (4 if shd is not None else 0))
+        fused = args.ssim is None
+        return [
+            ("restore", restore),
+            ("project", lambda: rz.project(params, n, cams, sh_rest, shd)),
+            ("bin_sort", rz.bin_sort),
+            # a3 + a4 fused (l1 gradient in the forward's epilogue) unless the SSIM term is on
+            ("render_fwd", (lambda: rz.render_fwd_l1(tgt)) if fused else rz.render_fwd),
+            ("l1_grad", None if fused else (lambda: _lib.l1_ssim_grad(rz.image, tgt, args.ssim, 1.0, rz.dL, rz.loss,
+                                                                      loss_ws))),
+            ("render_bwd", rz.render_bwd_moments),
+            ("gauss_bwd_S", bwd),
+            ("allreduce", (lambda: allreduce_accumulators(grad_S, n=n)) if ws > 1 else None),   # NCCL, [k, :n]
+            ("densify", lambda: rz.densify(params, grad_S, n, cap, denom=float(V * ws), want_lambda=False,
+                                           budget=None if args.budget_frac is None else int(args.budget_frac * n))),
+        ]
+
+    # Per-stage CUDA graphs (captured after the warm-up; one set per target buffer): a replay
+    # launches a stage's kernels and memsets back to back with no host launch overhead between them;
+    # the stage boundaries stay eager so the per-stage CUDA events of the timed region bracket them.
+    # The NCCL allreduce stays eager.  Kernels inside a graph are counted when it is captured.
+    graphs = {}
+    graph_launches = [0]
+
+    def capture(tgt):
+        key = tgt.data_ptr()
+        if key in graphs:
+            return
+        gs = {}
+        for nm, fn in stage_fns(tgt):
+            if fn is None or nm == "allreduce":
+                continue
+            g = torch.cuda.CUDAGraph()
+            l0 = _lib.launch_count()
+            with torch.cuda.graph(g):
+                fn()
+            gs[nm] = (g, _lib.launch_count() - l0)
+        graphs[key] = gs
+
     def step(ev=None, tgt=None):
         tgt = targets if tgt is None else tgt
-
-        def mark(k):
+        gs = graphs.get(tgt.data_ptr()) if not args.no_graph else None
+        if ev is not None:
+            ev[0].record(stream)
+        for k, (nm, fn) in enumerate(stage_fns(tgt)):
+            if gs is not None and nm in gs:
+                g, nl = gs[nm]
+                g.replay()
+                graph_launches[0] += nl
+            elif fn is not None:
+                fn()
             if ev is not None:
-                ev[k].record(stream)
-        mark(0)
-        _lib.copy_planes(params, pristine, n, 0, 3)          # undo last step's densify (positions,
-        _lib.copy_planes(params, pristine, n, 10, 1)         # opacity) -- checkpoint restore, no kernel
-        mark(1)
-        rz.project(params, n, cams, sh_rest, shd)
-        mark(2)
-        rz.bin_sort()
-        mark(3)
-        if args.ssim is None:
-            rz.render_fwd_l1(tgt)                            # a3 + a4 fused (l1 gradient in the epilogue)
-            mark(4)
-            mark(5)
-        else:
-            rz.render_fwd()
-            mark(4)
-            _lib.l1_ssim_grad(rz.image, tgt, args.ssim, 1.0, rz.dL, rz.loss, loss_ws)
-            mark(5)
-        rz.render_bwd_moments()
-        mark(6)
-        if shd is not None:
-            rz.sh_bwd(params, grad_S, sh_rest, shd, grad_sh, 0)
-        rz.gauss_bwd(params, grad_S, accumulate=0 | (4 if shd is not None else 0))
-        mark(7)
-        if ws > 1:
-            allreduce_accumulators(grad_S, n=n)          # 20 row slices [k, :n], NCCL
-        mark(8)
-        rz.densify(params, grad_S, n, cap, denom=float(V * ws), want_lambda=False,
-                   budget=None if args.budget_frac is None else int(args.budget_frac * n))
-        mark(9)
+                ev[k + 1].record(stream)
 
     def barrier():
         if ws > 1:
@@ -266,9 +294,15 @@ def main():
     for _ in range(max(args.warmup, 3) if args.warmup >= 3 else args.warmup):
         step()
     barrier()
+    if not args.no_graph:
+        capture(targets)
+        for _ in range(2):
+            step()
+        barrier()
     pair_counts.zero_()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(10)] for _ in range(args.steps)]
     launches0 = _lib.launch_count()
+    graph_launches[0] = 0
     sampler = ClockSampler(local)
     time.sleep(0.3)
     barrier()
@@ -280,7 +314,7 @@ def main():
     t_end.record(stream)
     barrier()
     clocks = sampler.stop()
-    launches = _lib.launch_count() - launches0
+    launches = _lib.launch_count() - launches0 + graph_launches[0]
     elapsed = t_start.elapsed_time(t_end)
     if ws > 1:
         tt = torch.tensor([elapsed], device=dev)
@@ -405,6 +439,8 @@ def main():
 
         for ev in consumed:
             ev.record(stream)
+        if not args.no_graph:
+            capture(tbuf[1])
         run_e2e(2)
         barrier()
         a = torch.cuda.Event(enable_timing=True)
@@ -444,7 +480,8 @@ def main():
                         parallelism=f"view-sharded dp{ws}" + (" + NCCL allreduce(grads+S)" if ws > 1 else ""),
                         l2="no flush: per-step working set (params 56 MB + splats 48 B x V x n + sort/moment "
                            "buffers) exceeds the 126 MB L2",
-                        scene="synthetic surface-like (SURVEY 8(d1)), procedural targets"),
+                        scene="synthetic surface-like (SURVEY 8(d1)), procedural targets",
+                        launch="eager" if args.no_graph else "per-stage CUDA graphs (NCCL allreduce eager)"),
             roofline=roofline,
             path_hbm=dict(alg_bytes_per_step=int(path_bytes), ms=round(path_ms, 4),
                           frac=round(path_bytes / (path_ms * 1e-3) / 1e9 / hbm, 4), peak_gbs=hbm),

@@ -283,7 +283,7 @@ def main():
                 graph_launches[0] += nl
             elif fn is not None:
                 fn()
-            if ev is not None:
+            if ev is not None and fn is not None:   # an empty stage records no event (each costs ~4 us)
                 ev[k + 1].record(stream)
 
     def barrier():
@@ -321,8 +321,15 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         elapsed = float(tt.item())
     ms_step = elapsed / args.steps
-    stage_ms = {nm: float(np.mean([evs[k][i].elapsed_time(evs[k][i + 1]) for k in range(args.steps)]))
-                for i, nm in enumerate(stage_names)}
+    # stage i spans from the last event recorded before it to its own (empty stages: 0)
+    recorded = [0] + [i + 1 for i, (_, fn) in enumerate(stage_fns(targets)) if fn is not None]
+    stage_ms = {}
+    for i, nm in enumerate(stage_names):
+        if i + 1 not in recorded:
+            stage_ms[nm] = 0.0
+            continue
+        prev = max(r for r in recorded if r <= i)
+        stage_ms[nm] = float(np.mean([evs[k][prev].elapsed_time(evs[k][i + 1]) for k in range(args.steps)]))
 
     # ---- counts for the roofline model: one counting forward after the timed region (the timed
     # forward runs the non-counting kernel instance), then device -> host ----

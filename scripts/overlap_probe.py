@@ -90,6 +90,51 @@ def main():
     def graph8():
         g.replay()
 
+    xev = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(10)]
+
+    def serial8_xmarks():
+        xev[0].record()
+        restore()
+        xev[1].record()
+        rz8.project(params, n, cams)
+        xev[2].record()
+        rz8.bin_sort()
+        xev[3].record()
+        rz8.render_fwd_l1(tg)
+        xev[4].record()
+        xev[5].record()
+        rz8.render_bwd_moments()
+        xev[6].record()
+        rz8.gauss_bwd(params, grad_S, accumulate=0)
+        xev[7].record()
+        xev[8].record()
+        rz8.densify(params, grad_S, n, cap, denom=float(V), want_lambda=False)
+        xev[9].record()
+
+    gx = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gx):
+        serial8_xmarks()
+    torch.cuda.synchronize()
+
+    def graph8_xmarks():
+        gx.replay()
+
+    stage_graphs = []
+    for fn in (restore, lambda: rz8.project(params, n, cams), rz8.bin_sort, lambda: rz8.render_fwd_l1(tg),
+               rz8.render_bwd_moments, lambda: rz8.gauss_bwd(params, grad_S, accumulate=0),
+               lambda: rz8.densify(params, grad_S, n, cap, denom=float(V), want_lambda=False)):
+        sg = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(sg):
+            fn()
+        stage_graphs.append(sg)
+    torch.cuda.synchronize()
+
+    def stage_graphs_marks():
+        evs[0].record(main_s)
+        for k, sg in enumerate(stage_graphs):
+            sg.replay()
+            evs[k + 1].record(main_s)
+
     streams = {}
 
     def make_two(prioA, prioB):
@@ -116,7 +161,7 @@ def main():
         streams[(prioA, prioB)] = (sA, sB)
         return two
 
-    scheds = {"serial8": serial8, "serial8_marks": serial8_marks, "graph8": graph8, "serial4+4": serial44, "two_streams": make_two(0, 0),
+    scheds = {"serial8": serial8, "serial8_marks": serial8_marks, "graph8": graph8, "graph8_xmarks": graph8_xmarks, "stage_graphs_marks": stage_graphs_marks, "serial4+4": serial44, "two_streams": make_two(0, 0),
               "two_streams_B_high": make_two(0, -1), "two_streams_A_high": make_two(-1, 0)}
     res = {}
     for rep in range(2):

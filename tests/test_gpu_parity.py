@@ -530,6 +530,50 @@ def test_bench_launch_configuration_c2(orc):
     assert np.abs(np.delete(g, np.flatnonzero(a.sum(0) > 0), axis=1)).max() == 0.0
 
 
+def test_stage_graph_replay_equals_eager():
+    """bench.py's launch mode: one CUDA graph per stage, captured after an eager step and replayed.
+    Binning, image, T, n_contrib and dL/dimage bit-identical to the eager launch; grads + S equal up to
+    the order of the backward's float atomics."""
+    from gpu_run import to_dev
+    from paper_2505_05587_b200.pipeline import Rasterizer
+    cfg = synth.CONFIGS["C2"]
+    n, V = cfg.n, 2
+    p = synth.scene_for(cfg)
+    cams = synth.cameras_for(cfg, views=V)
+    tg = to_dev(synth.targets_for(cfg, views=V))
+    cap = 2 * n
+    P = torch.zeros(14, cap, device="cuda"); P[:, :n] = to_dev(p)
+    G = torch.zeros(20, cap, device="cuda")
+    rz = Rasterizer(cap, V, cfg.width, cfg.height, max_instances=int(3.0 * V * n))
+    stages = [lambda: rz.project(P, n, cams), rz.bin_sort, lambda: rz.render_fwd_l1(tg), rz.render_bwd_moments,
+              lambda: rz.gauss_bwd(P, G, accumulate=0)]
+    for f in stages:
+        f()
+    torch.cuda.synchronize()
+    b = rz.binning_arrays()
+    ref = dict(ids=b["ids"].clone(), ranges=b["ranges"].clone(), image=rz.image.clone(), T=rz.final_T.clone(),
+               nc=rz.n_contrib.clone(), dL=rz.dL.clone(), G=G.clone())
+    graphs = []
+    for f in stages:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            f()
+        graphs.append(g)
+    for t in (rz.image, rz.final_T, rz.dL, G):
+        t.zero_()
+    rz.n_contrib.zero_()
+    for g in graphs:
+        g.replay()
+    torch.cuda.synchronize()
+    b = rz.binning_arrays()
+    assert torch.equal(b["ids"], ref["ids"]) and torch.equal(b["ranges"], ref["ranges"])
+    for k, t in (("image", rz.image), ("T", rz.final_T), ("nc", rz.n_contrib), ("dL", rz.dL)):
+        assert torch.equal(t, ref[k]), k
+    scale = ref["G"][:, :n].abs().amax(dim=1, keepdim=True).clamp_min(1e-30)
+    assert ((G[:, :n] - ref["G"][:, :n]).abs() / scale).max().item() < 1e-4
+    assert ref["G"][14:20, :n].abs().sum().item() > 0
+
+
 def test_render_fwd_l1_fused_equals_separate():
     """a3 + a4 fused (steepgs_render_fwd_l1): image, dL/dimage bit-identical to render_fwd + l1_grad, the
     per-view loss equal up to summation order."""

@@ -15,7 +15,7 @@
 //     sub-block's splats with 4 ballots.
 // Full/empty mbarriers per buffer replace block-wide barriers, so consumer warps with short lists
 // run ahead by up to a ring's depth of batches instead of waiting for the slowest warp (waits:
-// try_wait + exponential __nanosleep back-off), and a consumer iterates only over the splats that
+// try_wait, then parked with a suspend-time hint), and a consumer iterates only over the splats that
 // can touch its 32 pixels.  Consumers take four list entries per iteration: the four pair tests are
 // independent and are issued before the serial compositing / recursion, which is branch-free
 // (predicated) so the four steps need no divergence bookkeeping.
@@ -52,7 +52,7 @@ constexpr int kThreadsFwd = 32 * (kConsumers + kFwdProducers);
 constexpr int kBatch = 128;                         // splats per staged batch
 constexpr int kStages = 3;                          // ring depth (backward: bounded by shared memory)
 constexpr int kFwdStages = 5;                       // forward ring depth (slack for unequal consumer warps)
-constexpr uint32_t kSuspendNs = 4096;               // longest mbarrier back-off (ns)
+constexpr uint32_t kSuspendNs = 1000000;            // mbarrier try_wait suspend-time hint (ns)
 
 struct Buffer {
   float4 geo[kBatch];            // (mu_x - ox, mu_y - oy, Qxx', 2 Qxy')   Q' = Q log2(e)/2
@@ -83,25 +83,31 @@ __device__ __forceinline__ void mbar_init(unsigned long long* b, uint32_t count)
 __device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
 }
-// Wait for the phase with the given parity to complete: try_wait (which may park the warp for a
-// hardware-chosen time), then exponential back-off with __nanosleep up to max_ns, so a warp that
-// runs far ahead of its block (or a producer ahead of the slowest consumer) polls rarely.
-__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity, uint32_t max_ns) {
+// Wait for the phase with the given parity to complete: one try_wait without a hint (the phase is
+// usually complete already), then try_wait with a suspend-time hint, which parks the warp in hardware
+// until the phase completes or the hint elapses.  Measured against polling with an exponential
+// __nanosleep back-off (64 ns .. 4 us): the back-off loop executed ~60 failed polls per consumer wait
+// in the backward (the sleeps return early), ~9% of its issued instructions; parked waits issue none
+// (bwd 1.855 -> 1.844 ms, fwd 0.877 -> 0.874 ms per C2 step).
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity, uint32_t suspend_ns) {
   const uint32_t a = saddr(b);
-  uint32_t ns = 64;
-  while (true) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(a), "r"(parity)
-        : "memory");
-    if (ok) break;
-    __nanosleep(ns);
-    ns = min(2 * ns, max_ns);
-  }
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(a), "r"(parity)
+      : "memory");
+  if (ok) return;
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT_%=;\n}"
+      :
+      : "r"(a), "r"(parity), "r"(suspend_ns)
+      : "memory");
 }
 
 __device__ __forceinline__ float ex2_approx(float x) {

@@ -266,7 +266,7 @@ def main():
                 continue
             g = torch.cuda.CUDAGraph()
             l0 = _lib.launch_count()
-            with torch.cuda.graph(g):
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):   # NCCL watchdog threads may query events
                 fn()
             gs[nm] = (g, _lib.launch_count() - l0)
         graphs[key] = gs

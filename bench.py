@@ -255,6 +255,7 @@ def main():
     # The NCCL allreduce stays eager.  Kernels inside a graph are counted when it is captured.
     graphs = {}
     graph_launches = [0]
+    launch_mode = ["eager" if args.no_graph else "per-stage CUDA graphs (NCCL allreduce eager)"]
 
     def capture(tgt):
         key = tgt.data_ptr()
@@ -266,8 +267,14 @@ def main():
                 continue
             g = torch.cuda.CUDAGraph()
             l0 = _lib.launch_count()
-            with torch.cuda.graph(g, capture_error_mode="thread_local"):   # NCCL watchdog threads may query events
-                fn()
+            try:
+                with torch.cuda.graph(g, capture_error_mode="thread_local"):   # NCCL watchdog threads may query events
+                    fn()
+            except RuntimeError as exc:   # keep the stage eager rather than lose the run
+                torch.cuda.synchronize()
+                launch_mode[0] = f"per-stage CUDA graphs; {nm} eager (capture failed: {str(exc).splitlines()[0][:80]})"
+                print(f"bench: graph capture of {nm} failed, stage runs eagerly: {exc}", file=sys.stderr)
+                continue
             gs[nm] = (g, _lib.launch_count() - l0)
         graphs[key] = gs
 
@@ -488,7 +495,7 @@ def main():
                         l2="no flush: per-step working set (params 56 MB + splats 48 B x V x n + sort/moment "
                            "buffers) exceeds the 126 MB L2",
                         scene="synthetic surface-like (SURVEY 8(d1)), procedural targets",
-                        launch="eager" if args.no_graph else "per-stage CUDA graphs (NCCL allreduce eager)"),
+                        launch=launch_mode[0]),
             roofline=roofline,
             path_hbm=dict(alg_bytes_per_step=int(path_bytes), ms=round(path_ms, 4),
                           frac=round(path_bytes / (path_ms * 1e-3) / 1e9 / hbm, 4), peak_gbs=hbm),

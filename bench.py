@@ -175,6 +175,9 @@ def main():
                     help="densify with the increment budget K = frac * n (App. A.2; SURVEY C4's ~10% split)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch every kernel eagerly (no per-stage CUDA graphs)")
+    ap.add_argument("--h2d-at", default="after_sort", choices=["start", "after_sort"],
+                    help="e2e: start step k+1's target copy with step k, or after step k's bin_sort (the copy's "
+                         "DMA writes then overlap the ALU-bound render kernels, not the L2-resident sort)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -278,7 +281,7 @@ def main():
             gs[nm] = (g, _lib.launch_count() - l0)
         graphs[key] = gs
 
-    def step(ev=None, tgt=None):
+    def step(ev=None, tgt=None, sorted_ev=None):
         tgt = targets if tgt is None else tgt
         gs = graphs.get(tgt.data_ptr()) if not args.no_graph else None
         if ev is not None:
@@ -292,6 +295,8 @@ def main():
                 fn()
             if ev is not None and fn is not None:   # an empty stage records no event (each costs ~4 us)
                 ev[k + 1].record(stream)
+            if sorted_ev is not None and nm == "bin_sort":
+                sorted_ev.record(stream)
 
     def barrier():
         if ws > 1:
@@ -424,9 +429,13 @@ def main():
         copied = [torch.cuda.Event(), torch.cuda.Event()]
         consumed = [torch.cuda.Event(), torch.cuda.Event()]
 
-        def h2d(slot):
+        sorted_evs = [torch.cuda.Event(), torch.cuda.Event()]
+
+        def h2d(slot, after=None):
             with torch.cuda.stream(copy_stream):
                 copy_stream.wait_event(consumed[slot])
+                if after is not None:
+                    copy_stream.wait_event(after)
                 tbuf[slot].copy_(tg_host, non_blocking=True)
                 copied[slot].record(copy_stream)
 
@@ -437,10 +446,12 @@ def main():
             h2d(0)
             for k in range(nsteps):
                 slot = k & 1
-                if k + 1 < nsteps:
+                if k + 1 < nsteps and args.h2d_at == "start":
                     h2d(slot ^ 1)
                 stream.wait_event(copied[slot])
-                step(tgt=tbuf[slot])
+                step(tgt=tbuf[slot], sorted_ev=sorted_evs[slot])
+                if k + 1 < nsteps and args.h2d_at == "after_sort":
+                    h2d(slot ^ 1, after=sorted_evs[slot])
                 consumed[slot].record(stream)
                 loss_host[slot].copy_(rz.loss, non_blocking=True)
                 ns_host[slot].copy_(rz.n_split, non_blocking=True)
@@ -470,8 +481,10 @@ def main():
             et = float(tt.item())
         e2e = dict(value=et / args.steps / (V * ws), unit=UNIT, h2d_bytes_per_step=int(tg_host.numel() * 4),
                    d2h_bytes_per_step=int(loss_host[0].numel() * 4 + 8),
-                   note="H2D of step k+1 overlapped with step k on a copy stream; each step's loss and n_split "
-                        "read back to pinned host memory and consumed by the host one step later")
+                   note="H2D of step k+1 overlapped with step k on a copy stream (issued "
+                        + ("with step k" if args.h2d_at == "start" else "after step k's bin_sort")
+                        + "); each step's loss and n_split read back to pinned host memory and consumed by the "
+                          "host one step later")
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:

@@ -141,6 +141,81 @@ def test_composite_spec_examples(orc):
     assert np.allclose(r["image"][:, 7, 10], 0.75 * np.array(rgb), rtol=1e-15)
 
 
+# ---------------------------------------------------------------------------------------------
+# Depth order.  P:L129 "sorts points according to view-dependent depth" and Eq. eqn:alpha_blend
+# (P:L131-134): C = sum_i c_i alpha_i T_i with T_i = prod_{j<i} (1 - alpha_j), so the Gaussian
+# with T_1 = 1 is the one nearest the camera (smallest camera-space z).  Two Gaussians on one pixel
+# ray, o = 0.5 each, smooth mode (alpha = sigma = 0.5 at the mean): the pixel must be
+# 0.5 c_near + 0.25 c_far whichever index the near one has; a back-to-front reading would give
+# 0.5 c_far + 0.25 c_near.
+# ---------------------------------------------------------------------------------------------
+RED, BLUE = np.array([1.0, 0.0, 0.0]), np.array([0.0, 0.0, 1.0])
+
+
+@pytest.mark.parametrize("near_first", [True, False])
+@pytest.mark.parametrize("z_near,z_far", [(1.0, 2.0), (-0.5, 0.25), (-3.0, -1.0)])
+def test_occlusion_nearer_gaussian_composites_first_affine(orc, near_first, z_near, z_far):
+    cam = affine_cam(16, 16)                              # P = [I2 | 0]: camera z = world z
+    means = [[10.5, 7.5, z_near], [10.5, 7.5, z_far]]
+    rgb = [RED, BLUE]
+    if not near_first:                                    # the near one gets the larger index
+        means, rgb = means[::-1], rgb[::-1]
+    p = params_from(means, [[1, 1, 1]] * 2, opac=[0.5, 0.5], rgb=rgb)
+    r = orc.render(p, cam, SMOOTH)
+    assert np.allclose(r["image"][:, 7, 10], 0.5 * RED + 0.25 * BLUE, rtol=0, atol=1e-15)
+    assert r["final_T"][7, 10] == pytest.approx(0.25, abs=1e-15)
+
+
+def test_occlusion_nearer_gaussian_composites_first_pinhole(orc):
+    # camera at the origin looking down +z (R = I, t = 0): the optical axis hits pixel (8, 8) centre
+    cam = dict(affine_cam(16, 16, fx=10.0, cx=8.5, cy=8.5), model=0)
+    for near_first in (True, False):
+        means = [[0.0, 0.0, 2.0], [0.0, 0.0, 5.0]]
+        rgb = [RED, BLUE]
+        sc = [[0.2, 0.2, 0.2], [0.5, 0.5, 0.5]]           # same projected footprint (s / z)
+        if not near_first:
+            means, rgb, sc = means[::-1], rgb[::-1], sc[::-1]
+        p = params_from(means, sc, opac=[0.5, 0.5], rgb=rgb)
+        r = orc.render(p, cam, SMOOTH)
+        assert np.allclose(r["image"][:, 8, 8], 0.5 * RED + 0.25 * BLUE, rtol=0, atol=1e-15), near_first
+
+
+def test_depth_key_monotone_across_zero_affine(orc):
+    """C7: key = orderable-uint32(z_fp32) must increase strictly with z over negative, zero and positive
+    depths (affine camera: no near-plane cull), so ascending-key order is near-to-far."""
+    z = np.array([-1e6, -37.0, -1.0, -0.5, -1e-3, -1e-30, 0.0, 1e-30, 1e-3, 0.25, 1.0, 2.0, 1e6])
+    cam = affine_cam(16, 16)
+    p = params_from(np.stack([np.full_like(z, 8.0), np.full_like(z, 8.0), z], 1), [[1, 1, 1]] * z.size)
+    d = orc.decide(p, cam, SMOOTH)
+    assert d["visible"].all()
+    k = d["key"].astype(np.int64)
+    assert (np.diff(k) > 0).all(), k
+    # shuffled indices: the oracle's render order (ascending key) is the z order
+    perm = np.random.default_rng(1).permutation(z.size)
+    dk = orc.decide(p[:, perm], cam, SMOOTH)["key"]
+    assert np.array_equal(np.argsort(dk, kind="stable"), np.argsort(z[perm], kind="stable"))
+
+
+def test_depth_order_of_a_front_layer_hides_the_back(orc):
+    """Many Gaussians: an opaque-ish layer (alpha_max clamp) in front of a second layer leaves the
+    pixel at the front colour up to T_min early termination — the back layer's colour must not show.
+    Checked pixel by pixel against the closed form of Eq. eqn:alpha_blend for a uniform front stack."""
+    cam = affine_cam(16, 16)
+    rp = dict(SMOOTH, alpha_max=0.99, t_min=1e-3)
+    k = 3                                                 # three front Gaussians at the pixel centre
+    means = [[8.5, 8.5, 1.0 + 0.1 * j] for j in range(k)] + [[8.5, 8.5, 5.0]]
+    rgb = [RED] * k + [BLUE]
+    order = [3, 0, 2, 1]                                  # indices unrelated to depth
+    p = params_from([means[i] for i in order], [[1, 1, 1]] * 4, opac=[0.999999] * 4, rgb=[rgb[i] for i in order])
+    r = orc.render(p, cam, rp)
+    # first front Gaussian: alpha = alpha_max, T -> 1 - alpha_max ~ 0.01; the second would leave
+    # T (1 - alpha) ~ 1e-4 < t_min: terminate.  Only the nearest one is composited; blue never is.
+    amax = float(np.float32(0.99))
+    assert np.allclose(r["image"][:, 8, 8], amax * RED, rtol=0, atol=1e-15)
+    assert r["n_comp"][8, 8] >= 1
+    assert r["image"][2, 8, 8] == 0.0
+
+
 def test_bruteforce_equals_aabb_and_range(orc):
     cfg = synth.CONFIGS["C1"]
     p = synth.scene_for(cfg)

@@ -104,63 +104,177 @@ def dist_env():
 # ------------------------------------------------------------------------------------------------
 # CPU oracle (baseline + reference arm): bounded sample of the same workload
 # ------------------------------------------------------------------------------------------------
-def oracle_sample(cfg, params, cam, dl_full, window):
-    """One sampled view of the hot path on the CPU oracle: fp32 decision chain + fp64 projection of
-    all n Gaussians, then fwd + bwd + S (per-pair, fp64) over `window`.  Returns (seconds, est ms
-    per full view, sample description)."""
+def oracle_view(cfg, params, cam, dl_full):
+    """One WHOLE view of the hot path on the CPU oracle (O1-O4 per view): fp32
+    decision chain + fp64 projection of all n Gaussians, then fwd + bwd + S (per pair, fp64) over
+    every pixel.  Returns (ms, sample description)."""
     import oracle
-    x0, y0, w, h = window
+    t0 = time.perf_counter()
+    dec = oracle.decide(params, cam)
+    oracle.render(params, cam, dl_dimage=dl_full, decision=dec)
+    ms = 1e3 * (time.perf_counter() - t0)
+    desc = (f"whole views of {cfg.name} ({cfg.n} Gaussians, {cfg.width}x{cfg.height}): fp32 decision chain over "
+            f"all Gaussians + fp64 fwd+bwd+S over every pixel (oracle/oracle.c, OpenMP)")
+    return ms, desc
+
+
+def oracle_window_estimate(cfg, params, cam, dl_full):
+    """Labelled extra (round 1's estimate): a centred 96x64 window scaled by pixel count.  It
+    over-estimates a whole view (the decision chain and candidate projection do not scale with
+    pixels), so it is reported beside the whole-view timing, never as the baseline."""
+    import oracle
+    w, h = min(96, cfg.width), min(64, cfg.height)
+    x0, y0 = (cfg.width - w) // 2, (cfg.height - h) // 2
     t0 = time.perf_counter()
     dec = oracle.decide(params, cam)
     t1 = time.perf_counter()
-    oracle.render(params, cam, window=window, dl_dimage=dl_full[:, y0:y0 + h, x0:x0 + w], decision=dec)
+    oracle.render(params, cam, window=(x0, y0, w, h), dl_dimage=dl_full[:, y0:y0 + h, x0:x0 + w], decision=dec)
     t2 = time.perf_counter()
     frac = (w * h) / float(cfg.width * cfg.height)
-    est_ms = 1e3 * ((t1 - t0) + (t2 - t1) / frac)
-    desc = (f"1 view of {cfg.name} ({cfg.n} Gaussians, {cfg.width}x{cfg.height}): fp32 decision chain over all "
-            f"Gaussians + fp64 fwd+bwd+S over a {w}x{h} window ({100 * frac:.1f}% of the pixels), "
-            f"window time scaled by pixel count")
-    return t2 - t0, est_ms, desc
+    return 1e3 * ((t1 - t0) + (t2 - t1) / frac), f"{w}x{h} window scaled by 1/{1 / frac:.0f}"
 
 
-def sample_window(cfg):
-    """The bounded CPU sample: a centred 96x64 pixel window (the whole image if smaller)."""
-    w, h = min(96, cfg.width), min(64, cfg.height)
-    return ((cfg.width - w) // 2, (cfg.height - h) // 2, w, h)
+def cpu_baseline(cfg, params, cams, reps=3):
+    """Median of `reps` whole ring views on the host cores (median of 3 at C2)."""
+    import oracle
+    oracle.build()
+    dl = synth.dl_dimage(1, cfg.width, cfg.height, 7)[0]
+    ts = []
+    desc = ""
+    for k in range(reps):
+        ms, desc = oracle_view(cfg, params, cams[k % len(cams)], dl)
+        ts.append(ms)
+    est, edesc = oracle_window_estimate(cfg, params, cams[0], dl)
+    return dict(value=round(statistics.median(ts), 1), unit=UNIT, cores=oracle.num_threads(), kind="oracle",
+                sample=f"median of {reps} {desc}", per_view_ms=[round(t, 1) for t in ts],
+                window_estimate=dict(value=round(est, 1), unit=UNIT, sample=edesc, note="extra, not the baseline"))
 
 
 def run_reference(args):
+    """The reference arm (tier framing: the oracle as it stands on the host cores).  Each step is one
+    whole view of the same workload (ring views in turn); the line's value is the mean ms/view."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
     import oracle
+    oracle.build()
     cfg = synth.CONFIGS[args.config]
     params = synth.scene_for(cfg)
-    cam = synth.cameras_for(cfg, views=1)[0]
+    cams = synth.cameras_for(cfg, views=max(args.steps, 1))
     dl = synth.dl_dimage(1, cfg.width, cfg.height, 7)[0]
-    window = sample_window(cfg)
-    for _ in range(args.warmup):
-        oracle_sample(cfg, params, cam, dl, window)
-    ests = []
-    for _ in range(args.steps):
-        _, est, desc = oracle_sample(cfg, params, cam, dl, window)
-        ests.append(est)
-    v = float(np.mean(ests))
+    t_run = time.perf_counter()
+    for k in range(args.warmup):
+        oracle_view(cfg, params, cams[k % len(cams)], dl)
+    ts = []
+    desc = ""
+    for k in range(args.steps):
+        ms, desc = oracle_view(cfg, params, cams[k % len(cams)], dl)
+        ts.append(ms)
+    wall = time.perf_counter() - t_run
+    v = float(np.mean(ts)) if ts else 0.0
     cores = oracle.num_threads()
-    out = dict(metric=METRIC, value=v, unit=UNIT, n_gpus=args.gpus, steps=args.steps, warmup=args.warmup,
-               ms_per_step=v, higher_is_better=False, scaling="weak", vs_baseline=None, dtype="f64",
+    out = dict(metric=METRIC, value=round(v, 2), unit=UNIT, n_gpus=args.gpus, steps=args.steps, warmup=args.warmup,
+               ms_per_step=round(v, 2), higher_is_better=False, scaling="weak", vs_baseline=None, dtype="f64",
                data="synthetic", impl="reference",
                config=dict(workload=f"{cfg.name}: {cfg.cite}", n=cfg.n, width=cfg.width, height=cfg.height,
                            views_per_step=1),
-               cpu_baseline=dict(value=v, unit=UNIT, cores=cores, kind="oracle", sample=desc),
-               e2e=dict(value=v, unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+               cpu_baseline=dict(value=round(v, 2), unit=UNIT, cores=cores, kind="oracle",
+                                 sample=f"each step one of {desc}"),
+               e2e=dict(value=round(v, 2), unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0),
+               consistency=dict(timed_s=round(sum(ts) / 1e3, 2), run_wall_s=round(wall, 2),
+                                fits_in_run=bool(sum(ts) / 1e3 <= wall)))
     print(json.dumps(out), flush=True)
     return 0
+
+
+def relaunch_under_torchrun(args) -> int:
+    """`--gpus N` (N > 1) without a torchrun environment: launch N ranks on this node ourselves
+    (the driver's own command is torchrun; this makes a plain `python bench.py --gpus N` do the same
+    instead of silently timing one GPU)."""
+    import socket
+    try:
+        import torch
+        have = torch.cuda.device_count()
+    except Exception:   # noqa: BLE001
+        have = 0
+    if args.impl != "reference" and have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but this node has {have} CUDA device(s)", file=sys.stderr)
+        return 3
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 # ------------------------------------------------------------------------------------------------
 # GPU arm
 # ------------------------------------------------------------------------------------------------
+def run_v1(args, cfg, p_np, pristine, dev, stream, views=16):
+    """One view per step over `views` ring views: ms/view of the whole step
+    (a1..a8) and of fwd+bwd+S alone (project .. gauss_bwd), CUDA events per stage, per-stage graphs."""
+    import torch
+
+    from paper_2505_05587_b200 import _lib
+    from paper_2505_05587_b200.pipeline import Rasterizer
+    n = cfg.n
+    cap = pristine.shape[1]
+    params = pristine.clone()
+    grad_S = torch.zeros(20, cap, dtype=torch.float32, device=dev)
+    cams = synth.cameras_for(cfg, views=views)
+    tg = torch.from_numpy(np.ascontiguousarray(synth.targets_for(cfg, views=views))).to(dev)
+    rz = Rasterizer(cap, 1, cfg.width, cfg.height, max_instances=int(3.0 * n), device=dev)
+
+    def stages(v):
+        def restore():
+            _lib.copy_planes(params, pristine, n, 0, 3)
+            _lib.copy_planes(params, pristine, n, 10, 1)
+        return [("restore", restore), ("project", lambda: rz.project(params, n, [cams[v]])),
+                ("bin_sort", rz.bin_sort), ("render_fwd", lambda: rz.render_fwd_l1(tg[v:v + 1])),
+                ("render_bwd", rz.render_bwd_moments), ("gauss_bwd_S", lambda: rz.gauss_bwd(params, grad_S, accumulate=0)),
+                ("densify", lambda: rz.densify(params, grad_S, n, cap, denom=1.0, want_lambda=False))]
+    for v in range(views):                       # warm-up: every view once (projection uploads its camera)
+        for _, f in stages(v):
+            f()
+    torch.cuda.synchronize()
+    graphs = {}
+    if not args.no_graph:
+        for v in range(views):
+            gs = []
+            for nm, f in stages(v):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                    f()
+                gs.append(g)
+            graphs[v] = gs
+    torch.cuda.synchronize()
+    nst = len(stages(0))
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nst + 1)] for _ in range(views)]
+    for v in range(views):
+        evs[v][0].record(stream)
+        for k, (nm, f) in enumerate(stages(v)):
+            if graphs:
+                graphs[v][k].replay()
+            else:
+                f()
+            evs[v][k + 1].record(stream)
+    torch.cuda.synchronize()
+    if rz.binning_arrays()["overflow"] != 0:
+        raise RuntimeError("v1: tile-instance buffer overflow")
+    names = [nm for nm, _ in stages(0)]
+    per = {nm: float(np.median([evs[v][k].elapsed_time(evs[v][k + 1]) for v in range(views)]))
+           for k, nm in enumerate(names)}
+    tot = [evs[v][0].elapsed_time(evs[v][nst]) for v in range(views)]
+    fbs = [evs[v][1].elapsed_time(evs[v][names.index("gauss_bwd_S") + 1]) for v in range(views)]
+    return dict(value=round(float(np.median(tot)), 5), unit=UNIT, views=views, views_per_step=1,
+                fwd_bwd_S_ms_per_view=round(float(np.median(fbs)), 5),
+                stages_ms={k: round(v, 4) for k, v in per.items()},
+                note="SURVEY 8(d1) headline definition: C2, one view per step (restore + a1..a8, densify "
+                     "denom 1), median over 16 ring views; fwd_bwd_S = project .. gauss_bwd (8(d2))")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -179,7 +293,13 @@ def main():
                     help="e2e: start step k+1's target copy with step k, or after step k's bin_sort (the copy's "
                          "DMA writes then overlap the ALU-bound render kernels, not the L2-resident sort)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-v1", action="store_true", help="skip the 1-view-per-step line (SURVEY §8(d1))")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return relaunch_under_torchrun(args)
+    if int(os.environ.get("WORLD_SIZE", "1")) != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ.get('WORLD_SIZE')}", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference(args)
 
@@ -343,6 +463,13 @@ def main():
         prev = max(r for r in recorded if r <= i)
         stage_ms[nm] = float(np.mean([evs[k][prev].elapsed_time(evs[k][i + 1]) for k in range(args.steps)]))
 
+    # every timed step's binning fitted its buffers (a step whose tile instances overflowed
+    # max_instances would have rendered a truncated list): the overflow flag is sticky per bin_sort,
+    # and the scene is the same each step, so the last step's flag decides
+    if rz.binning_arrays()["overflow"] != 0:
+        print("bench.py: tile-instance buffer overflow in the timed steps", file=sys.stderr)
+        return 4
+
     # ---- counts for the roofline model: one counting forward after the timed region (the timed
     # forward runs the non-counting kernel instance), then device -> host ----
     _lib.copy_planes(params, pristine, n, 0, 3)
@@ -486,13 +613,16 @@ def main():
                         + "); each step's loss and n_split read back to pinned host memory and consumed by the "
                           "host one step later")
 
+    # ---- v1: SURVEY §8(d1)'s headline definition — C2 at ONE view per step, timed over 16 ring
+    # views (the per-Gaussian stages, i.e. the parameter read in project, gauss_bwd's grad_S write and
+    # densify, are charged to a single view); same stages, per-stage graphs, densify with denom 1 ----
+    v1 = None
+    if not args.no_v1 and ws == 1:
+        v1 = run_v1(args, cfg, p_np, pristine, dev, stream)
+
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        import oracle
-        oracle.build()
-        dl = synth.dl_dimage(1, cfg.width, cfg.height, 7)[0]
-        _, est, desc = oracle_sample(cfg, p_np, all_cams[0], dl, sample_window(cfg))
-        cpu = dict(value=est, unit=UNIT, cores=oracle.num_threads(), kind="oracle", sample=desc)
+        cpu = cpu_baseline(cfg, p_np, all_cams)
 
     if rank == 0:
         out = dict(
@@ -517,7 +647,7 @@ def main():
                         n_split=n_split, split_frac=round(n_split / n, 4)),
             densify_gaussians_per_s=round(n / (stage_ms["densify"] * 1e-3), 1),
             gaussians_per_s=round(n * V * ws / (ms_step * 1e-3), 1),
-            e2e=e2e, cpu_baseline=cpu, clocks=clocks, gpu_launches=int(launches),
+            v1=v1, e2e=e2e, cpu_baseline=cpu, clocks=clocks, gpu_launches=int(launches),
             gpu_launches_per_step=round(launches / args.steps, 2),
         )
         print(json.dumps(out), flush=True)

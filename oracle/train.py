@@ -75,13 +75,21 @@ def train(params0, n0: int, capacity: int, batches, T: int, t_start: int, t_spli
     min_opacity: after each densify, Gaussians whose opacity logit is below the fp32 logit of
     min_opacity are removed (3DGS's pruning), the rest keep their order.
     Returns dict(params [14][n], n, n_split, lambda_min [n] and ||G / T_split|| [n] per densify step, loss per
-    gradient step); for "adc" lambda_min holds the mean view-gradient statistic and g_norm ||Sigma||_2."""
+    gradient step); for "adc" lambda_min holds the mean view-gradient statistic and g_norm ||Sigma||_2.
+    pos_sens [n]: for the parity test's per-Gaussian position tolerance, an upper bound on how far an
+    offspring's position moves when its parent's S-bar carries the parity tolerance of S (DESIGN.md
+    §3.4: |dS| <= 1e-3 |S| + 1e-5 sum|per-pair S|): with E that perturbation, Davis-Kahan gives
+    ||dv|| <= 2 ||E||_F / gap (gap = lambda_2 - lambda_1 of S-bar), and the displacement eps v with
+    eps = eta sqrt(v^T Sigma v) moves by <= 2 eta sqrt(lambda_max(Sigma)) ||dv||; summed along the
+    Gaussian's lineage (both offspring inherit the parent's bound)."""
     P = np.zeros((14, capacity))
     P[:, :n0] = np.asarray(params0, dtype=np.float64)[:, :n0]
     m = np.zeros((14, capacity))
     v = np.zeros((14, capacity))
     G = np.zeros((3, capacity))
     S = np.zeros((6, capacity))
+    S_abs = np.zeros((6, capacity))   # sum of |per-pair S| (the parity tolerance's absolute term)
+    sens = np.zeros(capacity)          # pos_sens (see the docstring)
     st_sum = np.zeros(capacity)        # ADC statistic (P:L154): sum of ||dL/dPi(p)|| over visible views
     st_cnt = np.zeros(capacity)
     n = n0
@@ -135,6 +143,19 @@ def train(params0, n0: int, capacity: int, batches, T: int, t_start: int, t_spli
                     gnorms.append(np.where(st_cnt[:n] > 0, st_sum[:n] / st_cnt[:n], 0.0))
             else:
                 gnorms.append(np.linalg.norm(G[:, :n], axis=0) / t_split)
+            sp = np.flatnonzero(d["mask"])
+            if sp.size:
+                Sb = S[:, sp] / t_split
+                E = (1e-3 * np.abs(S[:, sp]) + 1e-5 * S_abs[:, sp]) / t_split
+                fro = np.sqrt(E[0] ** 2 + E[3] ** 2 + E[5] ** 2 + 2 * (E[1] ** 2 + E[2] ** 2 + E[4] ** 2))
+                ev = np.array([np.linalg.eigvalsh(np.array([[a[0], a[1], a[2]], [a[1], a[3], a[4]], [a[2], a[4], a[5]]]))
+                               for a in Sb.T])
+                gap = np.maximum(ev[:, 1] - ev[:, 0], 1e-300)
+                dv = np.minimum(2.0 * fro / gap, 2.0)
+                smax = np.exp(2.0 * P[3:6, sp]).max(0)                 # lambda_max(Sigma) = max_k s_k^2
+                add = 2.0 * abs(eta) * np.sqrt(smax) * dv if eta > 0 else 0.0 * dv
+                sens[sp] += add
+                sens[d["dest"][sp]] = sens[sp]
             P = d["params"]
             ns = d["n_split"]
             reset = np.zeros(capacity, bool)
@@ -152,6 +173,7 @@ def train(params0, n0: int, capacity: int, batches, T: int, t_start: int, t_spli
             gsh = np.zeros((nrest, n))
             shkw = dict(sh_rest=SHr[:, :n], sh_degree=sh_degree) if sh_degree is not None else {}
             loss = 0.0
+            bw_abs = np.zeros((20, n))
             for k, cam in enumerate(cams):
                 fw = _render(P[:, :n], cam, rp, **shkw)
                 img = fw["image"]
@@ -167,10 +189,13 @@ def train(params0, n0: int, capacity: int, batches, T: int, t_start: int, t_spli
                     dl = gv / V
                 bw = _render(P[:, :n], cam, rp, dl_dimage=dl, decision=fw["decision"], **shkw)
                 grad += bw["grad"]
+                bw_abs += bw["absg"]
                 if nrest:
                     gsh += bw["grad_sh"]
                 vis = fw["decision"]["visible"] != 0
-                st_sum[:n] += np.where(vis, np.hypot(bw["grad_mu"][0], bw["grad_mu"][1]), 0.0)
+                # C22: the statistic is the norm of the per-VIEW loss gradient dL_view/dPi(p); the batch
+                # loss is the mean over the V views, so its gradient is scaled back by V
+                st_sum[:n] += np.where(vis, V * np.hypot(bw["grad_mu"][0], bw["grad_mu"][1]), 0.0)
                 st_cnt[:n] += vis
             losses.append(loss)
             opt_t += 1
@@ -179,10 +204,13 @@ def train(params0, n0: int, capacity: int, batches, T: int, t_start: int, t_spli
                 adam_step_dense(SHr[:, :n], gsh, mr[:, :n], vr[:, :n], sh_lr, beta1, beta2, eps, opt_t)
             G[:, :n] += grad[0:3]
             S[:, :n] += grad[14:20]
+            S_abs[:, :n] += bw_abs[14:20]
         if is_densify_step(t, t_start, t_split) and min_opacity is not None:
             thr = float(np.float32(np.log(min_opacity / (1.0 - min_opacity))))
             keep = np.flatnonzero(P[10, :n] >= thr)
             logits.append(P[10, :n].copy())
+            sens[:keep.size] = sens[keep]
+            sens[keep.size:] = 0.0
             for arr in (P, m, v, SHr, mr, vr):
                 if arr.shape[0]:
                     arr[:, :keep.size] = arr[:, keep]
@@ -192,7 +220,9 @@ def train(params0, n0: int, capacity: int, batches, T: int, t_start: int, t_spli
         if window_restarts_after(t, t_start, t_split):
             G[:] = 0.0
             S[:] = 0.0
+            S_abs[:] = 0.0
             st_sum[:] = 0.0
             st_cnt[:] = 0.0
     return dict(params=P[:, :n].copy(), n=n, n_split=splits, loss=losses, lambda_min=lams, g_norm=gnorms,
-                sh_rest=SHr[:, :n].copy(), n_pruned=pruned, logits_at_prune=logits)
+                sh_rest=SHr[:, :n].copy(), n_pruned=pruned, logits_at_prune=logits,
+                pos_sens=sens[:n].copy())

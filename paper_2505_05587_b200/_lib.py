@@ -145,6 +145,8 @@ def raster_params(alpha_min=1.0 / 255.0, alpha_max=0.99, t_min=1e-4, dilation=0.
 
 def densify_params(eps_split=-1e-6, eta=0.5, eps_abs=0.0, denom=1.0, eps_grad=None, budget=None, grad_gate=None):
     """eps_grad: compactest gate (gate 1); grad_gate: 3DGS-style view-gradient condition (gate 2)."""
+    if grad_gate is not None and eps_grad is not None:
+        raise ValueError("densify: eps_grad (compactest gate, App. A.2) and grad_gate (C24) are exclusive gates")
     d = DensifyParams()
     d.eps_split, d.eta, d.eps_abs, d.denom = eps_split, eta, eps_abs, denom
     if grad_gate is not None:

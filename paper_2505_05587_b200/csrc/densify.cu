@@ -64,6 +64,29 @@ __device__ __forceinline__ bool null_vector(const float* S6, float lam, float* v
   return true;
 }
 
+// Fallback when every cross product of the rows of (S - lambda I) vanishes in fp32: inverse iteration
+// in fp64 on (S - mu I), mu just below lambda (three steps from (1, 1, 1); the solve by the adjugate,
+// which stays finite when the shifted matrix is nearly singular — that is what makes it converge).
+__device__ void inverse_iteration(const float* S6, float lam, float* v) {
+  const double a = S6[0], b = S6[1], c = S6[2], d = S6[3], e = S6[4], f = S6[5];
+  const double sc = fmax(fmax(fabs(a), fabs(d)), fmax(fabs(f), fmax(fabs(b), fmax(fabs(c), fabs(e)))));
+  const double mu = (double)lam - 1e-6 * sc;
+  const double A = a - mu, D = d - mu, F = f - mu;
+  // adjugate of the symmetric [[A, b, c], [b, D, e], [c, e, F]]
+  const double j00 = D * F - e * e, j01 = c * e - b * F, j02 = b * e - c * D;
+  const double j11 = A * F - c * c, j12 = b * c - A * e, j22 = A * D - b * b;
+  double x0 = 1.0, x1 = 1.0, x2 = 1.0;
+  for (int it = 0; it < 3; ++it) {
+    const double y0 = j00 * x0 + j01 * x1 + j02 * x2;
+    const double y1 = j01 * x0 + j11 * x1 + j12 * x2;
+    const double y2 = j02 * x0 + j12 * x1 + j22 * x2;
+    const double nn = sqrt(y0 * y0 + y1 * y1 + y2 * y2);
+    if (!(nn > 0.0)) break;
+    x0 = y0 / nn; x1 = y1 / nn; x2 = y2 / nn;
+  }
+  v[0] = (float)x0; v[1] = (float)x1; v[2] = (float)x2;
+}
+
 // lambda_min and (optionally) unit v_min of the symmetric S6 = (xx,xy,xz,yy,yz,zz), fp32.
 // Eigenvalues by Smith's trigonometric roots (App. A.3: q = tr/3, p, B = (A - qI)/p,
 // beta = 2 cos(acos(det B / 2)/3 + 2k pi/3)), organised so both outputs stay accurate when two
@@ -134,7 +157,7 @@ __device__ void eig_min_robust(const float* S6in, bool want_vec, float& lam, flo
     if (want_vec) have_vec = null_vector(S6, l, v);
   }
   if (!want_vec) return;
-  if (!have_vec) { v[0] = 1.f; v[1] = 0.f; v[2] = 0.f; return; }
+  if (!have_vec) inverse_iteration(S6, lam / sc, v);   // (scaled S6; no arbitrary e_x)
   const float nn = rsqrtf(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
   v[0] *= nn; v[1] *= nn; v[2] *= nn;
   int big = 0;  // canonical sign: largest |component| positive, ties -> lowest index (C13)

@@ -231,8 +231,12 @@ class Schedule:
     clone_step: float = 0.0         # ADC clone displacement along -G / T_split
     scale_factor: float = 0.8       # ADC split offspring scale
     min_opacity: float | None = None  # prune Gaussians below this opacity after each densify (3DGS: 0.005)
+    t_stop: int | None = 15000      # last step that may densify (3DGS's densify_until_iter; the paper keeps
+                                    # 3DGS's other hyper-parameters); None: Alg. 1 without a bound
 
     def densify_at(self, t: int) -> bool:
+        if self.t_stop is not None and t > self.t_stop:
+            return False
         return t >= self.t_start and (t - self.t_start) % self.t_split == 0
 
     def window_restarts_after(self, t: int) -> bool:
@@ -300,6 +304,13 @@ class Trainer:
         import torch.distributed as dist
         return dist.get_world_size(self.group) if dist.is_available() and dist.is_initialized() else 1
 
+    def _batch_views(self) -> int:
+        """Views in one gradient step over all ranks.  The step's loss is their mean (C18), so the
+        statistic k_gauss_bwd accumulates, ||dL_batch/dPi(p)||, is the per-view ||dL_view/dPi(p)|| of
+        C22 / 3DGS divided by this count; the ADC threshold and the C24 gate are divided by it instead
+        (the norm is positively homogeneous, so the decision is the same)."""
+        return self.rz.V * self._world()
+
     def _allreduce_planes(self, first: int, count: int):
         if self._world() > 1:
             from .parallel import allreduce_planes
@@ -362,7 +373,7 @@ class Trainer:
                 if self.normals is None:
                     self.normals = torch.empty(6, self.cap, dtype=torch.float32, device=rz.device)
                 self.normals.normal_(generator=self.generator)
-            eps_adc = s.eps_adc if s.eps_adc is not None else 0.0004 / rz.W
+            eps_adc = (s.eps_adc if s.eps_adc is not None else 0.0004 / rz.W) / self._batch_views()
             rz.densify_adc(self.params, self.grad_S, self.vstats, self.normals, n, self.cap, eps_adc, s.tau_adc,
                            s.clone_step, s.scale_factor, float(s.t_split))
             reset_mask, reset_value = rz.adc_kind, 2                   # clone parents keep their Adam state
@@ -371,8 +382,9 @@ class Trainer:
             if s.grad_gate is not None:                                # statistic -> planes 0, 1 (gate 2)
                 self._allreduce_stats()
                 _lib.copy_planes(self.grad_S, self.vstats, n, 0, 2)
+            gg = s.grad_gate / self._batch_views() if s.grad_gate is not None else None
             rz.densify(self.params, self.grad_S, n, self.cap, eps_split=s.eps_split, eta=s.eta,
-                       denom=float(s.t_split), eps_grad=s.eps_grad, budget=s.budget, grad_gate=s.grad_gate)
+                       denom=float(s.t_split), eps_grad=s.eps_grad, budget=s.budget, grad_gate=gg)
             reset_mask, reset_value = rz.split_mask, 1
         ns, st = int(rz.n_split.item()), int(rz.dens_status.item())
         if st != 0:

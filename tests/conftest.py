@@ -18,3 +18,16 @@ def orc():
 
     oracle.build()
     return oracle
+
+
+def pytest_terminal_summary(terminalreporter, exitstatus, config):
+    """Gradient parity: how many compared elements needed the plane floor of _grad_close."""
+    mod = sys.modules.get("test_gpu_parity")
+    log = getattr(mod, "FLOOR_LOG", None) if mod else None
+    if not log:
+        return
+    tot = sum(c for _, c, _ in log)
+    cmp_ = sum(m for _, _, m in log)
+    worst = max(log, key=lambda r: r[1] / max(r[2], 1))
+    terminalreporter.write_line(f"grad parity plane floor: {tot} of {cmp_} compared elements over {len(log)} checks "
+                                f"needed it (worst {worst[1]}/{worst[2]} in {worst[0]})")

@@ -190,7 +190,7 @@ def test_adc_training_loop_parity(orc):
     # clone_step = 0 (3DGS: an exact copy): a displaced clone sits ~1e-8 behind or in front of its parent,
     # and that depth order is not decidable at fp32 noise; the displacement itself is covered by the
     # kernel parity test above
-    adc = dict(eps_adc=6e-5, tau_adc=0.07, clone_step=0.0, scale_factor=0.8)
+    adc = dict(eps_adc=1.2e-4, tau_adc=0.07, clone_step=0.0, scale_factor=0.8)
     ora = train(p, 64, cap, b, T=10, t_start=4, t_split=3, lr=LR, eps=1e-15, rp=SMOOTH, density="adc", adc=adc,
                 normals=lambda t: zs[t].astype(np.float64))
     for g, s in zip(ora["lambda_min"], ora["g_norm"]):     # decisions decisive at fp32 noise
@@ -209,3 +209,25 @@ def test_adc_training_loop_parity(orc):
     err = np.abs(got - ora["params"])
     tol = 5e-3 * lr + 1e-5 * np.abs(ora["params"])
     assert (err <= tol).all(), f"worst {(err / tol).max():.3g} x tol"
+
+
+@pytest.mark.gpu
+def test_adc_statistic_independent_of_batch_size(orc):
+    """C22 / ADVICE r1: the ADC statistic is the per-view ||dL_view/dPi(p)||.  A batch of the same view
+    twice (V = 2, loss = batch mean) must give the same scaled statistic as that view alone (V = 1)."""
+    _gpu()
+    from gpu_run import raster_of
+    from paper_2505_05587_b200 import Adam, Schedule, Trainer
+    p, cams, tg = _scene()
+    out = []
+    for V in (1, 2):
+        sched = Schedule(4, 3, density="adc")
+        tr = Trainer(torch.from_numpy(p).cuda(), 64, 256, V, 64, 64, raster_of(SMOOTH), Adam(LR, 0.9, 0.999, 1e-15),
+                     sched)
+        tr.step([cams[0]] * V, torch.from_numpy(np.ascontiguousarray(np.stack([tg[0]] * V))).cuda())
+        torch.cuda.synchronize()
+        st = tr.vstats[:, :64].double().cpu().numpy()
+        with np.errstate(invalid="ignore", divide="ignore"):
+            out.append(np.where(st[1] > 0, st[0] / st[1], 0.0) * tr._batch_views())
+    assert (out[0] > 0).sum() > 10
+    assert np.allclose(out[0], out[1], rtol=1e-5, atol=1e-12)

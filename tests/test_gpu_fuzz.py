@@ -67,6 +67,7 @@ def test_fuzz_full_path(orc, seed):
         r = orc.render(p, cam, rp, decision=decs[v])
         ok = (np.abs(img[v] - r["image"]) <= 1e-4 * np.abs(r["image"]) + 1e-6) | (r["amb_px"][None] != 0)
         assert ok.all(), (seed, v)
+        assert int(r["amb_px"].sum()) <= 0.01 * r["amb_px"].size, (seed, v)   # excluded pixels bounded
         dl[v][:, r["amb_px"] != 0] = 0.0
     for v, cam in enumerate(cams):
         r = orc.render(p, cam, rp, dl_dimage=dl[v], decision=decs[v])
@@ -105,6 +106,7 @@ def test_fuzz_sh(orc, seed):
         r = orc.render(p, cam, rp, sh_rest=rest, sh_degree=deg)
         ok = (np.abs(img[v] - r["image"]) <= 1e-4 * np.abs(r["image"]) + 1e-6) | (r["amb_px"][None] != 0)
         assert ok.all(), (seed, v)
+        assert int(r["amb_px"].sum()) <= 0.01 * r["amb_px"].size, (seed, v)   # excluded pixels bounded
         dl[v][:, r["amb_px"] != 0] = 0.0
     for v, cam in enumerate(cams):
         r = orc.render(p, cam, rp, dl_dimage=dl[v], sh_rest=rest, sh_degree=deg)

@@ -145,13 +145,28 @@ def test_render_fwd_parity_c1(orc, model, rp):
         assert (okT | (o["amb_px"] != 0)).all()
 
 
-def _grad_close(g, o, absg, ambg, rtol=1e-3, atol_rel=1e-5, plane_rel=1e-6):
-    """|d| <= 1e-3 |ora| + 1e-5 abs_ora + 1e-6 max_i |ora[plane]|: the last term is
-    the fp32 cancellation floor of gradients that are small differences of O(|dL/dSigma| |Sigma|)
-    terms (e.g. the quaternion gradient of a nearly isotropic Gaussian)."""
+# Elements that pass only through the plane floor of _grad_close: (test id, count, compared elements);
+# printed at the end of the session by tests/conftest.py (pytest_terminal_summary).
+FLOOR_LOG: list = []
+
+
+def _grad_close(g, o, absg, ambg, rtol=1e-3, atol_rel=1e-5, plane_rel=1e-6, max_floor_frac=1e-3):
+    """|d| <= 1e-3 |ora| + 1e-5 abs_ora (north_star's rel 1e-3 plus the absolute term
+    that absorbs fp32 cancellation in per-pair sums).  A third term, 1e-6 max_i |ora[plane]|, is the
+    fp32 floor of gradients that are small differences of O(|dL/dSigma| |Sigma|) terms (e.g. the
+    quaternion gradient of a nearly isotropic Gaussian, where the per-pair terms cancel in the
+    Jacobian and not in the sum abs_ora sees).  It is allowed for at most max(4, 1e-3 of the compared
+    elements) per call; the count is asserted, logged and printed at the end of the run."""
+    import os
+    d = np.abs(g - o)
+    strict = d <= rtol * np.abs(o) + atol_rel * absg + 1e-30
     floor = plane_rel * np.abs(o).max(axis=1, keepdims=True)
-    ok = np.abs(g - o) <= rtol * np.abs(o) + atol_rel * absg + floor + 1e-30
+    ok = d <= rtol * np.abs(o) + atol_rel * absg + floor + 1e-30
     ok[:, ambg != 0] = True
+    strict[:, ambg != 0] = True
+    need = int((ok & ~strict).sum())
+    FLOOR_LOG.append((os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0], need, int(strict.size)))
+    assert need <= max(4, max_floor_frac * strict.size), f"{need} of {strict.size} elements need the plane floor"
     return ok
 
 
@@ -223,6 +238,8 @@ def test_render_windows_full_size(orc, name):
         win[:, r["amb_px"] != 0] = 0.0                      # ambiguous pixels carry no gradient
         dl[:, y0:y0 + h, x0:x0 + w] = win
         n_amb_px += int(r["amb_px"].sum())
+    # excluded pixels are bounded (threshold decisions within rounding are rare)
+    assert n_amb_px <= 0.01 * sum(w * h for (_, _, w, h) in windows), n_amb_px
     g = run_backward(rz, pt, dl[None])
     o = np.zeros_like(g); a = np.zeros_like(g); amb = np.zeros(p.shape[1], np.uint8)
     for (x0, y0, w, h) in windows:
@@ -358,6 +375,31 @@ def test_densify_parity(orc, eta):
     fro = np.abs(S[:, sp]).max(0) / denom
     near_degenerate = gap < 1e-3 * fro
     assert (same | swap | near_degenerate).all(), int((~(same | swap | near_degenerate)).sum())
+    # Z16, for every split parent (and the only check where the min-eigenspace is (nearly) repeated):
+    # v = (A - B) / |A - B| is a unit min-eigenvector of S-bar by its residual and Rayleigh quotient,
+    # and the offspring half-distance is eps = eta sqrt(v^T Sigma v) (C15) or eps_abs.
+    from scipy.spatial.transform import Rotation
+    dAB = ga - gb
+    half = 0.5 * np.linalg.norm(dAB, axis=0)
+    v = dAB / np.maximum(2.0 * half, 1e-300)
+    Sb = S[:, sp].astype(np.float64) / denom
+    Sm = np.stack([np.stack([Sb[0], Sb[1], Sb[2]]), np.stack([Sb[1], Sb[3], Sb[4]]),
+                   np.stack([Sb[2], Sb[4], Sb[5]])]).transpose(2, 0, 1)           # [k][3][3]
+    lam_o = r["lambda_min"][sp]
+    Sv = np.einsum("kab,bk->ak", Sm, v)
+    res = np.linalg.norm(Sv - lam_o[None] * v, axis=0)
+    rq = np.einsum("ak,ak->k", v, Sv)
+    fro_f = np.linalg.norm(Sm.reshape(-1, 9), axis=1)
+    # the position difference carries ~1e-7 |p| / half of rounding in v, and the fp32 eigensolve ~1e-6
+    vtol = 1e-4 * fro_f + fro_f * 4e-7 * scale / np.maximum(half, 1e-30)
+    assert (res <= np.maximum(vtol, gap + vtol)).all(), np.max(res / np.maximum(vtol, gap + vtol))
+    assert (np.abs(rq - lam_o) <= np.maximum(vtol, gap + vtol)).all()
+    q = p[6:10, sp].astype(np.float64)
+    Rm = Rotation.from_quat(np.stack([q[1], q[2], q[3], q[0]], 1)).as_matrix()  # scipy: (x, y, z, w)
+    s2 = np.exp(2.0 * p[3:6, sp].astype(np.float64)).T
+    Sig = np.einsum("kab,kb,kcb->kac", Rm, s2, Rm)
+    eps_ref = eta * np.sqrt(np.einsum("ak,kab,bk->k", v, Sig, v)) if eta > 0 else np.full(sp.size, 0.05)
+    assert np.allclose(half, eps_ref, rtol=2e-4, atol=1e-6 * scale), np.max(np.abs(half - eps_ref) / eps_ref)
     assert np.allclose(0.5 * (ga + gb), p[0:3, sp], atol=1e-6 * scale)    # mean(offspring) = parent
     assert np.abs(Pg[10, sp] - r["params"][10, sp]).max() <= 1e-6
     assert np.abs(Pg[10, b] - r["params"][10, b]).max() <= 1e-6
@@ -506,11 +548,14 @@ def test_bench_launch_configuration_c2(orc):
     dl = np.zeros((V, 3, H, W), np.float32)
     full = synth.dl_dimage(V, W, H, 17)
     wins = {2: [(100, 60, 40, 32)], 5: [(W - 49, H - 45, 49, 45), (W // 2, H // 2, 32, 24)]}
+    n_amb = 0
     for v, ws in wins.items():
         for (x0, y0, w, h) in ws:
             r = orc.render(p, cams[v], DEFAULT, window=(x0, y0, w, h), decision=decs[v])
             ok = _img_close(img[v][:, y0:y0 + h, x0:x0 + w], r["image"], r["amb_px"])
             assert ok.all()
+            n_amb += int(r["amb_px"].sum())
+            assert n_amb <= 0.01 * sum(w_ * h_ for ws_ in wins.values() for (_, _, w_, h_) in ws_)
             win = full[v][:, y0:y0 + h, x0:x0 + w].copy()
             win[:, r["amb_px"] != 0] = 0.0
             dl[v][:, y0:y0 + h, x0:x0 + w] = win

@@ -171,3 +171,33 @@ def test_bench_reference_arm_runs_on_cpu():
     assert d["impl"] == "reference" and d["unit"] == "ms/view" and d["higher_is_better"] is False
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["value"] > 0
+
+
+def test_schedule_densify_until_and_exclusive_gates():
+    """Schedule.t_stop (3DGS's densify_until_iter): no densify step and no window restart after it;
+    densify_params rejects the compactest gate together with the C24 gate (ADVICE r1)."""
+    from paper_2505_05587_b200 import _lib
+    from paper_2505_05587_b200.pipeline import Schedule
+    s = Schedule(t_start=5, t_split=3, t_stop=20)
+    assert [t for t in range(1, 40) if s.densify_at(t)] == [5, 8, 11, 14, 17, 20]
+    assert [t for t in range(1, 40) if s.window_restarts_after(t)] == [2, 5, 8, 11, 14, 17, 20]
+    assert Schedule().t_stop == 15000 and not Schedule(t_start=500, t_split=100).densify_at(15100)
+    assert Schedule(t_start=500, t_split=100, t_stop=None).densify_at(15100)
+    with pytest.raises(ValueError):
+        _lib.densify_params(eps_grad=1e-3, grad_gate=1e-4)
+
+
+def test_bench_gpus_flag_never_times_fewer_ranks():
+    """`python bench.py --gpus 2` without torchrun launches 2 ranks itself, and fails loudly (non-zero,
+    nothing printed on stdout) when the node has fewer devices; a WORLD_SIZE that disagrees with
+    --gpus is an error too (VERDICT r1 weak #14)."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1", "--warmup", "0"],
+                       capture_output=True, text=True, timeout=300, env={k: v for k, v in os.environ.items()
+                                                                         if k not in ("WORLD_SIZE", "RANK")})
+    import torch
+    if torch.cuda.device_count() < 2:
+        assert r.returncode == 3 and "CUDA device" in r.stderr and r.stdout.strip() == ""
+    env = dict(os.environ, WORLD_SIZE="4", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--impl", "reference",
+                        "--steps", "0", "--warmup", "0"], capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 2 and "WORLD_SIZE" in r.stderr and r.stdout.strip() == ""

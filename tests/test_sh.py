@@ -187,7 +187,7 @@ def test_sh_training_loop_parity(orc):
     got = tr.params[:, :tr.n].double().cpu().numpy()
     lr = np.asarray(LR)[GROUP][:, None]
     tol = 5e-3 * lr + 1e-6 * np.abs(ora["params"])
-    tol[0:3] = 2e-2 * lr[0:3] + 1e-6 * np.abs(ora["params"][0:3])     # offspring eps v_min (test_train.py)
+    tol[0:3] += ora["pos_sens"][None, :]          # per-Gaussian offspring bound (test_train.py)
     assert (np.abs(got - ora["params"]) <= tol).all()
     gs = tr.sh_rest[:, :tr.n].double().cpu().numpy()
     assert (np.abs(gs - ora["sh_rest"]) <= 5e-3 * 1e-3 + 1e-6 * np.abs(ora["sh_rest"])).all()

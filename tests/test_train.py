@@ -172,7 +172,7 @@ def test_training_loop_parity(orc, variant):
     elif variant == "gate":
         kw["eps_grad"] = 1e-3
     elif variant == "grad_gate":
-        kw["grad_gate"] = 7e-5
+        kw["grad_gate"] = 1.4e-4
     T, t_start, t_split, cap, eps = 10, 4, 3, 512, 1e-15     # 3DGS's Adam eps
     ssim_lam = 0.2 if variant == "ssim" else None
     ora = train(p, 64, cap, _batches(cams, tg), T=T, t_start=t_start, t_split=t_split, lr=LR, eps=eps, rp=SMOOTH,
@@ -183,7 +183,7 @@ def test_training_loop_parity(orc, variant):
         if variant == "gate":
             assert np.abs(gn - 1e-3).min() > 1e-3 * 1e-3
         if variant == "grad_gate":
-            assert np.abs(gn / 7e-5 - 1).min() > 2e-4
+            assert np.abs(gn / 1.4e-4 - 1).min() > 2e-4
         assert np.abs(lam - (-1e-6)).min() > 1e-4 * scale
         if variant == "budget":
             srt = np.sort(lam)
@@ -202,10 +202,12 @@ def test_training_loop_parity(orc, variant):
     ref = ora["params"]
     lr = np.asarray(LR)[GROUP][:, None]
     err = np.abs(got - ref)
-    # measured worst (scripts/diag_train.py): 1.5e-3 lr on non-position planes; positions up to 5e-3 lr
-    # because an offspring's displacement eps v_min amplifies S's fp32 error by ||S|| / eigengap
+    # measured worst (scripts/diag_train.py): 1.5e-3 lr on non-position planes.  Positions add a
+    # per-Gaussian bound from the oracle (pos_sens, oracle/train.py): an offspring's displacement
+    # eps v_min moves by <= 2 eta sqrt(lambda_max Sigma) * 2 ||dS||_F / eigengap when S-bar carries
+    # the S parity tolerance dS, summed along the Gaussian's lineage.
     tol = 5e-3 * lr + 1e-6 * np.abs(ref)
-    tol[0:3] = 2e-2 * lr[0:3] + 1e-6 * np.abs(ref[0:3])
+    tol[0:3] += ora["pos_sens"][None, :]
     if not (err <= tol).all():
         bad = np.argwhere(err > tol)
         raise AssertionError(f"{len(bad)} params off; worst {(err / tol).max():.3g} x tol at {bad[:5].tolist()}")
@@ -272,5 +274,5 @@ def test_training_loop_with_pruning_parity(orc):
     got = tr.params[:, :tr.n].double().cpu().numpy()
     lr = np.asarray(LR)[GROUP][:, None]
     tol = 5e-3 * lr + 1e-6 * np.abs(ora["params"])
-    tol[0:3] = 2e-2 * lr[0:3] + 1e-6 * np.abs(ora["params"][0:3])
+    tol[0:3] += ora["pos_sens"][None, :]                  # per-Gaussian offspring bound (see above)
     assert (np.abs(got - ora["params"]) <= tol).all()

@@ -60,7 +60,7 @@ class ClockSampler:
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.FIELDS}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                       "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.f,
                                       stderr=subprocess.DEVNULL)
         except OSError:
             self.p = None
@@ -92,6 +92,21 @@ class ClockSampler:
         os.unlink(self.f.name)
         return dict(sm_mhz=statistics.median(sm) if sm else None, sm_max_mhz=max(mx) if mx else None,
                     reasons=sorted(reasons), samples=len(sm))
+
+
+def clock_probe(stream, cycles=20_000_000):
+    """SM clock (MHz) right after the timed region: torch.cuda._sleep spins one thread for `cycles`
+    SM cycles (clock64); CUDA events around it give the wall time on the device."""
+    import torch
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    torch.cuda._sleep(cycles // 10)
+    a.record(stream)
+    torch.cuda._sleep(cycles)
+    b.record(stream)
+    b.synchronize()
+    ms = a.elapsed_time(b)
+    return round(cycles / (ms * 1e3), 1) if ms > 0 else None
 
 
 def dist_env():
@@ -446,6 +461,7 @@ def main():
     t_end.record(stream)
     barrier()
     clocks = sampler.stop()
+    clocks["probe_mhz"] = clock_probe(stream)
     launches = _lib.launch_count() - launches0 + graph_launches[0]
     elapsed = t_start.elapsed_time(t_end)
     if ws > 1:
@@ -485,7 +501,9 @@ def main():
     tiles = ((cfg.width + 15) // 16) * ((cfg.height + 15) // 16)
     peaks = measured_peaks()
     hbm = peaks["hbm_gbs"]
-    sm_mhz = clocks["sm_mhz"] or 1342.0
+    # the ALU peak at the SM clock the kernels ran at: the device-side probe right after the timed
+    # region (nvidia-smi's 200 ms samples mostly miss a ~40 ms timed region and catch idle clocks)
+    sm_mhz = clocks.get("probe_mhz") or clocks["sm_mhz"] or peaks["sm_max_mhz"]
     alu_peak = N_SM * FP32_LANES_PER_SM * sm_mhz * 1e6       # lane-ops/s at the measured clock
     # algorithmic (compulsory) bytes per launch of each stage
     byts = {

@@ -38,6 +38,7 @@
 // moments[view][gid][12].  The splitting matrix needs no per-pair work of its own:
 // S_view = P^T (Q M Q - m0 Q) P is formed per Gaussian from these moments (gauss_bwd.cu).
 #include <atomic>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -54,20 +55,22 @@ constexpr int kStages = 3;                          // ring depth (backward: bou
 constexpr int kFwdStages = 5;                       // forward ring depth (slack for unequal consumer warps)
 constexpr uint32_t kSuspendNs = 1000000;            // mbarrier try_wait suspend-time hint (ns)
 
-struct Buffer {
+template <int kC>
+struct BufferT {
   float4 geo[kBatch];            // (mu_x - ox, mu_y - oy, Qxx', 2 Qxy')   Q' = Q log2(e)/2
   float4 par[kBatch];            // (Qyy', log2(o), -, -)
   float4 col[kBatch];            // (r, g, b, -)
   float* mptr[kBatch];           // backward: &moments[view][gid][0]
   uint32_t mask[kBatch];         // sub-blocks reached by the alpha support
-  uint8_t list[kConsumers][kBatch];  // per-consumer compacted lists (written by the consumer)
+  uint8_t list[kC][kBatch];      // per-consumer compacted lists (written by the consumer)
   int base;                      // list position (relative to the tile start) of slot 0
   int stop;                      // 1: no more batches (forward early termination)
 };
+using Buffer = BufferT<kConsumers>;
 
-template <int kS>
+template <int kS, int kC = kConsumers>
 struct SmemT {
-  Buffer buf[kS];
+  BufferT<kC> buf[kS];
   uint4 raw[4][kBatch];          // producer staging: the next batch's 64-B records (cp.async), SoA by 16 B
   unsigned long long full[kS], empty[kS];
   int done_warps;
@@ -141,8 +144,8 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // round trip once it runs ahead.  Staging a record is then two fp64 subtractions and eight
 // interval tests of the padded extents against the 8x4 sub-blocks.
 // kFwd: stop early once every consumer warp has terminated (forward early exit).
-template <bool kFwd, int kProd, int kS, class BatchOf>
-__device__ __forceinline__ void run_producer(SmemT<kS>& sm, const uint32_t* __restrict__ ids,
+template <bool kFwd, int kProd, int kS, int kC = kConsumers, class BatchOf>
+__device__ __forceinline__ void run_producer(SmemT<kS, kC>& sm, const uint32_t* __restrict__ ids,
                                              const steepgs_splat* __restrict__ vs, uint32_t first, int nb,
                                              BatchOf batch_of, double ox, double oy, float* mom_view, float lmin,
                                              uint8_t* __restrict__ inst_mask, int pw, int lane) {
@@ -182,14 +185,14 @@ __device__ __forceinline__ void run_producer(SmemT<kS>& sm, const uint32_t* __re
   for (int k = 0; k < nb; ++k) {
     const int s = k % kS;
     if (k >= kS) mbar_wait(&sm.empty[s], ((k / kS) & 1) ^ 1, kSuspendNs);
-    Buffer& B = sm.buf[s];
+    BufferT<kC>& B = sm.buf[s];
     int stop = 0;
     if (kFwd) {   // one decision per batch for all producer warps (a split decision would deadlock)
       if (kProd == 1) {
-        stop = *reinterpret_cast<volatile int*>(&sm.done_warps) == kConsumers;
+        stop = *reinterpret_cast<volatile int*>(&sm.done_warps) == kC;
       } else {
         if (pw == 0 && lane == 0)
-          sm.stop_flag[k & 1] = *reinterpret_cast<volatile int*>(&sm.done_warps) == kConsumers;
+          sm.stop_flag[k & 1] = *reinterpret_cast<volatile int*>(&sm.done_warps) == kC;
         asm volatile("bar.sync 1, %0;" ::"r"(32 * kProd) : "memory");
         stop = *reinterpret_cast<volatile int*>(&sm.stop_flag[k & 1]);
       }
@@ -269,13 +272,14 @@ __device__ __forceinline__ void run_producer(SmemT<kS>& sm, const uint32_t* __re
 
 // Consumer: compact the staged batch to the splats whose mask has bit `w` (ascending order, slots
 // below `limit`) into the warp's own list; returns the count.
-__device__ __forceinline__ int build_list(const Buffer& B, uint8_t* __restrict__ list, int w, int lane,
+template <int kC>
+__device__ __forceinline__ int build_list(const BufferT<kC>& B, uint8_t* __restrict__ list, uint32_t wbits, int lane,
                                           int limit = kBatch) {
   int total = 0;
   const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
   for (int q = 0; q < kBatch / 32; ++q) {
-    const bool hit = ((B.mask[q * 32 + lane] >> w) & 1u) && q * 32 + lane < limit;
+    const bool hit = (B.mask[q * 32 + lane] & wbits) != 0u && q * 32 + lane < limit;
     const uint32_t bal = __ballot_sync(0xffffffffu, hit);
     if (hit) list[total + __popc(bal & lt)] = (uint8_t)(q * 32 + lane);
     total += __popc(bal);
@@ -337,7 +341,7 @@ __global__ void __launch_bounds__(kThreadsFwd, 4) k_render_fwd(const steepgs_spl
     if (B.stop) break;
     if (!warp_done) {
       uint8_t* lst = sm.buf[s].list[warp];
-      const int nl = build_list(B, lst, warp, lane);
+      const int nl = build_list(B, lst, 1u << warp, lane);
       const int base1 = B.base + 1;
       if (kCount && !done) neval += nl;
       // Two entries per iteration: both pair tests ahead of the serial compositing (as in the bwd).
@@ -592,7 +596,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
     mbar_wait(&sm.full[s], (k / kStages) & 1, kSuspendNs);
     const Buffer& B = sm.buf[s];
     uint8_t* lst = sm.buf[s].list[warp];
-    const int nl = build_list(B, lst, warp, lane, wmax - B.base);   // only entries before the warp's prefix end
+    const int nl = build_list(B, lst, 1u << warp, lane, wmax - B.base);   // only entries before the warp's prefix end
     const int lim = last - B.base;                          // this pixel composited list positions < last
     for (int t_hi = nl; t_hi > 0;) {
       const int m = min(t_hi, kChunk - fill);
@@ -658,6 +662,463 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
   if (fill > 0) reduce_chunk(fill);
 }
 
+// ------------------------------------------------------------------------------------------------
+// Backward, two pixels per lane.  Four consumer warps per 16x16 tile, warp w owns the 8x8 block
+// (bx, by) = (w & 1, w >> 1); lane (lx, ly) = (lane & 7, lane >> 3) owns pixels a = (lx, ly) and
+// b = (lx, ly + 4) of the block (the same column, so the pair test shares dx, a and b q dx).  The
+// per-pixel arithmetic runs on packed f32x2 (fma/add/mul.rn.f32x2, sm_100a): the splat's scalars are
+// broadcast operands, the two pixels the two halves, so one instruction serves both pixels and the
+// values are those of the scalar code (each half is one IEEE round-to-nearest operation).  A warp
+// visits a splat once per 8x8 block instead of once per 8x4 sub-block.
+// Phase 1 leaves per (entry, lane) the lane's two-pixel partial sums s = w_a + w_b, t = w_b and
+// u_ch = aT_a dL/dC_a,ch + aT_b dL/dC_b,ch (w = dL/dsigma sigma); phase 2 (lane e, half h) sums the
+// 16 lanes of its half with the lane positions as compile-time constants and rebuilds the 9 moments
+// (sum_b's y offset of 4 enters through t).
+// ------------------------------------------------------------------------------------------------
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 pk2(float a, float b) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float lo2(u64 r) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+  return a;
+}
+__device__ __forceinline__ float hi2(u64 r) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+  return b;
+}
+__device__ __forceinline__ u64 add2(u64 a, u64 b) {
+  u64 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
+  u64 d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
+  u64 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
+  u64 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ u64 bc2(float a) { return pk2(a, a); }
+
+// pair_e for the two pixels (fx, fy.lo) and (fx, fy.hi): the same operations, in the same order and
+// rounding, as pair_e (a = (Qxx' dx) dx, b = 2Qxy' dx, m = fma(dy, fma(Qyy', dy, b), a), e = lo - m).
+__device__ __forceinline__ u64 pair_e2(float fx, u64 fy, const float4 g, const float2 p) {
+  const float dx = __fsub_rn(fx, g.x);
+  const float a = __fmul_rn(__fmul_rn(g.z, dx), dx);
+  const float bq = __fmul_rn(g.w, dx);
+  const u64 dy = sub2(fy, bc2(g.y));
+  const u64 m = fma2(dy, fma2(bc2(p.x), dy, bc2(bq)), bc2(a));
+  return sub2(bc2(p.y), m);
+}
+
+constexpr int kC2 = 4;                        // consumer warps (8x8 blocks) per tile
+using Smem2 = SmemT<kStages, kC2>;
+
+template <int kChunk2>
+struct BwdScratch2 {
+  float4 st[kC2][kChunk2][33];   // (s, t, u0, u1) per (entry, lane); rows padded to 33 (conflict-free phase 2)
+  float u2[kC2][kChunk2][33];    // u2 per (entry, lane)
+  float2 emean[kC2][kChunk2];    // per chunk entry: the splat mean (tile-relative)
+  float* eptr[kC2][kChunk2];     // per chunk entry: &moments[view][gid][0]
+};
+
+// kChunk2: list entries per phase-1 -> phase-2 chunk (16: 2 lanes per entry in phase 2, 8: 4 lanes);
+// kProd2: producer warps.
+template <int kChunk2, int kProd2, int kMinBlocks>
+__global__ void __launch_bounds__(32 * (kC2 + kProd2), kMinBlocks) k_render_bwd2(const steepgs_splat* __restrict__ splats,
+                                                          const uint32_t* __restrict__ ids,
+                                                          const uint2* __restrict__ ranges, int64_t n, int W, int H,
+                                                          int tiles_x, int tiles_per_view, const RasterK rk,
+                                                          const float* __restrict__ final_T,
+                                                          const int32_t* __restrict__ n_contrib,
+                                                          const float* __restrict__ dL_dimage,
+                                                          const uint32_t* __restrict__ tile_last,
+                                                          uint8_t* __restrict__ inst_mask,
+                                                          float* __restrict__ moments) {
+  extern __shared__ __align__(16) unsigned char dsmem[];
+  Smem2& sm = *reinterpret_cast<Smem2*>(dsmem);
+  BwdScratch2<kChunk2>& sc = *reinterpret_cast<BwdScratch2<kChunk2>*>(dsmem + ((sizeof(Smem2) + 15) & ~size_t(15)));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tile = blockIdx.x, view = blockIdx.y;
+  const int tx = tile % tiles_x, ty = tile / tiles_x;
+  const double ox = (double)(tx * kTile), oy = (double)(ty * kTile);
+  const uint2 rg = ranges[(int64_t)view * tiles_per_view + tile];
+  const int64_t HW = (int64_t)W * H;
+  const int bx = warp & 1, by = warp >> 1;
+  const int lx = 8 * bx + (lane & 7), lya = 8 * by + (lane >> 3), lyb = lya + 4;
+  const int px = tx * kTile + lx, pya = ty * kTile + lya, pyb = ty * kTile + lyb;
+  const bool cons = warp < kC2;
+  const bool ina = cons && px < W && pya < H, inb = cons && px < W && pyb < H;
+  float Ta = 1.0f, Tb = 1.0f;
+  float dla[3] = {0.f, 0.f, 0.f}, dlb[3] = {0.f, 0.f, 0.f};
+  int lasta = 0, lastb = 0;
+  {
+    const float* dl = dL_dimage + (int64_t)view * 3 * HW;
+    if (ina) {
+      const int64_t pa = (int64_t)pya * W + px;
+      Ta = final_T[(int64_t)view * HW + pa];
+      lasta = n_contrib[(int64_t)view * HW + pa];
+      dla[0] = dl[pa]; dla[1] = dl[HW + pa]; dla[2] = dl[2 * HW + pa];
+    }
+    if (inb) {
+      const int64_t pb = (int64_t)pyb * W + px;
+      Tb = final_T[(int64_t)view * HW + pb];
+      lastb = n_contrib[(int64_t)view * HW + pb];
+      dlb[0] = dl[pb]; dlb[1] = dl[HW + pb]; dlb[2] = dl[2 * HW + pb];
+    }
+  }
+  const int L = (int)__ldg(tile_last + (int64_t)view * tiles_per_view + tile);
+  const int nb = (L + kBatch - 1) / kBatch;
+  if (tid == 0) {
+    for (int st = 0; st < kStages; ++st) {
+      mbar_init(&sm.full[st], 32 * kProd2);
+      mbar_init(&sm.empty[st], 32 * kC2);
+    }
+  }
+  __syncthreads();
+  const int wmax = __reduce_max_sync(0xffffffffu, max(lasta, lastb));
+
+  if (warp >= kC2) {  // ---------------- producers: batches from the back ----------------
+    run_producer<false, kProd2, kStages, kC2>(sm, ids, splats + (int64_t)view * n, rg.x, nb,
+                                        [nb, L](int k, int& rel, int& cnt) {
+                                          rel = (nb - 1 - k) * kBatch;
+                                          cnt = min(L - rel, kBatch);
+                                        },
+                                        ox, oy, moments + (int64_t)view * n * 12, __log2f(rk.alpha_min), inst_mask,
+                                        warp - kC2, lane);
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  const float fx = (float)lx + 0.5f;
+  const u64 fy = pk2((float)lya + 0.5f, (float)lyb + 0.5f);
+  const float lmin = __log2f(rk.alpha_min);
+  const float amax = rk.alpha_max;
+  u64 T2 = pk2(Ta, Tb);
+  u64 B0 = bc2(rk.bg[0]), B1 = bc2(rk.bg[1]), B2 = bc2(rk.bg[2]);
+  const u64 dl0 = pk2(dla[0], dlb[0]), dl1 = pk2(dla[1], dlb[1]), dl2 = pk2(dla[2], dlb[2]);
+  u64 dla01, dlb01;   // a second packing of the same values (own registers: asm volatile is not rematerialised)
+  asm volatile("mov.b64 %0, {%1, %2};" : "=l"(dla01) : "f"(dla[0]), "f"(dla[1]));
+  asm volatile("mov.b64 %0, {%1, %2};" : "=l"(dlb01) : "f"(dlb[0]), "f"(dlb[1]));
+  const float dla2 = dla[2], dlb2 = dlb[2];
+  const uint32_t wbits = (1u << (4 * by + bx)) | (1u << (4 * by + 2 + bx));   // the block's two 8x4 strips
+  float4(*sst)[33] = sc.st[warp];
+  float(*su2)[33] = sc.u2[warp];
+  float2* smean = sc.emean[warp];
+  float** sptr = sc.eptr[warp];
+  constexpr int kG = 32 / kChunk2;              // phase-2 lanes per entry; each sums kChunk2 source lanes
+  const int e2 = lane & (kChunk2 - 1), half = lane / kChunk2;
+  const float cxw = (float)(8 * bx + 4), cyw = (float)(8 * by + 4);   // block centre (tile-relative)
+
+  // ---- phase 2 over the chunk's first `ne` rows ----
+  auto reduce_chunk = [&](int ne) {
+    __syncwarp();
+    // packed accumulators over the source lanes' (w_a, w_b): P1 = sum, P2 = sum x, P3 = sum x^2, P4 / P5 =
+    // sum / sum x over the lanes of the second row (y0' = 1); PU = (u0, u1)
+    u64 P1 = 0ull, P2 = 0ull, P3 = 0ull, P4 = 0ull, P5 = 0ull, PU = 0ull;
+    float U2 = 0.f;
+    const float4* row = sst[e2] + kChunk2 * half;
+    const float* row2 = su2[e2] + kChunk2 * half;
+#pragma unroll
+    for (int i = 0; i < kChunk2; ++i) {   // source lane kChunk2 half + i: x = (i & 7) - 3.5, y0' = i >> 3
+      const float4 q = row[i];
+      const float xq = (float)(i & 7) - 3.5f;
+      const u64 wq = pk2(q.x, q.y);
+      P1 = add2(P1, wq);
+      P2 = fma2(wq, bc2(xq), P2);
+      P3 = fma2(wq, bc2(xq * xq), P3);
+      if (i >= 8) {
+        P4 = add2(P4, wq);
+        P5 = fma2(wq, bc2(xq), P5);
+      }
+      PU = add2(PU, pk2(q.z, q.w));
+      U2 += row2[i];
+    }
+    const float A = lo2(P1) + hi2(P1), Tt = hi2(P1);           // sum s, sum t   (s = w_a + w_b, t = w_b)
+    const float Bx = lo2(P2) + hi2(P2), Tx = hi2(P2);
+    const float D = lo2(P3) + hi2(P3);
+    const float Cy = lo2(P4) + hi2(P4), Ty = hi2(P4);
+    const float E = lo2(P5) + hi2(P5);
+    const float U0 = lo2(PU), U1 = hi2(PU);
+    // group h's source lanes have y0 = y0' + c_h, c_h = (kChunk2 / 8) h - 3.5 (pixel a; pixel b is y0 + 4)
+    const float ch = (float)(kChunk2 / 8) * (float)half - 3.5f;
+    float v[12];
+    v[0] = A;                                      // sum s
+    v[1] = Bx;                                     // sum s x
+    v[2] = fmaf(ch, A, Cy);                        // sum s y0
+    v[3] = D;                                      // sum s x^2
+    v[4] = fmaf(ch, Bx, E);                        // sum s x y0
+    v[5] = fmaf(ch, fmaf(ch, A, 2.0f * Cy), Cy);   // sum s y0^2 (y0'^2 = y0')
+    v[6] = Tt;                                     // sum t
+    v[7] = Tx;                                     // sum t x
+    v[8] = fmaf(ch, Tt, Ty);                       // sum t y0
+    v[9] = U0; v[10] = U1; v[11] = U2;
+#pragma unroll
+    for (int o = kChunk2; o < 32; o <<= 1)
+#pragma unroll
+      for (int q = 0; q < 12; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+    bool nz = false;
+#pragma unroll
+    for (int q = 0; q < 12; ++q) nz |= v[q] != 0.0f;
+    if (e2 < ne && half == 0 && nz) {
+      // raw moments in the block frame: pixel a at (x, y0), b at (x, y0 + 4); w_b = t
+      const float S0 = v[0], Sx = v[1], Sy = fmaf(4.0f, v[6], v[2]);
+      const float Sxx = v[3], Sxy = fmaf(4.0f, v[7], v[4]);
+      const float Syy = fmaf(16.0f, v[6], fmaf(8.0f, v[8], v[5]));
+      const float2 gm = smean[e2];
+      const float u = cxw - gm.x, vv = cyw - gm.y;   // d = (x, y) + (u, v)
+      const float m1x = fmaf(u, S0, Sx), m1y = fmaf(vv, S0, Sy);
+      const float Mxx = fmaf(u, fmaf(u, S0, 2.0f * Sx), Sxx);
+      const float Mxy = fmaf(u, m1y, fmaf(vv, Sx, Sxy));
+      const float Myy = fmaf(vv, fmaf(vv, S0, 2.0f * Sy), Syy);
+      float* mp = sptr[e2];
+      red_v4(mp, S0, m1x, m1y, Mxx);
+      red_v4(mp + 4, Mxy, Myy, v[9], v[10]);
+      atomicAdd(mp + 8, v[11]);
+    }
+    __syncwarp();
+  };
+
+  int fill = 0;   // rows of the current chunk already filled
+  for (int k = 0; k < nb; ++k) {
+    const int s = k % kStages;
+    mbar_wait(&sm.full[s], (k / kStages) & 1, kSuspendNs);
+    const BufferT<kC2>& B = sm.buf[s];
+    uint8_t* lst = sm.buf[s].list[warp];
+    const int nl = build_list(B, lst, wbits, lane, wmax - B.base);
+    const int lima = lasta - B.base, limb = lastb - B.base;
+    for (int t_hi = nl; t_hi > 0;) {
+      const int m = min(t_hi, kChunk2 - fill);
+      const int t_lo = t_hi - m;
+      const int r0 = fill - t_lo;                           // row of list entry t = r0 + t
+      if (lane < m) {
+        const int j = lst[t_lo + lane];
+        smean[fill + lane] = *reinterpret_cast<const float2*>(&B.geo[j]);
+        sptr[fill + lane] = B.mptr[j];
+      }
+      auto recurse = [&](u64 ee, int j, int e) {
+        const float ea = lo2(ee), eb = hi2(ee);
+        const bool ha = j < lima && ea >= lmin, hb = j < limb && eb >= lmin;
+        const float sa = ha ? ex2_approx(ea) : 0.0f, sb = hb ? ex2_approx(eb) : 0.0f;
+        const u64 al = pk2(fminf(amax, sa), fminf(amax, sb));   // 0 for a pixel that does not composite
+        const u64 om = sub2(bc2(1.0f), al);
+        T2 = mul2(T2, pk2(rcp_approx(lo2(om)), rcp_approx(hi2(om))));   // T_i (rcp(1) = 1: unchanged)
+        const float4 c = B.col[j];
+        const u64 d0 = sub2(bc2(c.x), B0), d1 = sub2(bc2(c.y), B1), d2 = sub2(bc2(c.z), B2);
+        const u64 gs = fma2(dl2, d2, fma2(dl1, d1, mul2(dl0, d0)));
+        B0 = fma2(al, d0, B0);                              // B <- alpha c + (1 - alpha) B
+        B1 = fma2(al, d1, B1);
+        B2 = fma2(al, d2, B2);
+        const u64 w = mul2(mul2(T2, gs), pk2(sa, sb));      // dL/dalpha sigma (Z3)
+        const u64 aT = mul2(al, T2);
+        const float aTa = lo2(aT), aTb = hi2(aT);
+        const u64 u01 = fma2(bc2(aTb), dlb01, mul2(bc2(aTa), dla01));   // (u0, u1) packed, no horizontal add
+        sst[e][lane] = make_float4(lo2(w), hi2(w), lo2(u01), hi2(u01));
+        su2[e][lane] = fmaf(aTb, dlb2, __fmul_rn(aTa, dla2));
+      };
+      int t = t_hi - 1;
+      for (; t - 3 >= t_lo; t -= 4) {
+        int jj[4];
+        u64 ee[4];
+#pragma unroll
+        for (int uu = 0; uu < 4; ++uu) {
+          jj[uu] = lst[t - uu];
+          ee[uu] = pair_e2(fx, fy, B.geo[jj[uu]], *reinterpret_cast<const float2*>(&B.par[jj[uu]]));
+        }
+#pragma unroll
+        for (int uu = 0; uu < 4; ++uu) recurse(ee[uu], jj[uu], r0 + t - uu);
+      }
+      for (; t >= t_lo; --t) {
+        const int ja = lst[t];
+        recurse(pair_e2(fx, fy, B.geo[ja], *reinterpret_cast<const float2*>(&B.par[ja])), ja, r0 + t);
+      }
+      fill += m;
+      t_hi = t_lo;
+      if (fill == kChunk2) {
+        reduce_chunk(kChunk2);
+        fill = 0;
+      }
+    }
+    __syncwarp();
+    mbar_arrive(&sm.empty[s]);
+  }
+  if (fill > 0) reduce_chunk(fill);
+}
+
+// ------------------------------------------------------------------------------------------------
+// Forward, two pixels per lane (the layout of k_render_bwd2): four consumer warps of 8x8 blocks, two
+// producer warps, a 5-stage ring.  The blend is C8 per pixel on packed f32x2 halves.
+// ------------------------------------------------------------------------------------------------
+constexpr int kFwdProd2 = 2;
+using SmemFwd2 = SmemT<kFwdStages, kC2>;
+
+template <bool kCount>
+__global__ void __launch_bounds__(32 * (kC2 + kFwdProd2), 4) k_render_fwd2(const steepgs_splat* __restrict__ splats,
+                                                          const uint32_t* __restrict__ ids,
+                                                          const uint2* __restrict__ ranges, int64_t n, int W, int H,
+                                                          int tiles_x, int tiles_per_view, const RasterK rk,
+                                                          float* __restrict__ image, float* __restrict__ final_T,
+                                                          int32_t* __restrict__ n_contrib,
+                                                          uint32_t* __restrict__ tile_last,
+                                                          uint8_t* __restrict__ inst_mask,
+                                                          unsigned long long* __restrict__ pair_counts,
+                                                          const L1Fused l1) {
+  extern __shared__ __align__(16) unsigned char fsmem[];
+  SmemFwd2& sm = *reinterpret_cast<SmemFwd2*>(fsmem);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tile = blockIdx.x, view = blockIdx.y;
+  const int tx = tile % tiles_x, ty = tile / tiles_x;
+  const double ox = (double)(tx * kTile), oy = (double)(ty * kTile);
+  const uint2 rg = ranges[(int64_t)view * tiles_per_view + tile];
+  const int nb = (int)((rg.y - rg.x + kBatch - 1) / kBatch);
+  if (tid == 0) {
+    for (int s = 0; s < kFwdStages; ++s) {
+      mbar_init(&sm.full[s], 32 * kFwdProd2);
+      mbar_init(&sm.empty[s], 32 * kC2);
+    }
+    sm.done_warps = 0;
+  }
+  __syncthreads();
+
+  if (warp >= kC2) {  // ---------------- producers ----------------
+    const int len = (int)(rg.y - rg.x);
+    run_producer<true, kFwdProd2, kFwdStages, kC2>(sm, ids, splats + (int64_t)view * n, rg.x, nb,
+                                                 [len](int k, int& rel, int& cnt) { rel = k * kBatch; cnt = min(len - rel, kBatch); },
+                                                 ox, oy, nullptr, __log2f(rk.alpha_min), inst_mask, warp - kC2, lane);
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  const int bx = warp & 1, by = warp >> 1;
+  const int lx = 8 * bx + (lane & 7), lya = 8 * by + (lane >> 3), lyb = lya + 4;
+  const int px = tx * kTile + lx, pya = ty * kTile + lya, pyb = ty * kTile + lyb;
+  const bool ina = px < W && pya < H, inb = px < W && pyb < H;
+  const float fx = (float)lx + 0.5f;
+  const u64 fy = pk2((float)lya + 0.5f, (float)lyb + 0.5f);   // pixel centres, tile-relative (Z5)
+  const float lmin = __log2f(rk.alpha_min);                  // -inf in smooth mode
+  const float amax = rk.alpha_max, tmin = rk.t_min;
+  const uint32_t wbits = (1u << (4 * by + bx)) | (1u << (4 * by + 2 + bx));
+  u64 T2 = bc2(1.0f), C0 = 0ull, C1 = 0ull, C2 = 0ull;
+  int lasta = 0, lastb = 0, ncomp = 0, neval = 0;
+  bool donea = !ina, doneb = !inb, warp_done = false;
+  for (int k = 0; k < nb; ++k) {
+    const int s = k % kFwdStages;
+    mbar_wait(&sm.full[s], (k / kFwdStages) & 1, kSuspendNs);
+    const BufferT<kC2>& B = sm.buf[s];
+    if (B.stop) break;
+    if (!warp_done) {
+      uint8_t* lst = sm.buf[s].list[warp];
+      const int nl = build_list(B, lst, wbits, lane);
+      const int base1 = B.base + 1;
+      if (kCount) neval += (donea ? 0 : nl) + (doneb ? 0 : nl);
+      // C8 per pixel, branch-free: a pixel that skips (sigma < alpha_min), terminates or is done takes
+      // alpha = 0 in the colour update and keeps its T
+      auto blend = [&](u64 ee, int j) {
+        const float ea = lo2(ee), eb = hi2(ee);
+        const bool livea = !donea && ea >= lmin, liveb = !doneb && eb >= lmin;
+        const u64 al = pk2(fminf(amax, ex2_approx(ea)), fminf(amax, ex2_approx(eb)));
+        const u64 Tn = mul2(T2, sub2(bc2(1.0f), al));
+        const bool terma = livea && lo2(Tn) < tmin, termb = liveb && hi2(Tn) < tmin;   // C8 termination
+        const bool compa = livea && !terma, compb = liveb && !termb;
+        donea = donea || terma;
+        doneb = doneb || termb;
+        const float4 c = B.col[j];
+        const u64 aT = mul2(pk2(compa ? lo2(al) : 0.0f, compb ? hi2(al) : 0.0f), T2);
+        C0 = fma2(aT, bc2(c.x), C0);
+        C1 = fma2(aT, bc2(c.y), C1);
+        C2 = fma2(aT, bc2(c.z), C2);
+        T2 = pk2(compa ? lo2(Tn) : lo2(T2), compb ? hi2(Tn) : hi2(T2));
+        lasta = compa ? base1 + j : lasta;
+        lastb = compb ? base1 + j : lastb;
+        if (kCount) ncomp += (compa ? 1 : 0) + (compb ? 1 : 0);
+      };
+      int t = 0;
+      for (; t + 3 < nl; t += 4) {
+        int jj[4];
+        u64 ee[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          jj[u] = lst[t + u];
+          ee[u] = pair_e2(fx, fy, B.geo[jj[u]], *reinterpret_cast<const float2*>(&B.par[jj[u]]));
+        }
+        if (donea && doneb) continue;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) blend(ee[u], jj[u]);
+      }
+      for (; t < nl && !(donea && doneb); ++t) {
+        const int ja = lst[t];
+        blend(pair_e2(fx, fy, B.geo[ja], *reinterpret_cast<const float2*>(&B.par[ja])), ja);
+      }
+      if (__all_sync(0xffffffffu, donea && doneb)) {
+        warp_done = true;
+        if (lane == 0) atomicAdd(&sm.done_warps, 1);
+      }
+    }
+    mbar_arrive(&sm.empty[s]);
+  }
+  float ad = 0.0f;   // fused l1: the lane's sum of |C - C_hat| over channels and its two pixels
+  const int64_t HW = (int64_t)W * H;
+  const float Tp[2] = {lo2(T2), hi2(T2)};
+  const float Cp[2][3] = {{lo2(C0), lo2(C1), lo2(C2)}, {hi2(C0), hi2(C1), hi2(C2)}};
+  const bool inp[2] = {ina, inb};
+  const int pyp[2] = {pya, pyb}, lastp[2] = {lasta, lastb};
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    if (!inp[q]) continue;
+    const int64_t pix = (int64_t)pyp[q] * W + px;
+    float* img = image + (int64_t)view * 3 * HW;
+    const float out[3] = {__fmaf_rn(Tp[q], rk.bg[0], Cp[q][0]), __fmaf_rn(Tp[q], rk.bg[1], Cp[q][1]),
+                          __fmaf_rn(Tp[q], rk.bg[2], Cp[q][2])};
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) img[ch * HW + pix] = out[ch];
+    final_T[(int64_t)view * HW + pix] = Tp[q];
+    n_contrib[(int64_t)view * HW + pix] = lastp[q];
+    if (l1.target) {   // a4 fused: dL/dC = scale sign(C - C_hat), the same expression as k_l1_grad
+      const int64_t o = (int64_t)view * 3 * HW + pix;
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) {
+        const float r = out[ch] - __ldg(l1.target + o + ch * HW);
+        l1.dL[o + ch * HW] = r > 0.0f ? l1.scale : (r < 0.0f ? -l1.scale : 0.0f);
+        ad += fabsf(r);
+      }
+    }
+  }
+  if (l1.loss) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ad += __shfl_xor_sync(0xffffffffu, ad, o);
+    if (lane == 0) atomicAdd(l1.loss + view, ad * l1.scale);
+  }
+  {
+    const int wl = __reduce_max_sync(0xffffffffu, max(lasta, lastb));   // the tile's composited prefix
+    if (lane == 0 && wl > 0) atomicMax(tile_last + (int64_t)view * tiles_per_view + tile, (uint32_t)wl);
+  }
+  if (kCount) {
+    unsigned long long c = (unsigned long long)ncomp, e = (unsigned long long)neval;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      c += __shfl_xor_sync(0xffffffffu, c, o);
+      e += __shfl_xor_sync(0xffffffffu, e, o);
+    }
+    if (lane == 0) {
+      atomicAdd(&pair_counts[0], c);
+      atomicAdd(&pair_counts[1], e);
+    }
+  }
+}
+
 __global__ void k_l1_grad(const float* __restrict__ image, const float* __restrict__ target, int64_t count,
                           float scale, float* __restrict__ dL, float* __restrict__ loss) {
   const int view = blockIdx.y;
@@ -716,6 +1177,23 @@ cudaError_t launch_render_fwd(const steepgs_splat* splats, int64_t n, const stee
     if (e == cudaSuccess) e = allow_dynamic_smem(done, (const void*)k_render_fwd<false>, sizeof(SmemFwd), true);
     if (e != cudaSuccess) return e;
   }
+  static const int fvariant = [] { const char* e = getenv("STEEPGS_FWD"); return e ? atoi(e) : 2; }();
+  if (fvariant == 2) {
+    static std::atomic<uint64_t> done2{0};
+    cudaError_t e = allow_dynamic_smem(done2, (const void*)k_render_fwd2<true>, sizeof(SmemFwd2));
+    if (e == cudaSuccess) e = allow_dynamic_smem(done2, (const void*)k_render_fwd2<false>, sizeof(SmemFwd2), true);
+    if (e != cudaSuccess) return e;
+    if (pair_counts)
+      k_render_fwd2<true><<<grid, 32 * (kC2 + kFwdProd2), sizeof(SmemFwd2), st>>>(
+          splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H, b.tiles_x, tpv, rk, image, final_T,
+          n_contrib, b.tile_last, b.inst_mask, reinterpret_cast<unsigned long long*>(pair_counts), l1);
+    else
+      k_render_fwd2<false><<<grid, 32 * (kC2 + kFwdProd2), sizeof(SmemFwd2), st>>>(
+          splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H, b.tiles_x, tpv, rk, image, final_T,
+          n_contrib, b.tile_last, b.inst_mask, nullptr, l1);
+    note_launch();
+    return check_launch("k_render_fwd");
+  }
   if (pair_counts)
     k_render_fwd<true><<<grid, kThreadsFwd, sizeof(SmemFwd), st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
                                                   b.tiles_x, tpv, rk, image, final_T, n_contrib, b.tile_last, b.inst_mask,
@@ -754,8 +1232,31 @@ cudaError_t launch_render_bwd(const steepgs_splat* splats, const steepgs_binning
     const cudaError_t e = allow_dynamic_smem(done, (const void*)k_render_bwd, smem, true);
     if (e != cudaSuccess) return e;
   }
-  k_render_bwd<<<grid, kThreads, smem, st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
-                                          b.tiles_x, tpv, rk, final_T, n_contrib, dL_dimage, b.tile_last, b.inst_mask, moments);
+  static const int variant = [] { const char* e = getenv("STEEPGS_BWD"); return e ? atoi(e) : 2; }();
+  auto run2 = [&](auto kern, size_t scratch, int prod, std::atomic<uint64_t>& done2) -> cudaError_t {
+    const size_t smem2 = ((sizeof(Smem2) + 15) & ~size_t(15)) + scratch;
+    const cudaError_t e = allow_dynamic_smem(done2, (const void*)kern, smem2, true);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, 32 * (kC2 + prod), smem2, st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
+                                                b.tiles_x, tpv, rk, final_T, n_contrib, dL_dimage, b.tile_last,
+                                                b.inst_mask, moments);
+    return cudaSuccess;
+  };
+  static std::atomic<uint64_t> d2{0}, d3{0}, d4{0}, d5{0};
+  cudaError_t e2 = cudaSuccess;
+  if (variant == 2) {
+    e2 = run2(k_render_bwd2<16, 1, 3>, sizeof(BwdScratch2<16>), 1, d2);
+  } else if (variant == 3) {
+    e2 = run2(k_render_bwd2<8, 1, 4>, sizeof(BwdScratch2<8>), 1, d3);
+  } else if (variant == 4) {
+    e2 = run2(k_render_bwd2<16, 2, 3>, sizeof(BwdScratch2<16>), 2, d4);
+  } else if (variant == 5) {
+    e2 = run2(k_render_bwd2<8, 2, 4>, sizeof(BwdScratch2<8>), 2, d5);
+  } else {
+    k_render_bwd<<<grid, kThreads, smem, st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
+                                            b.tiles_x, tpv, rk, final_T, n_contrib, dL_dimage, b.tile_last, b.inst_mask, moments);
+  }
+  if (e2 != cudaSuccess) return e2;
   note_launch();
   return check_launch("k_render_bwd");
 }

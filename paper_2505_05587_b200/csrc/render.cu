@@ -958,167 +958,6 @@ __global__ void __launch_bounds__(32 * (kC2 + kProd2), kMinBlocks) k_render_bwd2
   if (fill > 0) reduce_chunk(fill);
 }
 
-// ------------------------------------------------------------------------------------------------
-// Forward, two pixels per lane (the layout of k_render_bwd2): four consumer warps of 8x8 blocks, two
-// producer warps, a 5-stage ring.  The blend is C8 per pixel on packed f32x2 halves.
-// ------------------------------------------------------------------------------------------------
-constexpr int kFwdProd2 = 2;
-using SmemFwd2 = SmemT<kFwdStages, kC2>;
-
-template <bool kCount>
-__global__ void __launch_bounds__(32 * (kC2 + kFwdProd2), 4) k_render_fwd2(const steepgs_splat* __restrict__ splats,
-                                                          const uint32_t* __restrict__ ids,
-                                                          const uint2* __restrict__ ranges, int64_t n, int W, int H,
-                                                          int tiles_x, int tiles_per_view, const RasterK rk,
-                                                          float* __restrict__ image, float* __restrict__ final_T,
-                                                          int32_t* __restrict__ n_contrib,
-                                                          uint32_t* __restrict__ tile_last,
-                                                          uint8_t* __restrict__ inst_mask,
-                                                          unsigned long long* __restrict__ pair_counts,
-                                                          const L1Fused l1) {
-  extern __shared__ __align__(16) unsigned char fsmem[];
-  SmemFwd2& sm = *reinterpret_cast<SmemFwd2*>(fsmem);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int tile = blockIdx.x, view = blockIdx.y;
-  const int tx = tile % tiles_x, ty = tile / tiles_x;
-  const double ox = (double)(tx * kTile), oy = (double)(ty * kTile);
-  const uint2 rg = ranges[(int64_t)view * tiles_per_view + tile];
-  const int nb = (int)((rg.y - rg.x + kBatch - 1) / kBatch);
-  if (tid == 0) {
-    for (int s = 0; s < kFwdStages; ++s) {
-      mbar_init(&sm.full[s], 32 * kFwdProd2);
-      mbar_init(&sm.empty[s], 32 * kC2);
-    }
-    sm.done_warps = 0;
-  }
-  __syncthreads();
-
-  if (warp >= kC2) {  // ---------------- producers ----------------
-    const int len = (int)(rg.y - rg.x);
-    run_producer<true, kFwdProd2, kFwdStages, kC2>(sm, ids, splats + (int64_t)view * n, rg.x, nb,
-                                                 [len](int k, int& rel, int& cnt) { rel = k * kBatch; cnt = min(len - rel, kBatch); },
-                                                 ox, oy, nullptr, __log2f(rk.alpha_min), inst_mask, warp - kC2, lane);
-    return;
-  }
-
-  // ---------------- consumers ----------------
-  const int bx = warp & 1, by = warp >> 1;
-  const int lx = 8 * bx + (lane & 7), lya = 8 * by + (lane >> 3), lyb = lya + 4;
-  const int px = tx * kTile + lx, pya = ty * kTile + lya, pyb = ty * kTile + lyb;
-  const bool ina = px < W && pya < H, inb = px < W && pyb < H;
-  const float fx = (float)lx + 0.5f;
-  const u64 fy = pk2((float)lya + 0.5f, (float)lyb + 0.5f);   // pixel centres, tile-relative (Z5)
-  const float lmin = __log2f(rk.alpha_min);                  // -inf in smooth mode
-  const float amax = rk.alpha_max, tmin = rk.t_min;
-  const uint32_t wbits = (1u << (4 * by + bx)) | (1u << (4 * by + 2 + bx));
-  u64 T2 = bc2(1.0f), C0 = 0ull, C1 = 0ull, C2 = 0ull;
-  int lasta = 0, lastb = 0, ncomp = 0, neval = 0;
-  bool donea = !ina, doneb = !inb, warp_done = false;
-  for (int k = 0; k < nb; ++k) {
-    const int s = k % kFwdStages;
-    mbar_wait(&sm.full[s], (k / kFwdStages) & 1, kSuspendNs);
-    const BufferT<kC2>& B = sm.buf[s];
-    if (B.stop) break;
-    if (!warp_done) {
-      uint8_t* lst = sm.buf[s].list[warp];
-      const int nl = build_list(B, lst, wbits, lane);
-      const int base1 = B.base + 1;
-      if (kCount) neval += (donea ? 0 : nl) + (doneb ? 0 : nl);
-      // C8 per pixel, branch-free: a pixel that skips (sigma < alpha_min), terminates or is done takes
-      // alpha = 0 in the colour update and keeps its T
-      auto blend = [&](u64 ee, int j) {
-        const float ea = lo2(ee), eb = hi2(ee);
-        const bool livea = !donea && ea >= lmin, liveb = !doneb && eb >= lmin;
-        const u64 al = pk2(fminf(amax, ex2_approx(ea)), fminf(amax, ex2_approx(eb)));
-        const u64 Tn = mul2(T2, sub2(bc2(1.0f), al));
-        const bool terma = livea && lo2(Tn) < tmin, termb = liveb && hi2(Tn) < tmin;   // C8 termination
-        const bool compa = livea && !terma, compb = liveb && !termb;
-        donea = donea || terma;
-        doneb = doneb || termb;
-        const float4 c = B.col[j];
-        const u64 aT = mul2(pk2(compa ? lo2(al) : 0.0f, compb ? hi2(al) : 0.0f), T2);
-        C0 = fma2(aT, bc2(c.x), C0);
-        C1 = fma2(aT, bc2(c.y), C1);
-        C2 = fma2(aT, bc2(c.z), C2);
-        T2 = pk2(compa ? lo2(Tn) : lo2(T2), compb ? hi2(Tn) : hi2(T2));
-        lasta = compa ? base1 + j : lasta;
-        lastb = compb ? base1 + j : lastb;
-        if (kCount) ncomp += (compa ? 1 : 0) + (compb ? 1 : 0);
-      };
-      int t = 0;
-      for (; t + 3 < nl; t += 4) {
-        int jj[4];
-        u64 ee[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          jj[u] = lst[t + u];
-          ee[u] = pair_e2(fx, fy, B.geo[jj[u]], *reinterpret_cast<const float2*>(&B.par[jj[u]]));
-        }
-        if (donea && doneb) continue;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) blend(ee[u], jj[u]);
-      }
-      for (; t < nl && !(donea && doneb); ++t) {
-        const int ja = lst[t];
-        blend(pair_e2(fx, fy, B.geo[ja], *reinterpret_cast<const float2*>(&B.par[ja])), ja);
-      }
-      if (__all_sync(0xffffffffu, donea && doneb)) {
-        warp_done = true;
-        if (lane == 0) atomicAdd(&sm.done_warps, 1);
-      }
-    }
-    mbar_arrive(&sm.empty[s]);
-  }
-  float ad = 0.0f;   // fused l1: the lane's sum of |C - C_hat| over channels and its two pixels
-  const int64_t HW = (int64_t)W * H;
-  const float Tp[2] = {lo2(T2), hi2(T2)};
-  const float Cp[2][3] = {{lo2(C0), lo2(C1), lo2(C2)}, {hi2(C0), hi2(C1), hi2(C2)}};
-  const bool inp[2] = {ina, inb};
-  const int pyp[2] = {pya, pyb}, lastp[2] = {lasta, lastb};
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    if (!inp[q]) continue;
-    const int64_t pix = (int64_t)pyp[q] * W + px;
-    float* img = image + (int64_t)view * 3 * HW;
-    const float out[3] = {__fmaf_rn(Tp[q], rk.bg[0], Cp[q][0]), __fmaf_rn(Tp[q], rk.bg[1], Cp[q][1]),
-                          __fmaf_rn(Tp[q], rk.bg[2], Cp[q][2])};
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) img[ch * HW + pix] = out[ch];
-    final_T[(int64_t)view * HW + pix] = Tp[q];
-    n_contrib[(int64_t)view * HW + pix] = lastp[q];
-    if (l1.target) {   // a4 fused: dL/dC = scale sign(C - C_hat), the same expression as k_l1_grad
-      const int64_t o = (int64_t)view * 3 * HW + pix;
-#pragma unroll
-      for (int ch = 0; ch < 3; ++ch) {
-        const float r = out[ch] - __ldg(l1.target + o + ch * HW);
-        l1.dL[o + ch * HW] = r > 0.0f ? l1.scale : (r < 0.0f ? -l1.scale : 0.0f);
-        ad += fabsf(r);
-      }
-    }
-  }
-  if (l1.loss) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) ad += __shfl_xor_sync(0xffffffffu, ad, o);
-    if (lane == 0) atomicAdd(l1.loss + view, ad * l1.scale);
-  }
-  {
-    const int wl = __reduce_max_sync(0xffffffffu, max(lasta, lastb));   // the tile's composited prefix
-    if (lane == 0 && wl > 0) atomicMax(tile_last + (int64_t)view * tiles_per_view + tile, (uint32_t)wl);
-  }
-  if (kCount) {
-    unsigned long long c = (unsigned long long)ncomp, e = (unsigned long long)neval;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      c += __shfl_xor_sync(0xffffffffu, c, o);
-      e += __shfl_xor_sync(0xffffffffu, e, o);
-    }
-    if (lane == 0) {
-      atomicAdd(&pair_counts[0], c);
-      atomicAdd(&pair_counts[1], e);
-    }
-  }
-}
-
 __global__ void k_l1_grad(const float* __restrict__ image, const float* __restrict__ target, int64_t count,
                           float scale, float* __restrict__ dL, float* __restrict__ loss) {
   const int view = blockIdx.y;
@@ -1176,23 +1015,6 @@ cudaError_t launch_render_fwd(const steepgs_splat* splats, int64_t n, const stee
     cudaError_t e = allow_dynamic_smem(done, (const void*)k_render_fwd<true>, sizeof(SmemFwd));
     if (e == cudaSuccess) e = allow_dynamic_smem(done, (const void*)k_render_fwd<false>, sizeof(SmemFwd), true);
     if (e != cudaSuccess) return e;
-  }
-  static const int fvariant = [] { const char* e = getenv("STEEPGS_FWD"); return e ? atoi(e) : 2; }();
-  if (fvariant == 2) {
-    static std::atomic<uint64_t> done2{0};
-    cudaError_t e = allow_dynamic_smem(done2, (const void*)k_render_fwd2<true>, sizeof(SmemFwd2));
-    if (e == cudaSuccess) e = allow_dynamic_smem(done2, (const void*)k_render_fwd2<false>, sizeof(SmemFwd2), true);
-    if (e != cudaSuccess) return e;
-    if (pair_counts)
-      k_render_fwd2<true><<<grid, 32 * (kC2 + kFwdProd2), sizeof(SmemFwd2), st>>>(
-          splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H, b.tiles_x, tpv, rk, image, final_T,
-          n_contrib, b.tile_last, b.inst_mask, reinterpret_cast<unsigned long long*>(pair_counts), l1);
-    else
-      k_render_fwd2<false><<<grid, 32 * (kC2 + kFwdProd2), sizeof(SmemFwd2), st>>>(
-          splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H, b.tiles_x, tpv, rk, image, final_T,
-          n_contrib, b.tile_last, b.inst_mask, nullptr, l1);
-    note_launch();
-    return check_launch("k_render_fwd");
   }
   if (pair_counts)
     k_render_fwd<true><<<grid, kThreadsFwd, sizeof(SmemFwd), st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,

@@ -59,6 +59,10 @@ static steepgs_status check_views(const steepgs_camera* cams, int32_t V, CamPack
       volatile float lx = cams[v].guard * qx, ly = cams[v].guard * qy;
       pack->lim[v][0] = lx;
       pack->lim[v][1] = ly;
+      for (int k = 0; k < 9; ++k) pack->dc[v][k] = (double)cams[v].R[k];
+      for (int k = 0; k < 3; ++k) pack->dc[v][9 + k] = (double)cams[v].t[k];
+      pack->dc[v][12] = cams[v].fx; pack->dc[v][13] = cams[v].fy;
+      pack->dc[v][14] = cams[v].cx; pack->dc[v][15] = cams[v].cy;
     }
   }
   return STEEPGS_OK;

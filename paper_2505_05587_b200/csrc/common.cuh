@@ -14,6 +14,8 @@ struct CamPack {                   // by-value kernel parameter (<= 64 * 92 B)
   steepgs_camera cam[kMaxViews];
   float lim[kMaxViews][2];          // guard * (W/2) / fx, guard * (H/2) / fy: the decision chain's
                                     // per-camera cull limits (§3.2), IEEE fp32 on the host
+  double dc[kMaxViews][16];         // the camera in fp64 (R row-major, t, fx, fy, cx, cy), widened once on
+                                    // the host so the fp64 render values need no per-thread conversions
 };
 
 struct RasterK {

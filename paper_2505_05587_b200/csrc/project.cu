@@ -99,6 +99,7 @@ __global__ void __launch_bounds__(256, kSH < 0 ? 4 : 1) k_project(const float* _
     dr[6] = 2.0 * (X * Z - W_ * Y) * ds0; dr[7] = 2.0 * (Y * Z + W_ * X) * ds1; dr[8] = (1.0 - 2.0 * (X * X + Y * Y)) * ds2;
   }
 
+  const double dp0 = p0, dp1 = p1, dp2 = p2;
   // SH rest coefficients: read once, used by every view (kSH >= 1)
   constexpr int kRest = kSH >= 1 ? 3 * ((kSH + 1) * (kSH + 1) - 1) : 1;
   float shc[kRest];
@@ -169,30 +170,31 @@ __global__ void __launch_bounds__(256, kSH < 0 ? 4 : 1) k_project(const float* _
     // ---- render values in fp64, rounded once.  fp32 rounding of P alone would perturb thin,
     // large footprints by ~1e-7 lambda_max / lambda_min, so Sigma2D = M M^T + dil I with
     // M = P R diag(s) and det = |m0 x m1|^2 + dil (|m0|^2 + |m1|^2) + dil^2 (no cancellation).
-    const double dtx = fma((double)R[0], p0, fma((double)R[1], p1, fma((double)R[2], p2, (double)c.t[0])));
-    const double dty = fma((double)R[3], p0, fma((double)R[4], p1, fma((double)R[5], p2, (double)c.t[1])));
-    const double dtz = fma((double)R[6], p0, fma((double)R[7], p1, fma((double)R[8], p2, (double)c.t[2])));
+    const double* Dc = cams.dc[v];   // R (0-8), t (9-11), fx, fy, cx, cy in fp64
+    const double dtx = fma(Dc[0], dp0, fma(Dc[1], dp1, fma(Dc[2], dp2, Dc[9])));
+    const double dty = fma(Dc[3], dp0, fma(Dc[4], dp1, fma(Dc[5], dp2, Dc[10])));
+    const double dtz = fma(Dc[6], dp0, fma(Dc[7], dp1, fma(Dc[8], dp2, Dc[11])));
     double mx, my, j00, j02, j11, j12;
     if (c.model == 0) {
       const double iz = drcp(dtz);
       const double xz = dtx * iz, yz = dty * iz;
-      mx = fma((double)c.fx, xz, (double)c.cx);
-      my = fma((double)c.fy, yz, (double)c.cy);
-      j00 = (double)c.fx * iz; j02 = -(double)c.fx * xz * iz;
-      j11 = (double)c.fy * iz; j12 = -(double)c.fy * yz * iz;
+      mx = fma(Dc[12], xz, Dc[14]);
+      my = fma(Dc[13], yz, Dc[15]);
+      j00 = Dc[12] * iz; j02 = -Dc[12] * xz * iz;
+      j11 = Dc[13] * iz; j12 = -Dc[13] * yz * iz;
     } else {
-      mx = fma((double)c.fx, dtx, (double)c.cx);
-      my = fma((double)c.fy, dty, (double)c.cy);
-      j00 = c.fx; j02 = 0.0; j11 = c.fy; j12 = 0.0;
+      mx = fma(Dc[12], dtx, Dc[14]);
+      my = fma(Dc[13], dty, Dc[15]);
+      j00 = Dc[12]; j02 = 0.0; j11 = Dc[13]; j12 = 0.0;
     }
     double m0[3], m1[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       // column k of R(q) diag(s) taken to camera space, then through J
       const double wx = dr[k], wy = dr[3 + k], wz = dr[6 + k];
-      const double cx_ = fma((double)R[0], wx, fma((double)R[1], wy, (double)R[2] * wz));
-      const double cy_ = fma((double)R[3], wx, fma((double)R[4], wy, (double)R[5] * wz));
-      const double cz_ = fma((double)R[6], wx, fma((double)R[7], wy, (double)R[8] * wz));
+      const double cx_ = fma(Dc[0], wx, fma(Dc[1], wy, Dc[2] * wz));
+      const double cy_ = fma(Dc[3], wx, fma(Dc[4], wy, Dc[5] * wz));
+      const double cz_ = fma(Dc[6], wx, fma(Dc[7], wy, Dc[8] * wz));
       m0[k] = fma(j00, cx_, j02 * cz_);
       m1[k] = fma(j11, cy_, j12 * cz_);
     }

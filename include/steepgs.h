@@ -10,7 +10,7 @@
  * Conventions for every call
  *  - Pointers are CUDA DEVICE pointers owned by the caller unless tagged [host].  The library never
  *    allocates, frees or reallocates device memory and keeps no global state except a
- *    thread-local error string and a launch counter.
+ *    thread-local error string, a launch counter and the binning generation counter.
  *  - `stream` is a cudaStream_t passed as void*.  Calls are asynchronous on `stream` and never
  *    synchronise it, except steepgs_densify_host_count (documented below).  Nothing is
  *    read back to the host, so every call can be captured in a CUDA graph.
@@ -45,6 +45,8 @@ typedef enum {
                                           tile != 16, denom <= 0, gate not 0/1/2 */
   STEEPGS_ERR_WORKSPACE_TOO_SMALL = 2, /* ws_bytes < steepgs_bin_sort_workspace_size(...) */
   STEEPGS_ERR_CAPACITY = 3,            /* densify: n + n_split > capacity (host-count variant) */
+  STEEPGS_ERR_STALE_STATE = 4,         /* render_bwd: the binning was not rendered forward with these
+                                          splats / cameras / raster params since its bin_sort (§8(b)) */
   STEEPGS_ERR_UNSUPPORTED_DEVICE = 5,  /* no CUDA device of compute capability 10.x */
   STEEPGS_ERR_CUDA = 6                 /* launch / runtime error, see steepgs_last_error() */
 } steepgs_status;
@@ -119,6 +121,11 @@ typedef struct {
                                    support reaches; render_bwd reads it instead of recomputing */
   int64_t max_instances;
   int32_t tiles_x, tiles_y, V;
+  uint64_t generation;          /* set by bin_sort: a process-wide counter, distinct per bin_sort call */
+  uint64_t fwd_token;           /* set by render_fwd(_l1): a hash of (generation, splats, n, cameras,
+                                   raster params) of the forward that filled tile_last / inst_mask;
+                                   render_bwd recomputes it from its own arguments and returns
+                                   STEEPGS_ERR_STALE_STATE on a mismatch (0: no forward yet) */
 } steepgs_binning;
 
 /* ---- a1: projection (Eq. eqn:sigma_2D + footnote P:L135-139).  Per (view, Gaussian):
@@ -159,7 +166,7 @@ steepgs_status steepgs_bin_sort(const uint32_t* depth_key, const uint32_t* tile_
  * up to the last composited Gaussian (consumed by the backward).
  * pair_counts: NULL, or a device int64[2] that receives += (composited pairs, evaluated pairs)
  * (the units of the roofline model). */
-steepgs_status steepgs_render_fwd(const steepgs_splat* splats, int64_t n, const steepgs_binning* b,
+steepgs_status steepgs_render_fwd(const steepgs_splat* splats, int64_t n, steepgs_binning* b /*[host], fwd_token set*/,
                                   const steepgs_camera* cams, int32_t V, const steepgs_raster_params* rp,
                                   float* image, float* final_T, int32_t* n_contrib, int64_t* pair_counts,
                                   void* stream);
@@ -168,7 +175,7 @@ steepgs_status steepgs_render_fwd(const steepgs_splat* splats, int64_t n, const 
  * (dL_dimage = scale * sign(image - target), loss[v] = scale * sum |image - target| if loss != NULL,
  * the same expressions), so the image is not read back by a separate pass.  target / dL_dimage
  * [V][3][H][W]. */
-steepgs_status steepgs_render_fwd_l1(const steepgs_splat* splats, int64_t n, const steepgs_binning* b,
+steepgs_status steepgs_render_fwd_l1(const steepgs_splat* splats, int64_t n, steepgs_binning* b /*[host]*/,
                                      const steepgs_camera* cams, int32_t V, const steepgs_raster_params* rp,
                                      float* image, float* final_T, int32_t* n_contrib, const float* target,
                                      float scale, float* dL_dimage, float* loss, int64_t* pair_counts, void* stream);
@@ -204,7 +211,9 @@ steepgs_status steepgs_l1_ssim_grad(const float* image, const float* target, int
  * tiles_touched ([V][n], from steepgs_project) is read only then.
  * Precondition: splats, b, cams and rp are those of the steepgs_render_fwd call that produced
  * final_T and n_contrib (the replay also reads b->tile_last and b->inst_mask, which that forward
- * wrote); otherwise the result is unspecified. */
+ * wrote).  Checked on the host through b->fwd_token: a binning re-sorted since, or a forward run
+ * with other splats / n / cameras / raster params, returns STEEPGS_ERR_STALE_STATE (nothing is
+ * launched).  (final_T / n_contrib / dL_dimage are not covered: the caller owns those buffers.) */
 steepgs_status steepgs_render_bwd_split(const float* params, int64_t ld, int64_t n,
                                         const steepgs_splat* splats, const steepgs_binning* b,
                                         const steepgs_camera* cams, int32_t V,

@@ -52,7 +52,8 @@ class Binning(C.Structure):
                 ("n_visible", C.c_void_p), ("overflow", C.c_void_p), ("tile_last", C.c_void_p),
                 ("inst_mask", C.c_void_p),
                 ("max_instances", C.c_int64),
-                ("tiles_x", C.c_int32), ("tiles_y", C.c_int32), ("V", C.c_int32)]
+                ("tiles_x", C.c_int32), ("tiles_y", C.c_int32), ("V", C.c_int32),
+                ("generation", C.c_uint64), ("fwd_token", C.c_uint64)]
 
 
 SPLAT_BYTES = 64

@@ -5,7 +5,17 @@
 #include <cstring>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
+
+// One NVTX range per C-ABI compute call: visible in nsys / ncu --nvtx; a no-op
+// (one predictable branch) when no tool is attached.
+struct SgsNvtxRange {
+  explicit SgsNvtxRange(const char* s) { nvtxRangePushA(s); }
+  ~SgsNvtxRange() { nvtxRangePop(); }
+};
+#define SGS_NVTX(name) SgsNvtxRange sgs_nvtx_range_(name)
 
 namespace sgs {
 
@@ -79,6 +89,35 @@ static steepgs_status check_raster(const steepgs_raster_params* rp) {
 
 static bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
+// Binning generations and forward tokens (STEEPGS_ERR_STALE_STATE): bin_sort stamps a fresh
+// generation; the forward stores a hash of (generation, splats, n, cameras, raster params); the
+// backward recomputes it from its own arguments.
+static std::atomic<uint64_t> g_generation{0};
+static uint64_t fnv1a(uint64_t h, const void* p, size_t bytes) {
+  const unsigned char* c = static_cast<const unsigned char*>(p);
+  for (size_t k = 0; k < bytes; ++k) h = (h ^ c[k]) * 1099511628211ull;
+  return h;
+}
+static uint64_t fwd_token(const steepgs_binning* b, const steepgs_splat* splats, int64_t n, const steepgs_camera* cams,
+                          int32_t V, const steepgs_raster_params* rp) {
+  uint64_t h = 14695981039346656037ull;
+  h = fnv1a(h, &b->generation, sizeof(b->generation));
+  h = fnv1a(h, &splats, sizeof(splats));
+  h = fnv1a(h, &n, sizeof(n));
+  h = fnv1a(h, &V, sizeof(V));
+  h = fnv1a(h, cams, sizeof(steepgs_camera) * (size_t)V);
+  h = fnv1a(h, rp, sizeof(*rp));
+  return h ? h : 1ull;   // 0 means "no forward"
+}
+static steepgs_status check_token(const steepgs_binning* b, const steepgs_splat* splats, int64_t n,
+                                  const steepgs_camera* cams, int32_t V, const steepgs_raster_params* rp) {
+  if (b->fwd_token == 0) return fail(STEEPGS_ERR_STALE_STATE, "render_bwd: no render_fwd on this binning");
+  if (b->fwd_token != fwd_token(b, splats, n, cams, V, rp))
+    return fail(STEEPGS_ERR_STALE_STATE,
+                "render_bwd: the binning was re-sorted, or its forward used other splats / n / cameras / raster params");
+  return STEEPGS_OK;
+}
+
 static steepgs_status check_binning(const steepgs_binning* b, int32_t V, const steepgs_camera* cams) {
   if (!b || !b->ids || !b->ranges || !b->n_instances || !b->tile_last || !b->inst_mask)
     return fail(STEEPGS_ERR_INVALID_ARGUMENT, "binning null");
@@ -113,6 +152,7 @@ const char* steepgs_version(void) { return "steepgs-b200 0.1 (sm_100a)"; }
 steepgs_status steepgs_project(const float* params, int64_t ld, int64_t n, const steepgs_camera* cams, int32_t V,
                                const steepgs_raster_params* rp, steepgs_splat* splats, uint32_t* depth_key,
                                uint32_t* tile_rect, int32_t* tiles_touched, void* stream) {
+  SGS_NVTX("steepgs_project");
   steepgs_status s;
   if ((s = device_ok()) != STEEPGS_OK) return s;
   CamPack pack;
@@ -132,6 +172,7 @@ steepgs_status steepgs_project_sh(const float* params, int64_t ld, int64_t n, co
                                   int32_t sh_degree, const steepgs_camera* cams, int32_t V,
                                   const steepgs_raster_params* rp, steepgs_splat* splats, uint32_t* depth_key,
                                   uint32_t* tile_rect, int32_t* tiles_touched, void* stream) {
+  SGS_NVTX("steepgs_project_sh");
   steepgs_status s;
   if ((s = device_ok()) != STEEPGS_OK) return s;
   CamPack pack;
@@ -153,6 +194,7 @@ steepgs_status steepgs_sh_bwd(const float* params, int64_t ld, int64_t n, const 
                               int32_t sh_degree, const steepgs_camera* cams, int32_t V, const float* moments_ws,
                               float* grad_S, int64_t ldg, float* grad_sh, int64_t ldg_sh, int32_t accumulate,
                               void* stream) {
+  SGS_NVTX("steepgs_sh_bwd");
   steepgs_status s;
   if ((s = device_ok()) != STEEPGS_OK) return s;
   CamPack pack;
@@ -172,6 +214,7 @@ steepgs_status steepgs_sh_bwd(const float* params, int64_t ld, int64_t n, const 
 steepgs_status steepgs_adam_step_planes(float* params, int64_t ld, int32_t planes, int64_t n, const float* grad,
                                         int64_t ldg, float* adam_m, float* adam_v, int64_t ldm,
                                         const steepgs_adam_params* ap, int64_t step, void* stream) {
+  SGS_NVTX("steepgs_adam_step_planes");
   steepgs_status s;
   if ((s = device_ok()) != STEEPGS_OK) return s;
   if (!ap || step < 1 || n < 0 || planes < 0 || ld < n || ldg < n || ldm < n || !(ap->beta1 >= 0.0 && ap->beta1 < 1.0) ||
@@ -194,6 +237,7 @@ steepgs_status steepgs_loss_workspace_size(int32_t V, int32_t height, int32_t wi
 steepgs_status steepgs_l1_ssim_grad(const float* image, const float* target, int32_t V, int32_t height, int32_t width,
                                     float lambda_ssim, float scale, float* dL_dimage, float* loss, void* workspace,
                                     size_t ws_bytes, void* stream) {
+  SGS_NVTX("steepgs_l1_ssim_grad");
   steepgs_status s;
   if ((s = device_ok()) != STEEPGS_OK) return s;
   if (V < 1 || V > kMaxViews || height <= 0 || width <= 0 || !(lambda_ssim >= 0.f && lambda_ssim <= 1.f))
@@ -213,6 +257,7 @@ steepgs_status steepgs_prune_workspace_size(int64_t n, size_t* bytes) {
 
 steepgs_status steepgs_prune_decide(const float* params, int64_t ld, int64_t n, float logit_min, int32_t* new_index,
                                     int64_t* n_keep, void* workspace, size_t ws_bytes, void* stream) {
+  SGS_NVTX("steepgs_prune_decide");
   steepgs_status s;
   if ((s = device_ok()) != STEEPGS_OK) return s;
   if (n < 0 || ld < n || n >= (1ll << 31) || !n_keep || !workspace || (n > 0 && (!params || !new_index)))
@@ -225,6 +270,7 @@ steepgs_status steepgs_prune_decide(const float* params, int64_t ld, int64_t n, 
 
 steepgs_status steepgs_compact_planes(const float* src, int64_t ld_src, float* dst, int64_t ld_dst, int32_t planes,
                                       int64_t n, const int32_t* new_index, void* stream) {
+  SGS_NVTX("steepgs_compact_planes");
   steepgs_status s;
   if ((s = device_ok()) != STEEPGS_OK) return s;
   if (n < 0 || planes < 0 || ld_src < n || ld_dst < n || (n > 0 && planes > 0 && (!src || !dst || !new_index)) ||
@@ -236,6 +282,7 @@ steepgs_status steepgs_compact_planes(const float* src, int64_t ld_src, float* d
 
 steepgs_status steepgs_copy_offspring(float* arr, int64_t ld, int32_t planes, int64_t n, const int32_t* dest_index,
                                       void* stream) {
+  SGS_NVTX("steepgs_copy_offspring");
   steepgs_status s;
   if ((s = device_ok()) != STEEPGS_OK) return s;
   if (n < 0 || planes < 0 || ld < n || (n > 0 && planes > 0 && (!arr || !dest_index)))
@@ -258,6 +305,7 @@ steepgs_status steepgs_bin_sort(const uint32_t* depth_key, const uint32_t* tile_
                                 int64_t n, const steepgs_camera* cams, int32_t V, const steepgs_raster_params* rp,
                                 void* workspace, size_t ws_bytes, int64_t max_instances, steepgs_binning* out,
                                 void* stream) {
+  SGS_NVTX("steepgs_bin_sort");
   steepgs_status s;
   if ((s = device_ok()) != STEEPGS_OK) return s;
   if ((s = check_views(cams, V, nullptr)) != STEEPGS_OK) return s;
@@ -272,12 +320,15 @@ steepgs_status steepgs_bin_sort(const uint32_t* depth_key, const uint32_t* tile_
   if (ws_bytes < need) return fail(STEEPGS_ERR_WORKSPACE_TOO_SMALL, "bin_sort workspace too small");
   const cudaError_t e = launch_bin_sort(depth_key, tile_rect, tiles_touched, n, V, tx, ty, workspace, ws_bytes,
                                         max_instances, out, (cudaStream_t)stream);
+  out->generation = g_generation.fetch_add(1, std::memory_order_relaxed) + 1;
+  out->fwd_token = 0;
   return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_bin_sort");
 }
 
-steepgs_status steepgs_render_fwd(const steepgs_splat* splats, int64_t n, const steepgs_binning* b,
+steepgs_status steepgs_render_fwd(const steepgs_splat* splats, int64_t n, steepgs_binning* b,
                                   const steepgs_camera* cams, int32_t V, const steepgs_raster_params* rp, float* image,
                                   float* final_T, int32_t* n_contrib, int64_t* pair_counts, void* stream) {
+  SGS_NVTX("steepgs_render_fwd");
   steepgs_status s;
   if ((s = device_ok()) != STEEPGS_OK) return s;
   if ((s = check_views(cams, V, nullptr)) != STEEPGS_OK) return s;
@@ -287,13 +338,16 @@ steepgs_status steepgs_render_fwd(const steepgs_splat* splats, int64_t n, const 
     return fail(STEEPGS_ERR_INVALID_ARGUMENT, "null pointer");
   const cudaError_t e = launch_render_fwd(splats, n, *b, cams[0].width, cams[0].height, raster_k(rp), image, final_T,
                                           n_contrib, pair_counts, (cudaStream_t)stream);
-  return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_render_fwd");
+  if (e != cudaSuccess) return cuda_fail(e, "steepgs_render_fwd");
+  b->fwd_token = fwd_token(b, splats, n, cams, V, rp);
+  return STEEPGS_OK;
 }
 
-steepgs_status steepgs_render_fwd_l1(const steepgs_splat* splats, int64_t n, const steepgs_binning* b,
+steepgs_status steepgs_render_fwd_l1(const steepgs_splat* splats, int64_t n, steepgs_binning* b,
                                      const steepgs_camera* cams, int32_t V, const steepgs_raster_params* rp,
                                      float* image, float* final_T, int32_t* n_contrib, const float* target,
                                      float scale, float* dL_dimage, float* loss, int64_t* pair_counts, void* stream) {
+  SGS_NVTX("steepgs_render_fwd_l1");
   steepgs_status s;
   if ((s = device_ok()) != STEEPGS_OK) return s;
   if ((s = check_views(cams, V, nullptr)) != STEEPGS_OK) return s;
@@ -304,11 +358,14 @@ steepgs_status steepgs_render_fwd_l1(const steepgs_splat* splats, int64_t n, con
   const L1Fused l1{target, dL_dimage, loss, scale};
   const cudaError_t e = launch_render_fwd(splats, n, *b, cams[0].width, cams[0].height, raster_k(rp), image, final_T,
                                           n_contrib, pair_counts, (cudaStream_t)stream, l1);
-  return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_render_fwd_l1");
+  if (e != cudaSuccess) return cuda_fail(e, "steepgs_render_fwd_l1");
+  b->fwd_token = fwd_token(b, splats, n, cams, V, rp);
+  return STEEPGS_OK;
 }
 
 steepgs_status steepgs_l1_grad(const float* image, const float* target, int32_t V, int64_t count, float scale,
                                float* dL_dimage, float* loss, void* stream) {
+  SGS_NVTX("steepgs_l1_grad");
   steepgs_status s;
   if ((s = device_ok()) != STEEPGS_OK) return s;
   if (V < 1 || count < 0 || !image || !target || !dL_dimage) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "bad l1 arguments");
@@ -322,6 +379,7 @@ steepgs_status steepgs_render_bwd_split(const float* params, int64_t ld, int64_t
                                         const float* final_T, const int32_t* n_contrib, const float* dL_dimage,
                                         float* moments_ws, float* grad_S, int64_t ldg, int32_t accumulate,
                                         const int32_t* tiles_touched, float* view_grad_stats, void* stream) {
+  SGS_NVTX("steepgs_render_bwd_split");
   steepgs_status s;
   if ((s = device_ok()) != STEEPGS_OK) return s;
   CamPack pack;
@@ -336,6 +394,7 @@ steepgs_status steepgs_render_bwd_split(const float* params, int64_t ld, int64_t
   if (n > 0 && (!params || !splats || !final_T || !n_contrib || !dL_dimage || !moments_ws || !grad_S))
     return fail(STEEPGS_ERR_INVALID_ARGUMENT, "null pointer");
   if (!aligned(moments_ws, 16)) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "moments_ws must be 16-byte aligned");
+  if ((s = check_token(b, splats, n, cams, V, rp)) != STEEPGS_OK) return s;
   const RasterK rk = raster_k(rp);
   cudaError_t e = launch_render_bwd(splats, *b, cams[0].width, cams[0].height, rk, final_T, n_contrib, dL_dimage, n,
                                     moments_ws, (cudaStream_t)stream);
@@ -349,6 +408,7 @@ steepgs_status steepgs_render_bwd_moments(const steepgs_splat* splats, int64_t n
                                           const steepgs_camera* cams, int32_t V, const steepgs_raster_params* rp,
                                           const float* final_T, const int32_t* n_contrib, const float* dL_dimage,
                                           float* moments_ws, void* stream) {
+  SGS_NVTX("steepgs_render_bwd_moments");
   steepgs_status s;
   if ((s = device_ok()) != STEEPGS_OK) return s;
   if ((s = check_views(cams, V, nullptr)) != STEEPGS_OK) return s;
@@ -357,6 +417,7 @@ steepgs_status steepgs_render_bwd_moments(const steepgs_splat* splats, int64_t n
   if (n < 0 || (n > 0 && (!splats || !final_T || !n_contrib || !dL_dimage || !moments_ws)))
     return fail(STEEPGS_ERR_INVALID_ARGUMENT, "null pointer");
   if (!aligned(moments_ws, 16)) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "moments_ws must be 16-byte aligned");
+  if ((s = check_token(b, splats, n, cams, V, rp)) != STEEPGS_OK) return s;
   const cudaError_t e = launch_render_bwd(splats, *b, cams[0].width, cams[0].height, raster_k(rp), final_T, n_contrib,
                                           dL_dimage, n, moments_ws, (cudaStream_t)stream);
   return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_render_bwd_moments");
@@ -366,6 +427,7 @@ steepgs_status steepgs_gauss_bwd_split(const float* params, int64_t ld, int64_t 
                                        int32_t V, const steepgs_raster_params* rp,
                                        float* moments_ws, float* grad_S, int64_t ldg, int32_t accumulate,
                                        const int32_t* tiles_touched, float* view_grad_stats, void* stream) {
+  SGS_NVTX("steepgs_gauss_bwd_split");
   steepgs_status s;
   if ((s = device_ok()) != STEEPGS_OK) return s;
   CamPack pack;
@@ -394,6 +456,7 @@ steepgs_status steepgs_densify_adc(float* params, int64_t ld, int64_t n, int64_t
                                    const steepgs_adc_params* ap, uint8_t* kind, int32_t* dest_index,
                                    int64_t* n_new, int32_t* status, void* workspace, size_t ws_bytes,
                                    void* stream) {
+  SGS_NVTX("steepgs_densify_adc");
   steepgs_status s;
   if ((s = device_ok()) != STEEPGS_OK) return s;
   if (!ap || n < 0 || capacity < n || ld < capacity || ldg < capacity || ldz < n || capacity > INT32_MAX ||
@@ -411,6 +474,7 @@ steepgs_status steepgs_densify_adc(float* params, int64_t ld, int64_t n, int64_t
 steepgs_status steepgs_adam_step(float* params, int64_t ld, int64_t n, const float* grad_S, int64_t ldg,
                                  float* adam_m, float* adam_v, int64_t ldm, const steepgs_adam_params* ap,
                                  int64_t step, float* gacc, int32_t gacc_accumulate, void* stream) {
+  SGS_NVTX("steepgs_adam_step");
   steepgs_status s;
   if ((s = device_ok()) != STEEPGS_OK) return s;
   if (!ap || step < 1 || n < 0 || ld < n || ldg < n || ldm < n || !(ap->beta1 >= 0.0 && ap->beta1 < 1.0) ||
@@ -425,6 +489,7 @@ steepgs_status steepgs_adam_step(float* params, int64_t ld, int64_t n, const flo
 steepgs_status steepgs_reset_moments(float* adam_m, float* adam_v, int64_t ldm, int64_t n,
                                      const uint8_t* split_mask, const int64_t* n_split, int32_t mask_value,
                                      int32_t planes, void* stream) {
+  SGS_NVTX("steepgs_reset_moments");
   steepgs_status s;
   if ((s = device_ok()) != STEEPGS_OK) return s;
   if (!adam_m || !adam_v || !n_split || n < 0 || ldm < n || (n > 0 && !split_mask) || mask_value < 1 ||
@@ -437,6 +502,7 @@ steepgs_status steepgs_reset_moments(float* adam_m, float* adam_v, int64_t ldm, 
 
 steepgs_status steepgs_copy_planes(float* dst, int64_t ld_dst, const float* src, int64_t ld_src, int64_t n,
                                    int32_t first, int32_t count, void* stream) {
+  SGS_NVTX("steepgs_copy_planes");
   if (!dst || !src || n < 0 || ld_dst < n || ld_src < n || first < 0 || count < 0)
     return fail(STEEPGS_ERR_INVALID_ARGUMENT, "bad copy_planes arguments");
   if (n == 0 || count == 0) return STEEPGS_OK;
@@ -454,6 +520,7 @@ steepgs_status steepgs_densify(float* params, int64_t ld, int64_t n, int64_t cap
                                const steepgs_densify_params* dp, uint8_t* split_mask, int32_t* dest_index,
                                float* lambda_min, int64_t* n_split, int32_t* status, void* workspace,
                                size_t ws_bytes, void* stream) {
+  SGS_NVTX("steepgs_densify");
   steepgs_status s;
   if ((s = device_ok()) != STEEPGS_OK) return s;
   if (!dp || !(dp->denom > 0.f) || dp->gate < 0 || dp->gate > 2)
@@ -472,6 +539,7 @@ steepgs_status steepgs_densify_host_count(float* params, int64_t ld, int64_t n, 
                                           int64_t ldg, const steepgs_densify_params* dp, uint8_t* split_mask,
                                           int32_t* dest_index, float* lambda_min, int64_t* n_split, int32_t* status,
                                           void* workspace, size_t ws_bytes, int64_t* n_split_host, void* stream) {
+  SGS_NVTX("steepgs_densify_host_count");
   if (!n_split_host) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "n_split_host null");
   steepgs_status s = steepgs_densify(params, ld, n, capacity, grad_S, ldg, dp, split_mask, dest_index, lambda_min,
                                      n_split, status, workspace, ws_bytes, stream);

@@ -141,3 +141,45 @@ def test_instance_overflow_auto_grow():
     b = rz.binning_arrays()
     assert b["overflow"] == 0 and rz.max_instances >= b["n_instances"] > 16
     assert torch.equal(rz.image, ref.image)
+
+
+def test_backward_rejects_stale_binning():
+    """STEEPGS_ERR_STALE_STATE: render_bwd refuses a binning that was not rendered
+    forward since its bin_sort, or whose forward used other splats / cameras / raster params;
+    nothing is launched and the moments stay zero."""
+    from gpu_run import to_dev
+    from paper_2505_05587_b200 import _lib
+    from paper_2505_05587_b200.pipeline import Raster, Rasterizer
+    cfg = synth.CONFIGS["C1"]
+    p = to_dev(synth.scene_for(cfg))
+    cams = synth.cameras_for(cfg, views=1)
+    dl = to_dev(synth.dl_dimage(1, 64, 64, 3))
+    rz = Rasterizer(64, 1, 64, 64)
+    rz.project(p, 64, cams)
+    rz.bin_sort()
+
+    def bwd(rp=None, cams_arr=None, splats=None):
+        _lib.render_bwd_moments(rz.splats if splats is None else splats, 64, rz.binning,
+                                rz.cams_arr if cams_arr is None else cams_arr, 1, rz.rp if rp is None else rp,
+                                rz.final_T, rz.n_contrib, dl, rz.moments)
+
+    for case in ("no forward", "re-sorted", "other raster", "other camera", "other splats"):
+        if case == "re-sorted":
+            rz.render_fwd()
+            rz.bin_sort()
+        elif case != "no forward":
+            rz.render_fwd()
+        kw = {}
+        if case == "other raster":
+            kw["rp"] = Raster(alpha_min=0.01).c()
+        elif case == "other camera":
+            kw["cams_arr"] = _lib.cameras(synth.cameras_for(cfg, views=1, seed=99))
+        elif case == "other splats":
+            kw["splats"] = rz.splats[64:]
+        with pytest.raises(_lib.SteepGSError) as e:
+            bwd(**kw)
+        assert e.value.status == 4, case
+    rz.render_fwd()
+    bwd()                                                                   # the matching forward: accepted
+    torch.cuda.synchronize()
+    assert float(rz.moments.abs().sum()) > 0

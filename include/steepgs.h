@@ -346,6 +346,14 @@ uint64_t steepgs_launch_count(void);
 /* Library version / build string. */
 const char* steepgs_version(void);
 
+/* Debugging: the device-side invariant checks of the checked build (libsteepgs_checked.so, built with
+ * -DSTEEPGS_CHECKS): ring-stage identity under the mbarrier protocol of the raster kernels, list / row
+ * / instance-id bounds, radix scatter bounds, densify offspring slots.  *compiled = 0 in the release
+ * build (nothing is checked there); otherwise *failures = failed checks since the last reset and
+ * *first_line = the source line of the first (0 if none).  reset != 0 zeroes the counters after reading. */
+steepgs_status steepgs_debug_checks(int32_t* compiled /*[host]*/, uint64_t* failures /*[host]*/,
+                                    uint32_t* first_line /*[host]*/, int32_t reset);
+
 #ifdef __cplusplus
 }
 #endif

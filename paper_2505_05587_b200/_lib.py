@@ -10,7 +10,9 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsteepgs.so")
+# STEEPGS_LIB selects another build of the same library (the debug-checked libsteepgs_checked.so,
+# tests/test_checked_build.py); the default is the in-tree release build
+LIB_PATH = os.environ.get("STEEPGS_LIB") or os.path.join(_HERE, "libsteepgs.so")
 
 STATUS = {0: "ok", 1: "invalid argument", 2: "workspace too small", 3: "capacity exceeded",
           5: "unsupported device", 6: "CUDA error"}
@@ -95,6 +97,7 @@ def lib():
             "steepgs_compact_planes": [P, I64, P, I64, I32, I64, P, P],
             "steepgs_loss_workspace_size": [I32, I32, I32, P],
             "steepgs_l1_ssim_grad": [P, P, I32, I32, I32, F, F, P, P, P, C.c_size_t, P],
+            "steepgs_debug_checks": [P, P, P, I32],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -341,3 +344,10 @@ def launch_count() -> int:
 
 def version() -> str:
     return lib().steepgs_version().decode()
+
+
+def debug_checks(reset: bool = False) -> dict:
+    """Device-side invariant checks of the checked build (see steepgs.h): compiled, failures, first_line."""
+    c, f, l = C.c_int32(0), C.c_uint64(0), C.c_uint32(0)
+    _check("steepgs_debug_checks", lib().steepgs_debug_checks(C.byref(c), C.byref(f), C.byref(l), int(bool(reset))))
+    return dict(compiled=bool(c.value), failures=int(f.value), first_line=int(l.value))

@@ -131,7 +131,36 @@ static steepgs_status check_binning(const steepgs_binning* b, int32_t V, const s
 
 using namespace sgs;
 
+#ifdef STEEPGS_CHECKS
+namespace sgs {
+cudaError_t checks_io_render(unsigned int* out, bool reset);
+cudaError_t checks_io_sort(unsigned int* out, bool reset);
+cudaError_t checks_io_densify(unsigned int* out, bool reset);
+}  // namespace sgs
+#endif
+
 extern "C" {
+
+steepgs_status steepgs_debug_checks(int32_t* compiled, uint64_t* failures, uint32_t* first_line, int32_t reset) {
+  if (!compiled || !failures || !first_line) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "null pointer");
+  *failures = 0;
+  *first_line = 0;
+#ifdef STEEPGS_CHECKS
+  *compiled = 1;
+  cudaError_t (*io[3])(unsigned int*, bool) = {checks_io_render, checks_io_sort, checks_io_densify};
+  for (auto f : io) {
+    unsigned int v[2] = {0u, 0u};
+    const cudaError_t e = f(v, reset != 0);
+    if (e != cudaSuccess) return cuda_fail(e, "steepgs_debug_checks");
+    *failures += v[0];
+    if (v[0] && !*first_line) *first_line = v[1];
+  }
+#else
+  *compiled = 0;
+#endif
+  return STEEPGS_OK;
+}
+
 
 const char* steepgs_status_string(steepgs_status s) {
   switch (s) {

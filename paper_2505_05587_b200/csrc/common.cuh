@@ -7,6 +7,35 @@
 
 namespace sgs {
 
+// ---- debug-checked build (-DSTEEPGS_CHECKS, libsteepgs_checked.so; tests/test_checked_build.py) ----
+// Device-side invariants that compute-sanitizer would otherwise be needed for (ring stage identity
+// under the mbarrier protocol, list / row / instance / scatter bounds).  A failed check counts into a
+// per-translation-unit device word and records its line; steepgs_debug_checks() reads them.  In the
+// release build SGS_CHECK compiles to nothing.
+#ifdef STEEPGS_CHECKS
+#define SGS_CHECKS_TU(tag)                                                                 \
+  static __device__ unsigned int g_sgs_fail[2];                                            \
+  cudaError_t checks_io_##tag(unsigned int* out, bool reset) {                            \
+    cudaError_t e = cudaMemcpyFromSymbol(out, g_sgs_fail, sizeof(g_sgs_fail));             \
+    if (e == cudaSuccess && reset) {                                                       \
+      const unsigned int z[2] = {0u, 0u};                                                  \
+      e = cudaMemcpyToSymbol(g_sgs_fail, z, sizeof(z));                                    \
+    }                                                                                      \
+    return e;                                                                              \
+  }
+#define SGS_CHECK(cond)                                                                    \
+  do {                                                                                     \
+    if (!(cond)) {                                                                         \
+      if (atomicAdd(&g_sgs_fail[0], 1u) == 0u) g_sgs_fail[1] = (unsigned int)__LINE__;    \
+    }                                                                                      \
+  } while (0)
+#else
+#define SGS_CHECKS_TU(tag)
+#define SGS_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 constexpr int kTile = 16;          // tile edge in pixels (16x16 = 256 threads per tile block)
 constexpr int kMaxViews = 64;      // cameras passed by value in kernel parameters
 

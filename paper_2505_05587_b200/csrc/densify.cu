@@ -19,6 +19,8 @@
 
 namespace sgs {
 
+SGS_CHECKS_TU(densify)
+
 namespace {
 
 constexpr int kThreads = 256;
@@ -428,6 +430,7 @@ __global__ void __launch_bounds__(kThreads) k_densify_decide(float* __restrict__
     const int64_t b = n + (int64_t)(s_excl + s_cnt[j][warp] + pos[j]);
     mask[i] = split[j] ? 1 : 0;
     dest[i] = split[j] ? (int32_t)b : -1;  // Z24
+    SGS_CHECK(!split[j] || (b >= n && b < 2 * n));            // (the fused path needs capacity >= 2n)
     if (kFused) {
 #pragma unroll
       for (int k = 14; k < 20; ++k) grad_S[k * ldg + i] = 0.f;   // Z23
@@ -513,6 +516,7 @@ __global__ void __launch_bounds__(kThreads) k_densify_apply(float* __restrict__ 
 #pragma unroll
   for (int k = 14; k < 20; ++k) grad_S[k * ldg + i] = 0.f;
   if (!mask[i]) return;
+  SGS_CHECK(dest[i] >= n && dest[i] < n + ns);
   spawn(params, ld, grad_S, ldg, i, dest[i], S6, eta, eps_abs);
 }
 

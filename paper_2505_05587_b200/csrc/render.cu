@@ -44,6 +44,8 @@
 
 namespace sgs {
 
+SGS_CHECKS_TU(render)
+
 namespace {
 
 constexpr int kConsumers = 8;                       // one pixel per thread, 8 warps per 16x16 tile
@@ -148,7 +150,7 @@ template <bool kFwd, int kProd, int kS, int kC = kConsumers, class BatchOf>
 __device__ __forceinline__ void run_producer(SmemT<kS, kC>& sm, const uint32_t* __restrict__ ids,
                                              const steepgs_splat* __restrict__ vs, uint32_t first, int nb,
                                              BatchOf batch_of, double ox, double oy, float* mom_view, float lmin,
-                                             uint8_t* __restrict__ inst_mask, int pw, int lane) {
+                                             uint8_t* __restrict__ inst_mask, int pw, int lane, int64_t n_g) {
   // producer warp pw of kProd stages the batch slots kk = (q kProd + pw) * 32 + lane
   constexpr int kQ = kBatch / 32 / kProd;
   uint32_t gcur[kQ], gnext[kQ];
@@ -205,6 +207,7 @@ __device__ __forceinline__ void run_producer(SmemT<kS, kC>& sm, const uint32_t* 
       for (int q = 0; q < kQ; ++q) {
         const int kk = (q * kProd + pw) * 32 + lane;
         if (kk >= cnt) { B.mask[kk] = 0u; continue; }
+        SGS_CHECK((int64_t)gcur[q] < n_g);                           // instance ids index the splats
         const double2 mean = *reinterpret_cast<const double2*>(&sm.raw[0][kk]);
         const float4 a = *reinterpret_cast<const float4*>(&sm.raw[1][kk]);   // conic', log2 o
         const float4 b = *reinterpret_cast<const float4*>(&sm.raw[2][kk]);   // rgb, o
@@ -320,7 +323,7 @@ __global__ void __launch_bounds__(kThreadsFwd, 4) k_render_fwd(const steepgs_spl
     const int len = (int)(rg.y - rg.x);
     run_producer<true, kFwdProducers, kFwdStages>(sm, ids, splats + (int64_t)view * n, rg.x, nb,
                                       [len](int k, int& rel, int& cnt) { rel = k * kBatch; cnt = min(len - rel, kBatch); },
-                                      ox, oy, nullptr, __log2f(rk.alpha_min), inst_mask, warp - kConsumers, lane);
+                                      ox, oy, nullptr, __log2f(rk.alpha_min), inst_mask, warp - kConsumers, lane, n);
     return;
   }
 
@@ -338,6 +341,7 @@ __global__ void __launch_bounds__(kThreadsFwd, 4) k_render_fwd(const steepgs_spl
     const int s = k % kFwdStages;
     mbar_wait(&sm.full[s], (k / kFwdStages) & 1, kSuspendNs);
     const Buffer& B = sm.buf[s];
+    SGS_CHECK(B.base == k * kBatch);                 // the stage holds batch k (mbarrier ring protocol)
     if (B.stop) break;
     if (!warp_done) {
       uint8_t* lst = sm.buf[s].list[warp];
@@ -515,7 +519,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
                           rel = (nb - 1 - k) * kBatch;
                           cnt = min(L - rel, kBatch);
                         },
-                        ox, oy, moments + (int64_t)view * n * 12, __log2f(rk.alpha_min), inst_mask, 0, lane);
+                        ox, oy, moments + (int64_t)view * n * 12, __log2f(rk.alpha_min), inst_mask, 0, lane, n);
     return;
   }
 
@@ -595,6 +599,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat*
     const int s = k % kStages;
     mbar_wait(&sm.full[s], (k / kStages) & 1, kSuspendNs);
     const Buffer& B = sm.buf[s];
+    SGS_CHECK(B.base == (nb - 1 - k) * kBatch);      // the stage holds batch k (mbarrier ring protocol)
     uint8_t* lst = sm.buf[s].list[warp];
     const int nl = build_list(B, lst, 1u << warp, lane, wmax - B.base);   // only entries before the warp's prefix end
     const int lim = last - B.base;                          // this pixel composited list positions < last
@@ -798,7 +803,7 @@ __global__ void __launch_bounds__(32 * (kC2 + kProd2), kMinBlocks) k_render_bwd2
                                           cnt = min(L - rel, kBatch);
                                         },
                                         ox, oy, moments + (int64_t)view * n * 12, __log2f(rk.alpha_min), inst_mask,
-                                        warp - kC2, lane);
+                                        warp - kC2, lane, n);
     return;
   }
 
@@ -826,6 +831,7 @@ __global__ void __launch_bounds__(32 * (kC2 + kProd2), kMinBlocks) k_render_bwd2
   // ---- phase 2 over the chunk's first `ne` rows ----
   auto reduce_chunk = [&](int ne) {
     __syncwarp();
+    SGS_CHECK(ne >= 1 && ne <= kChunk2);
     // packed accumulators over the source lanes' (w_a, w_b): P1 = sum, P2 = sum x, P3 = sum x^2, P4 / P5 =
     // sum / sum x over the lanes of the second row (y0' = 1); PU = (u0, u1)
     u64 P1 = 0ull, P2 = 0ull, P3 = 0ull, P4 = 0ull, P5 = 0ull, PU = 0ull;
@@ -897,6 +903,7 @@ __global__ void __launch_bounds__(32 * (kC2 + kProd2), kMinBlocks) k_render_bwd2
     const int s = k % kStages;
     mbar_wait(&sm.full[s], (k / kStages) & 1, kSuspendNs);
     const BufferT<kC2>& B = sm.buf[s];
+    SGS_CHECK(B.base == (nb - 1 - k) * kBatch);      // the stage holds batch k (mbarrier ring protocol)
     uint8_t* lst = sm.buf[s].list[warp];
     const int nl = build_list(B, lst, wbits, lane, wmax - B.base);
     const int lima = lasta - B.base, limb = lastb - B.base;
@@ -910,6 +917,7 @@ __global__ void __launch_bounds__(32 * (kC2 + kProd2), kMinBlocks) k_render_bwd2
         sptr[fill + lane] = B.mptr[j];
       }
       auto recurse = [&](u64 ee, int j, int e) {
+        SGS_CHECK(e >= 0 && e < kChunk2 && j < kBatch);
         const float ea = lo2(ee), eb = hi2(ee);
         const bool ha = j < lima && ea >= lmin, hb = j < limb && eb >= lmin;
         const float sa = ha ? ex2_approx(ea) : 0.0f, sb = hb ? ex2_approx(eb) : 0.0f;

@@ -20,6 +20,8 @@
 
 namespace sgs {
 
+SGS_CHECKS_TU(sort)
+
 namespace {
 
 constexpr int kScanThreads = 256;
@@ -281,6 +283,7 @@ __global__ void __launch_bounds__(kRadixThreads, 3) k_radix_pass(const uint32_t*
   for (int j = 0; j < kRadixItems; ++j) {
     if (d[j] < 256u) {
       const uint32_t lp = s_local[d[j]] + s_whist[warp][d[j]] + rank[j];
+      SGS_CHECK(lp < (uint32_t)kRadixTile);
       s_keys[lp] = k[j];
       s_vals[lp] = v[j];
     }
@@ -291,6 +294,7 @@ __global__ void __launch_bounds__(kRadixThreads, 3) k_radix_pass(const uint32_t*
     const uint32_t kk = s_keys[idx];
     const uint32_t dd = (kk >> shift) & 255u;
     const uint32_t g = s_dbase[dd] + (uint32_t)idx - s_local[dd];
+    SGS_CHECK((int64_t)g < n);
     keys_out[g] = kk;
     vals_out[g] = s_vals[idx];
   }

@@ -1,0 +1,42 @@
+"""The debug-checked build (libsteepgs_checked.so, -DSTEEPGS_CHECKS) over the whole hot path
+(scripts/checked_path.py): zero failed device-side invariant checks — the mbarrier rings deliver
+the batch each consumer expects, list / row / instance-id / scatter / offspring indices stay in
+bounds — and results identical to the release build (the checks only read).  This stands in for
+SURVEY §5's compute-sanitizer row, which the GPU pool does not allow."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SCRIPT = os.path.join(ROOT, "scripts", "checked_path.py")
+
+
+def _run(lib):
+    env = dict(os.environ)
+    if lib:
+        env["STEEPGS_LIB"] = lib
+    r = subprocess.run([sys.executable, SCRIPT], capture_output=True, text=True, timeout=900, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    return json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+
+
+@pytest.mark.gpu
+def test_checked_build_whole_path():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2505_05587_b200 import build as B
+    lib = B.build(checked=True)
+    chk = _run(lib)
+    rel = _run(None)
+    assert chk["checks"]["compiled"] and not rel["checks"]["compiled"]
+    assert chk["checks"]["failures"] == 0, chk["checks"]
+    for name, a in chk["scenarios"].items():
+        b = rel["scenarios"][name]
+        for k in ("image", "ids", "n_instances", "n_split", "pairs"):
+            assert a[k] == b[k], (name, k)
+        for x, y in zip(a["grad_abs_sum"], b["grad_abs_sum"]):      # float atomics: order only
+            assert abs(x - y) <= 1e-4 * max(abs(y), 1e-30), name

@@ -3,42 +3,44 @@
 // §4.3).
 //
 // Work decomposition (B200): one block per 16x16 tile and view, warp-specialised:
-//   * warps 0..7 (consumers) own one pixel per thread; warp w covers the 8x4 sub-block
-//     x in 8 (w & 1) .. +7, y in 4 (w >> 1) .. +3;
 //   * producer warps (2 in the forward, 1 in the backward) stage the tile's depth-ordered splats
 //     into a ring of shared-memory buffers (5 in the forward, 3 in the backward) of kBatch splats:
 //     the 64-B records are copied with cp.async (ids prefetched two batches ahead), made
-//     tile-relative, and given the 8-bit mask of sub-blocks their alpha support {m <= tau} reaches
-//     (box test refined by an exact per-strip ellipse test).  The forward stores each instance's
-//     mask (binning.inst_mask); the backward's producer reads it back instead of recomputing it and
-//     copies only the 48 record bytes it needs.  Each consumer compacts a staged batch to its own
-//     sub-block's splats with 4 ballots.
+//     tile-relative, and given the 8-bit mask of 8x4 sub-blocks their alpha support {m <= tau}
+//     reaches (box test refined by an exact per-strip ellipse test).  The forward stores each
+//     instance's mask (binning.inst_mask); the backward's producer reads it back instead of
+//     recomputing it and copies only the 48 record bytes it needs.
+//   * forward consumers: 8 warps, one pixel per thread, warp w on the 8x4 sub-block
+//     x in 8 (w & 1) .. +7, y in 4 (w >> 1) .. +3;
+//   * backward consumers (k_render_bwd2): 4 warps, two pixels per thread, warp w on the 8x8 block
+//     (w & 1, w >> 1), lane (lx, ly) on pixels (lx, ly) and (lx, ly + 4), the per-pixel arithmetic
+//     on packed f32x2 (fma/add/mul.rn.f32x2): one warp visit per (8x8 block, splat) instead of one
+//     per (8x4 sub-block, splat).
+// Each consumer compacts a staged batch to the splats whose mask reaches its block (ballots).
 // Full/empty mbarriers per buffer replace block-wide barriers, so consumer warps with short lists
 // run ahead by up to a ring's depth of batches instead of waiting for the slowest warp (waits:
-// try_wait, then parked with a suspend-time hint), and a consumer iterates only over the splats that
-// can touch its 32 pixels.  Consumers take four list entries per iteration: the four pair tests are
-// independent and are issued before the serial compositing / recursion, which is branch-free
-// (predicated) so the four steps need no divergence bookkeeping.
+// try_wait, then parked with a suspend-time hint).  Consumers take four list entries per iteration:
+// the four pair tests are independent and are issued before the serial compositing / recursion,
+// which is branch-free (predicated) so the four steps need no divergence bookkeeping.
 //
 // Per-pair arithmetic: the mean is made tile-relative in fp64 before rounding (offsets
 // d = x - Pi(p) carry ~1e-7 px error); the conic arrives pre-scaled by log2(e)/2 (a1) so that
 //   e = log2(o) - m',  m' = a + dy (b + Qyy' dy),  a = Qxx' dx^2,  b = 2 Qxy' dx,
 //   skip if e < log2(alpha_min) (<=> sigma < alpha_min),  sigma = 2^e,  alpha = min(amax, sigma)
-// in one function shared by both kernels (explicit round-to-nearest intrinsics), so forward and
-// backward take bit-identical decisions.
+// with explicit round-to-nearest operations (scalar in the forward, the same operations per f32x2
+// half in the backward), so forward and backward take bit-identical decisions.
 //
 // Backward: back to front over each pixel's composited prefix (n_contrib from the forward; the
 // tile's longest prefix is stored by the forward), T_i recovered as T_{i+1} / (1 - alpha_i)
 // (approximate reciprocal; relative error ~1 ulp per step), dL/dalpha_i = T_i sum_ch dL/dC_ch
 // (c_ch - B_ch) with B the normalised colour behind (C10), w = dL/dsigma * sigma.  Two phases per
-// chunk of 16 list entries (a chunk continues across batch boundaries): the pixel-parallel
-// recursion leaves (w, alpha T) in shared memory, then the two lanes of each entry sum its raw
-// moments over the contributing pixels in the warp's sub-block frame, recentre them on the splat
-// mean and add the 9 moments (w, w d, w d d^T, alpha T dL/dC) with vector REDs into
-// moments[view][gid][12].  The splitting matrix needs no per-pair work of its own:
+// chunk of list entries (a chunk continues across batch boundaries): the pixel-parallel recursion
+// leaves each lane's two-pixel partial sums in shared memory, then lanes grouped per entry sum them
+// with the lane positions as compile-time constants, rebuild the 9 moments (w, w d, w d d^T,
+// alpha T dL/dC) in the block frame, recentre them on the splat mean and add them with vector REDs
+// into moments[view][gid][12].  The splitting matrix needs no per-pair work of its own:
 // S_view = P^T (Q M Q - m0 Q) P is formed per Gaussian from these moments (gauss_bwd.cu).
 #include <atomic>
-#include <cstdlib>
 
 #include "common.cuh"
 
@@ -49,7 +51,6 @@ SGS_CHECKS_TU(render)
 namespace {
 
 constexpr int kConsumers = 8;                       // one pixel per thread, 8 warps per 16x16 tile
-constexpr int kThreads = 32 * (kConsumers + 1);     // + 1 producer warp (backward)
 constexpr int kFwdProducers = 2;                    // the forward's consumers are faster: 2 producer warps
 constexpr int kThreadsFwd = 32 * (kConsumers + kFwdProducers);
 constexpr int kBatch = 128;                         // splats per staged batch
@@ -70,15 +71,15 @@ struct BufferT {
 };
 using Buffer = BufferT<kConsumers>;
 
-template <int kS, int kC = kConsumers>
+template <int kS, int kC = kConsumers, int kRaw = 4>
 struct SmemT {
   BufferT<kC> buf[kS];
-  uint4 raw[4][kBatch];          // producer staging: the next batch's 64-B records (cp.async), SoA by 16 B
+  uint4 raw[kRaw][kBatch];       // producer staging: the next batch's records (cp.async), SoA by 16 B
+                                 // (the backward copies 3 of the 4 16-B parts: no extents)
   unsigned long long full[kS], empty[kS];
   int done_warps;
   int stop_flag[2];              // forward: the producers' shared early-exit decision (double-buffered)
 };
-using Smem = SmemT<kStages>;
 using SmemFwd = SmemT<kFwdStages>;
 
 __device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -146,8 +147,8 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // round trip once it runs ahead.  Staging a record is then two fp64 subtractions and eight
 // interval tests of the padded extents against the 8x4 sub-blocks.
 // kFwd: stop early once every consumer warp has terminated (forward early exit).
-template <bool kFwd, int kProd, int kS, int kC = kConsumers, class BatchOf>
-__device__ __forceinline__ void run_producer(SmemT<kS, kC>& sm, const uint32_t* __restrict__ ids,
+template <bool kFwd, int kProd, int kS, int kC = kConsumers, int kRaw = 4, class BatchOf>
+__device__ __forceinline__ void run_producer(SmemT<kS, kC, kRaw>& sm, const uint32_t* __restrict__ ids,
                                              const steepgs_splat* __restrict__ vs, uint32_t first, int nb,
                                              BatchOf batch_of, double ox, double oy, float* mom_view, float lmin,
                                              uint8_t* __restrict__ inst_mask, int pw, int lane, int64_t n_g) {
@@ -438,233 +439,8 @@ __global__ void __launch_bounds__(kThreadsFwd, 4) k_render_fwd(const steepgs_spl
   }
 }
 
-constexpr int kChunk = 16;   // list entries per backward chunk (phase 1 -> phase 2)
-
-struct BwdScratch {
-  float2 wat[kConsumers][kChunk][33];  // (dL/dsigma * sigma, alpha T) per (entry, pixel); padded rows
-  uint32_t cmask[kConsumers][kChunk];  // contributing pixels of each entry (ballot)
-  float4 pix[kConsumers][32];          // per pixel: centre relative to the warp's 8x4 sub-block
-                                       // centre (x', y'), dL/dC_r, dL/dC_g
-  float pdl2[kConsumers][32];          // per pixel: dL/dC_b
-  float2 emean[kConsumers][kChunk];    // per chunk entry: the splat mean (tile-relative)
-  float* eptr[kConsumers][kChunk];     // per chunk entry: &moments[view][gid][0]
-};
-
 __device__ __forceinline__ void red_v4(float* p, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
-}
-
-// Backward.  Per consumer warp and chunk of 16 list entries (back to front; a chunk continues
-// across batch boundaries, so only the tile's last chunk is partial):
-//   phase 1 (pixel-parallel): each lane runs its pixel's recursion over the entries and leaves
-//     w = dL/dsigma * sigma and alpha T in shared memory, plus a ballot of contributing pixels;
-//     the entry's splat mean and moment address are kept beside the chunk (the batch buffer may
-//     be released before the chunk is reduced);
-//   phase 2 (splat-parallel): lanes e and e + 16 own entry e and sum its raw moments over the
-//     contributing pixels (even / odd rank) in the sub-block frame (x', y'), combine with one
-//     xor-16 shuffle per value, recentre on the splat mean (d = (x', y') + (u, v)) and add the 9
-//     moments with two 16-B + one 4-B vector REDs.
-// No per-(warp, splat) cross-lane reduction tree: the reduction costs O(contributing pairs).
-__global__ void __launch_bounds__(kThreads, 3) k_render_bwd(const steepgs_splat* __restrict__ splats,
-                                                         const uint32_t* __restrict__ ids,
-                                                         const uint2* __restrict__ ranges, int64_t n, int W, int H,
-                                                         int tiles_x, int tiles_per_view, const RasterK rk,
-                                                         const float* __restrict__ final_T,
-                                                         const int32_t* __restrict__ n_contrib,
-                                                         const float* __restrict__ dL_dimage,
-                                                         const uint32_t* __restrict__ tile_last,
-                                                         uint8_t* __restrict__ inst_mask,
-                                                         float* __restrict__ moments) {
-  extern __shared__ __align__(16) unsigned char dsmem[];
-  Smem& sm = *reinterpret_cast<Smem*>(dsmem);
-  BwdScratch& sc = *reinterpret_cast<BwdScratch*>(dsmem + ((sizeof(Smem) + 15) & ~size_t(15)));
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int tile = blockIdx.x, view = blockIdx.y;
-  const int tx = tile % tiles_x, ty = tile / tiles_x;
-  const double ox = (double)(tx * kTile), oy = (double)(ty * kTile);
-  const uint2 rg = ranges[(int64_t)view * tiles_per_view + tile];
-  const int64_t HW = (int64_t)W * H;
-  const int lx = 8 * (warp & 1) + (lane & 7), ly = 4 * (warp >> 1) + (lane >> 3);
-  const int px = tx * kTile + lx, py = ty * kTile + ly;
-  const bool inside = warp < kConsumers && px < W && py < H;
-  const int64_t pix = (int64_t)py * W + px;
-  float T = 1.0f, dl0 = 0.0f, dl1 = 0.0f, dl2 = 0.0f;
-  int last = 0;
-  if (inside) {
-    T = final_T[(int64_t)view * HW + pix];
-    last = n_contrib[(int64_t)view * HW + pix];
-    const float* dl = dL_dimage + (int64_t)view * 3 * HW;
-    dl0 = dl[pix]; dl1 = dl[HW + pix]; dl2 = dl[2 * HW + pix];
-  }
-  if (warp < kConsumers) {
-    sc.pix[warp][lane] = make_float4((float)(lane & 7) - 3.5f, (float)(lane >> 3) - 1.5f, dl0, dl1);
-    sc.pdl2[warp][lane] = dl2;
-  }
-  // list prefix any pixel of the tile composited (stored by the forward), so the producer starts at
-  // once instead of after a block-wide reduction of n_contrib
-  const int L = (int)__ldg(tile_last + (int64_t)view * tiles_per_view + tile);
-  const int nb = (L + kBatch - 1) / kBatch;
-  if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&sm.full[s], 32);
-      mbar_init(&sm.empty[s], 32 * kConsumers);
-    }
-  }
-  __syncthreads();
-  const int wmax = __reduce_max_sync(0xffffffffu, last);
-
-  if (warp == kConsumers) {  // ---------------- producer: batches from the back ----------------
-    run_producer<false, 1, kStages>(sm, ids, splats + (int64_t)view * n, rg.x, nb,
-                        [nb, L](int k, int& rel, int& cnt) {
-                          rel = (nb - 1 - k) * kBatch;
-                          cnt = min(L - rel, kBatch);
-                        },
-                        ox, oy, moments + (int64_t)view * n * 12, __log2f(rk.alpha_min), inst_mask, 0, lane, n);
-    return;
-  }
-
-  // ---------------- consumers ----------------
-  const float fx = (float)lx + 0.5f, fy = (float)ly + 0.5f;
-  const float lmin = __log2f(rk.alpha_min);
-  const float amax = rk.alpha_max;
-  float B0 = rk.bg[0], B1 = rk.bg[1], B2 = rk.bg[2];
-  float2(*swat)[33] = sc.wat[warp];
-  uint32_t* scm = sc.cmask[warp];
-  const float4* spix = sc.pix[warp];
-  const float* sdl2 = sc.pdl2[warp];
-  float2* smean = sc.emean[warp];
-  float** sptr = sc.eptr[warp];
-  const int e2 = lane & (kChunk - 1), half = lane >> 4;
-  const float cxw = (float)(8 * (warp & 1) + 4), cyw = (float)(4 * (warp >> 1) + 2);   // sub-block centre
-  // ---- phase 2 over the chunk's first `ne` rows ----
-  auto reduce_chunk = [&](int ne) {
-    __syncwarp();
-    float acc[9];
-#pragma unroll
-    for (int q = 0; q < 9; ++q) acc[q] = 0.0f;
-    const bool valid = e2 < ne;
-    uint32_t full_bits = 0u;
-    if (valid) {
-      full_bits = scm[e2];
-      // the two lanes of an entry take the contributing pixels of even / odd rank (prefix parity)
-      uint32_t x = full_bits;
-      x ^= x << 1; x ^= x << 2; x ^= x << 4; x ^= x << 8; x ^= x << 16;
-      const uint32_t odd = full_bits & (x << 1);
-      uint32_t bits = half ? odd : (full_bits & ~odd);
-      const float2* row = swat[e2];
-      auto add = [&](float w, float at, float4 d, float dl2p) {   // raw moments in the sub-block frame
-        const float wx = w * d.x, wy = w * d.y;
-        acc[0] += w;
-        acc[1] += wx;
-        acc[2] += wy;
-        acc[3] = fmaf(wx, d.x, acc[3]);
-        acc[4] = fmaf(wx, d.y, acc[4]);
-        acc[5] = fmaf(wy, d.y, acc[5]);
-        acc[6] = fmaf(at, d.z, acc[6]);
-        acc[7] = fmaf(at, d.w, acc[7]);
-        acc[8] = fmaf(at, dl2p, acc[8]);
-      };
-      while (bits) {        // two pixels per iteration; a missing second one adds zeros
-        const int pa = 31 - __clz(bits);
-        bits ^= 1u << pa;
-        const bool two = bits != 0u;
-        const int pb = two ? 31 - __clz(bits) : pa;
-        bits &= ~(two ? (1u << pb) : 0u);
-        const float2 wa = row[pa], wb = row[pb];
-        const float4 da = spix[pa], db = spix[pb];
-        const float la = sdl2[pa], lb = sdl2[pb];
-        add(wa.x, wa.y, da, la);
-        add(two ? wb.x : 0.0f, two ? wb.y : 0.0f, db, lb);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 9; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], 16);
-    if (valid && half == 0 && full_bits) {
-      const float2 gm = smean[e2];
-      const float u = cxw - gm.x, v = cyw - gm.y;   // d = (x', y') + (u, v)
-      const float S0 = acc[0], Sx = acc[1], Sy = acc[2];
-      const float m1x = fmaf(u, S0, Sx), m1y = fmaf(v, S0, Sy);
-      const float Mxx = fmaf(u, fmaf(u, S0, 2.0f * Sx), acc[3]);
-      const float Mxy = fmaf(u, m1y, fmaf(v, Sx, acc[4]));
-      const float Myy = fmaf(v, fmaf(v, S0, 2.0f * Sy), acc[5]);
-      float* mp = sptr[e2];
-      red_v4(mp, S0, m1x, m1y, Mxx);
-      red_v4(mp + 4, Mxy, Myy, acc[6], acc[7]);
-      atomicAdd(mp + 8, acc[8]);
-    }
-    __syncwarp();
-  };
-  int fill = 0;   // rows of the current chunk already filled
-  for (int k = 0; k < nb; ++k) {
-    const int s = k % kStages;
-    mbar_wait(&sm.full[s], (k / kStages) & 1, kSuspendNs);
-    const Buffer& B = sm.buf[s];
-    SGS_CHECK(B.base == (nb - 1 - k) * kBatch);      // the stage holds batch k (mbarrier ring protocol)
-    uint8_t* lst = sm.buf[s].list[warp];
-    const int nl = build_list(B, lst, 1u << warp, lane, wmax - B.base);   // only entries before the warp's prefix end
-    const int lim = last - B.base;                          // this pixel composited list positions < last
-    for (int t_hi = nl; t_hi > 0;) {
-      const int m = min(t_hi, kChunk - fill);
-      const int t_lo = t_hi - m;
-      const int r0 = fill - t_lo;                           // row of list entry t = r0 + t
-      if (lane < m) {
-        const int j = lst[t_lo + lane];
-        smean[fill + lane] = *reinterpret_cast<const float2*>(&B.geo[j]);
-        sptr[fill + lane] = B.mptr[j];
-      }
-      // ---- phase 1: pixel-parallel recursion over entries t_hi-1 .. t_lo ----
-      // Four entries per iteration: the pair tests are evaluated before the (serial) recursion, so
-      // their shared-memory loads and arithmetic overlap.
-      // Branch-free (predicated): a lane that does not composite the entry takes alpha = 0, which
-      // leaves B unchanged exactly, and keeps its T; the hit lanes' values are those of the plain
-      // C10 recursion.
-      auto recurse = [&](bool hit, float ee, int j, int e) {
-        const float sigma = ex2_approx(ee);
-        const float alpha = hit ? fminf(amax, sigma) : 0.0f;
-        const float4 c = B.col[j];
-        const float om = 1.0f - alpha;
-        T = hit ? T * rcp_approx(om) : T;                  // T_i (before this splat)
-        const float d0 = c.x - B0, d1 = c.y - B1, d2 = c.z - B2;   // colour minus the colour behind
-        const float gsum = fmaf(dl2, d2, fmaf(dl1, d1, dl0 * d0));
-        B0 = fmaf(alpha, d0, B0);                           // B <- alpha c + (1 - alpha) B
-        B1 = fmaf(alpha, d1, B1);
-        B2 = fmaf(alpha, d2, B2);
-        if (hit) swat[e][lane] = make_float2(T * gsum * sigma, alpha * T);  // dL/dalpha * sigma (Z3), alpha T
-        const uint32_t bal = __ballot_sync(0xffffffffu, hit);
-        if (lane == 0) scm[e] = bal;
-      };
-      int t = t_hi - 1;
-      for (; t - 3 >= t_lo; t -= 4) {
-        int jj[4];
-        float ee[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          jj[u] = lst[t - u];
-          const float4 g = B.geo[jj[u]];
-          const float4 p = B.par[jj[u]];
-          ee[u] = pair_e(__fsub_rn(fx, g.x), __fsub_rn(fy, g.y), g, p);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) recurse(jj[u] < lim && ee[u] >= lmin, ee[u], jj[u], r0 + t - u);
-      }
-      for (; t >= t_lo; --t) {
-        const int ja = lst[t];
-        const float4 ga = B.geo[ja];
-        const float4 pa = B.par[ja];
-        const float ea = pair_e(__fsub_rn(fx, ga.x), __fsub_rn(fy, ga.y), ga, pa);
-        recurse(ja < lim && ea >= lmin, ea, ja, r0 + t);
-      }
-      fill += m;
-      t_hi = t_lo;
-      if (fill == kChunk) {
-        reduce_chunk(kChunk);
-        fill = 0;
-      }
-    }
-    __syncwarp();
-    mbar_arrive(&sm.empty[s]);
-  }
-  if (fill > 0) reduce_chunk(fill);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -730,7 +506,8 @@ __device__ __forceinline__ u64 pair_e2(float fx, u64 fy, const float4 g, const f
 }
 
 constexpr int kC2 = 4;                        // consumer warps (8x8 blocks) per tile
-using Smem2 = SmemT<kStages, kC2>;
+template <int kS2>
+using Smem2T = SmemT<kS2, kC2, 3>;
 
 template <int kChunk2>
 struct BwdScratch2 {
@@ -742,7 +519,7 @@ struct BwdScratch2 {
 
 // kChunk2: list entries per phase-1 -> phase-2 chunk (16: 2 lanes per entry in phase 2, 8: 4 lanes);
 // kProd2: producer warps.
-template <int kChunk2, int kProd2, int kMinBlocks>
+template <int kChunk2, int kProd2, int kMinBlocks, int kS2>
 __global__ void __launch_bounds__(32 * (kC2 + kProd2), kMinBlocks) k_render_bwd2(const steepgs_splat* __restrict__ splats,
                                                           const uint32_t* __restrict__ ids,
                                                           const uint2* __restrict__ ranges, int64_t n, int W, int H,
@@ -754,6 +531,7 @@ __global__ void __launch_bounds__(32 * (kC2 + kProd2), kMinBlocks) k_render_bwd2
                                                           uint8_t* __restrict__ inst_mask,
                                                           float* __restrict__ moments) {
   extern __shared__ __align__(16) unsigned char dsmem[];
+  using Smem2 = Smem2T<kS2>;
   Smem2& sm = *reinterpret_cast<Smem2*>(dsmem);
   BwdScratch2<kChunk2>& sc = *reinterpret_cast<BwdScratch2<kChunk2>*>(dsmem + ((sizeof(Smem2) + 15) & ~size_t(15)));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -788,7 +566,7 @@ __global__ void __launch_bounds__(32 * (kC2 + kProd2), kMinBlocks) k_render_bwd2
   const int L = (int)__ldg(tile_last + (int64_t)view * tiles_per_view + tile);
   const int nb = (L + kBatch - 1) / kBatch;
   if (tid == 0) {
-    for (int st = 0; st < kStages; ++st) {
+    for (int st = 0; st < kS2; ++st) {
       mbar_init(&sm.full[st], 32 * kProd2);
       mbar_init(&sm.empty[st], 32 * kC2);
     }
@@ -797,7 +575,7 @@ __global__ void __launch_bounds__(32 * (kC2 + kProd2), kMinBlocks) k_render_bwd2
   const int wmax = __reduce_max_sync(0xffffffffu, max(lasta, lastb));
 
   if (warp >= kC2) {  // ---------------- producers: batches from the back ----------------
-    run_producer<false, kProd2, kStages, kC2>(sm, ids, splats + (int64_t)view * n, rg.x, nb,
+    run_producer<false, kProd2, kS2, kC2, 3>(sm, ids, splats + (int64_t)view * n, rg.x, nb,
                                         [nb, L](int k, int& rel, int& cnt) {
                                           rel = (nb - 1 - k) * kBatch;
                                           cnt = min(L - rel, kBatch);
@@ -900,8 +678,8 @@ __global__ void __launch_bounds__(32 * (kC2 + kProd2), kMinBlocks) k_render_bwd2
 
   int fill = 0;   // rows of the current chunk already filled
   for (int k = 0; k < nb; ++k) {
-    const int s = k % kStages;
-    mbar_wait(&sm.full[s], (k / kStages) & 1, kSuspendNs);
+    const int s = k % kS2;
+    mbar_wait(&sm.full[s], (k / kS2) & 1, kSuspendNs);
     const BufferT<kC2>& B = sm.buf[s];
     SGS_CHECK(B.base == (nb - 1 - k) * kBatch);      // the stage holds batch k (mbarrier ring protocol)
     uint8_t* lst = sm.buf[s].list[warp];
@@ -1056,36 +834,18 @@ cudaError_t launch_render_bwd(const steepgs_splat* splats, const steepgs_binning
                               const float* dL_dimage, int64_t n, float* moments, cudaStream_t st) {
   const int tpv = b.tiles_x * b.tiles_y;
   dim3 grid(tpv, b.V);
-  const size_t smem = ((sizeof(Smem) + 15) & ~size_t(15)) + sizeof(BwdScratch);
-  {
-    static std::atomic<uint64_t> done{0};   // devices whose function attribute is set
-    const cudaError_t e = allow_dynamic_smem(done, (const void*)k_render_bwd, smem, true);
-    if (e != cudaSuccess) return e;
-  }
-  static const int variant = [] { const char* e = getenv("STEEPGS_BWD"); return e ? atoi(e) : 2; }();
-  auto run2 = [&](auto kern, size_t scratch, int prod, std::atomic<uint64_t>& done2) -> cudaError_t {
-    const size_t smem2 = ((sizeof(Smem2) + 15) & ~size_t(15)) + scratch;
-    const cudaError_t e = allow_dynamic_smem(done2, (const void*)kern, smem2, true);
-    if (e != cudaSuccess) return e;
-    kern<<<grid, 32 * (kC2 + prod), smem2, st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
-                                                b.tiles_x, tpv, rk, final_T, n_contrib, dL_dimage, b.tile_last,
-                                                b.inst_mask, moments);
-    return cudaSuccess;
-  };
-  static std::atomic<uint64_t> d2{0}, d3{0}, d4{0}, d5{0};
-  cudaError_t e2 = cudaSuccess;
-  if (variant == 2) {
-    e2 = run2(k_render_bwd2<16, 1, 3>, sizeof(BwdScratch2<16>), 1, d2);
-  } else if (variant == 3) {
-    e2 = run2(k_render_bwd2<8, 1, 4>, sizeof(BwdScratch2<8>), 1, d3);
-  } else if (variant == 4) {
-    e2 = run2(k_render_bwd2<16, 2, 3>, sizeof(BwdScratch2<16>), 2, d4);
-  } else if (variant == 5) {
-    e2 = run2(k_render_bwd2<8, 2, 4>, sizeof(BwdScratch2<8>), 2, d5);
-  } else {
-    k_render_bwd<<<grid, kThreads, smem, st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
-                                            b.tiles_x, tpv, rk, final_T, n_contrib, dL_dimage, b.tile_last, b.inst_mask, moments);
-  }
+  // 8-entry chunks (4 phase-2 lanes per entry), one producer warp, 3-stage ring, 4 blocks per SM: the
+  // fastest of the measured configurations (round 2)
+  constexpr int kCh = 8, kS2 = kStages;
+  using Kern = void (*)(const steepgs_splat*, const uint32_t*, const uint2*, int64_t, int, int, int, int, const RasterK,
+                        const float*, const int32_t*, const float*, const uint32_t*, uint8_t*, float*);
+  const Kern kern = k_render_bwd2<kCh, 1, 4, kS2>;
+  const size_t smem2 = ((sizeof(Smem2T<kS2>) + 15) & ~size_t(15)) + sizeof(BwdScratch2<kCh>);
+  static std::atomic<uint64_t> done2{0};
+  const cudaError_t e2 = allow_dynamic_smem(done2, (const void*)kern, smem2, true);
+  if (e2 == cudaSuccess)
+    kern<<<grid, 32 * (kC2 + 1), smem2, st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H, b.tiles_x,
+                                             tpv, rk, final_T, n_contrib, dL_dimage, b.tile_last, b.inst_mask, moments);
   if (e2 != cudaSuccess) return e2;
   note_launch();
   return check_launch("k_render_bwd");

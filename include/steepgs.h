@@ -116,9 +116,13 @@ typedef struct {
   uint32_t* tile_last;          /* [V * tiles_x * tiles_y]: zeroed by bin_sort; render_fwd stores the
                                    tile's composited list prefix (max over its pixels of n_contrib),
                                    which render_bwd reads: the backward needs the forward's binning */
-  uint8_t* inst_mask;           /* [max_instances]: render_fwd stores, per tile instance it stages,
-                                   the 8-bit mask of the tile's 8x4 sub-blocks the splat's alpha
-                                   support reaches; render_bwd reads it instead of recomputing */
+  uint8_t* inst_mask;           /* [max_instances]: render_fwd stores, per tile instance it stages
+                                   and its consumers finish, the 8-bit mask of the tile's 8x4
+                                   sub-blocks in which at least one pixel composited the splat (bit
+                                   2 strip + column); render_bwd reads it to visit only contributing
+                                   (block, splat) pairs.  Instances after the forward's early exit
+                                   (all pixels of the tile terminated) are not written; the backward
+                                   never reaches them (it stops at tile_last) */
   int64_t max_instances;
   int32_t tiles_x, tiles_y, V;
   uint64_t generation;          /* set by bin_sort: a process-wide counter, distinct per bin_sort call */

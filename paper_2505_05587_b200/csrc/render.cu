@@ -7,9 +7,12 @@
 //     into a ring of shared-memory buffers (5 in the forward, 3 in the backward) of kBatch splats:
 //     the 64-B records are copied with cp.async (ids prefetched two batches ahead), made
 //     tile-relative, and given the 8-bit mask of 8x4 sub-blocks their alpha support {m <= tau}
-//     reaches (box test refined by an exact per-strip ellipse test).  The forward stores each
-//     instance's mask (binning.inst_mask); the backward's producer reads it back instead of
-//     recomputing it and copies only the 48 record bytes it needs.
+//     reaches (box test refined by an exact per-strip ellipse test).  The forward's consumers record
+//     which list entries each warp composited (a per-lane shift register, OR-reduced over the warp
+//     every 32 entries) and OR them into the batch's per-splat mask of COMPOSITING sub-blocks, which
+//     the producers store as binning.inst_mask once the stage is released; the backward's producer
+//     reads it instead of recomputing a geometric mask and copies only the 48 record bytes it needs,
+//     so the backward visits exactly the (8x8 block, splat) pairs with a contribution.
 //   * forward consumers: 8 warps, one pixel per thread, warp w on the 8x4 sub-block
 //     x in 8 (w & 1) .. +7, y in 4 (w >> 1) .. +3;
 //   * backward consumers (k_render_bwd2): 4 warps, two pixels per thread, warp w on the 8x8 block
@@ -65,9 +68,12 @@ struct BufferT {
   float4 col[kBatch];            // (r, g, b, -)
   float* mptr[kBatch];           // backward: &moments[view][gid][0]
   uint32_t mask[kBatch];         // sub-blocks reached by the alpha support
+  uint32_t cm[kBatch];           // forward: sub-blocks in which >= 1 pixel composited the splat
+  uint32_t cflag[kC][kBatch / 32];   // forward: per consumer, bit t = list entry t was composited
   uint8_t list[kC][kBatch];      // per-consumer compacted lists (written by the consumer)
   int base;                      // list position (relative to the tile start) of slot 0
   int stop;                      // 1: no more batches (forward early termination)
+  int cnt;                       // forward: splats in the batch
 };
 using Buffer = BufferT<kConsumers>;
 
@@ -185,10 +191,22 @@ __device__ __forceinline__ void run_producer(SmemT<kS, kC, kRaw>& sm, const uint
   load_ids(0, gcur, mcur);
   issue(0, gcur);
   load_ids(1, gnext, mnext);
+  // forward: once the consumers have released a stage, the composited sub-block masks of its batch
+  // (cm, ORed in by the consumers) are stored as binning.inst_mask; each producer warp stores the
+  // slots it stages, so no other synchronisation is needed
+  auto flush = [&](const BufferT<kC>& Bf, int base0, int cnt0) {
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
+      const int kk = (q * kProd + pw) * 32 + lane;
+      if (kk < cnt0) inst_mask[first + base0 + kk] = (uint8_t)(Bf.cm[kk] & 0xFFu);
+    }
+  };
+  int kend = nb, stopped = 0;
   for (int k = 0; k < nb; ++k) {
     const int s = k % kS;
     if (k >= kS) mbar_wait(&sm.empty[s], ((k / kS) & 1) ^ 1, kSuspendNs);
     BufferT<kC>& B = sm.buf[s];
+    if (kFwd && k >= kS) flush(B, B.base, B.cnt);   // batch k - kS (read before the named barrier below)
     int stop = 0;
     if (kFwd) {   // one decision per batch for all producer warps (a split decision would deadlock)
       if (kProd == 1) {
@@ -253,16 +271,21 @@ __device__ __forceinline__ void run_producer(SmemT<kS, kC, kRaw>& sm, const uint
           m |= ok ? (xs & xb) << (2 * t) : 0u;
         }
         B.mask[kk] = m;
-        inst_mask[first + rel + kk] = (uint8_t)m;   // for the backward's producer
+        B.cm[kk] = 0u;              // the consumers OR in the sub-blocks that composite the splat
       }
     }
     if (pw == 0 && lane == 0) {
       B.base = rel;
       B.stop = stop;
+      B.cnt = cnt;
     }
     __syncwarp();
     mbar_arrive(&sm.full[s]);
-    if (stop) break;
+    if (stop) {
+      kend = k;
+      stopped = 1;
+      break;
+    }
 #pragma unroll
     for (int q = 0; q < kQ; ++q) {
       gcur[q] = gnext[q];
@@ -272,6 +295,13 @@ __device__ __forceinline__ void run_producer(SmemT<kS, kC, kRaw>& sm, const uint
     load_ids(k + 2, gnext, mnext);
   }
   cp_async_wait_all();
+  if (kFwd) {   // the batches still in the ring (the stop batch itself was never consumed)
+    for (int kb = max(0, kend - kS + stopped); kb < kend; ++kb) {
+      const int s = kb % kS;
+      mbar_wait(&sm.empty[s], (kb / kS) & 1, kSuspendNs);
+      flush(sm.buf[s], sm.buf[s].base, sm.buf[s].cnt);
+    }
+  }
 }
 
 // Consumer: compact the staged batch to the splats whose mask has bit `w` (ascending order, slots
@@ -352,7 +382,14 @@ __global__ void __launch_bounds__(kThreadsFwd, 4) k_render_fwd(const steepgs_spl
       // Two entries per iteration: both pair tests ahead of the serial compositing (as in the bwd).
       // Branch-free (predicated) so the four calls need no divergence bookkeeping; the values are
       // those of the plain C8 loop.
-      auto blend = [&](float e, int j) {
+      // Which list entries the warp composited (a warp OR-reduction per four entries into cflag);
+      // after the batch they are ORed into the batch's cm[] (sub-blocks with >= 1 composited pixel),
+      // which the producers store as binning.inst_mask once the stage is released, so the backward
+      // visits exactly the (block, splat) pairs that contribute.
+      uint32_t* cfl = sm.buf[s].cflag[warp];
+      if (lane < kBatch / 32) cfl[lane] = 0u;
+      __syncwarp();
+      auto blend = [&](float e, int j) -> bool {
         const bool live = !done && e >= lmin;             // sigma < alpha_min: C8 skip
         const float alpha = fminf(amax, ex2_approx(e));
         const float Tn = __fmul_rn(T, __fsub_rn(1.0f, alpha));
@@ -367,9 +404,19 @@ __global__ void __launch_bounds__(kThreadsFwd, 4) k_render_fwd(const steepgs_spl
         T = comp ? Tn : T;
         last = comp ? base1 + j : last;
         if (kCount) ncomp += comp ? 1 : 0;
+        return comp;
       };
+      // lb: a shift register of this lane's composited flags (one LEA per entry): after list position
+      // t, bit 0 is position t, bit k position t - k.  Every 32 positions (at the top of the loop, lanes
+      // converged) and after the batch the warp's OR of the lanes' words is stored to cflag[w], with
+      // position 32 w + i at bit 31 - i.
+      uint32_t lb = 0u;
       int t = 0;
       for (; t + 3 < nl; t += 4) {
+        if (t && (t & 31) == 0) {
+          const uint32_t wb = __reduce_or_sync(0xffffffffu, lb);
+          if (lane == 0) cfl[(t >> 5) - 1] = wb;
+        }
         int jj[4];
         float ee[4];
 #pragma unroll
@@ -379,16 +426,34 @@ __global__ void __launch_bounds__(kThreadsFwd, 4) k_render_fwd(const steepgs_spl
           const float2 p = *reinterpret_cast<const float2*>(&B.par[jj[u]]);
           ee[u] = pair_e(__fsub_rn(fx, g.x), __fsub_rn(fy, g.y), g, make_float4(p.x, p.y, 0.f, 0.f));
         }
-        if (done) continue;
+        if (done) {
+          lb <<= 4;
+          continue;
+        }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) blend(ee[u], jj[u]);
+        for (int u = 0; u < 4; ++u) lb = (lb << 1) | (uint32_t)blend(ee[u], jj[u]);
       }
-      for (; t < nl && !done; ++t) {
+      const int t4 = t;   // the tail's positions t4 .. nl - 1 share the word of t4
+      if (t4 && (t4 & 31) == 0 && t4 < nl) {
+        const uint32_t wb = __reduce_or_sync(0xffffffffu, lb);
+        if (lane == 0) cfl[(t4 >> 5) - 1] = wb;
+      }
+      for (; t < nl; ++t) {
         const int ja = lst[t];
         const float4 ga = B.geo[ja];
         const float2 pa = *reinterpret_cast<const float2*>(&B.par[ja]);
-        blend(pair_e(__fsub_rn(fx, ga.x), __fsub_rn(fy, ga.y), ga, make_float4(pa.x, pa.y, 0.f, 0.f)), ja);
+        bool c = false;
+        if (!done) c = blend(pair_e(__fsub_rn(fx, ga.x), __fsub_rn(fy, ga.y), ga, make_float4(pa.x, pa.y, 0.f, 0.f)), ja);
+        lb = (lb << 1) | (uint32_t)c;
       }
+      __syncwarp();
+      if (nl > 0) {   // the last (partial) word: positions 32 w .. nl - 1 at bits (nl - 1 - pos)
+        const uint32_t wb = __reduce_or_sync(0xffffffffu, lb) << (31 - ((nl - 1) & 31));
+        if (lane == 0) cfl[(nl - 1) >> 5] = wb;
+      }
+      __syncwarp();
+      for (int tt = lane; tt < nl; tt += 32)
+        if ((cfl[tt >> 5] >> (31 - (tt & 31))) & 1u) atomicOr(&sm.buf[s].cm[lst[tt]], 1u << warp);
       if (__all_sync(0xffffffffu, done)) {
         warp_done = true;
         if (lane == 0) atomicAdd(&sm.done_warps, 1);

@@ -543,7 +543,7 @@ def main():
         roofline = dict(bound="hbm", kernel=dom, achieved=round(ach, 1), peak=hbm, unit="GB/s",
                         frac=round(ach / hbm, 4), traffic=None, peak_basis=f"MEASURED_PEAKS.json ({peaks['src']})")
     # DRAM traffic of the dominant kernel from the committed ncu --set full capture (profiles/)
-    kname = {"render_bwd": "k_render_bwd", "render_fwd": "k_render_fwd", "gauss_bwd_S": "k_gauss_bwd",
+    kname = {"render_bwd": "k_render_bwd2", "render_fwd": "k_render_fwd", "gauss_bwd_S": "k_gauss_bwd",
              "project": "k_project"}.get(dom)
     tfile = os.path.join(ROOT, "profiles", "traffic.json")
     if kname and os.path.exists(tfile):

@@ -7,6 +7,7 @@ import os
 import sys
 
 d = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out"
+ROUND = sys.argv[2] if len(sys.argv) > 2 else "2"
 
 
 def line(name):
@@ -18,9 +19,9 @@ def m(x):
     return f"{x / 1e6:.1f}M"
 
 
-print("# All BASELINE configs on 1×B200 (bench.py --config Cx, 8 views per step; round 1)\n")
+print(f"# All BASELINE configs on 1×B200 (bench.py --config Cx, 8 views per step; round {ROUND})\n")
 print("`python bench.py --config Cx --no-cpu-baseline` on the gpurun box (`scripts/gpu_configs.sh`, same build as the "
-      "C2 headline in `r01_summary.md`).  C1 is the oracle-sized parity case (64 Gaussians) and is not a bench line.  "
+      f"C2 headline in `r0{ROUND}_summary.md`).  C1 is the oracle-sized parity case (64 Gaussians) and is not a bench line.  "
       "Per-stage ms are CUDA-event means over the timed steps.\n")
 print("| config | n | W×H | ms/view | e2e ms/view | ms/step | project | bin_sort | fwd | bwd | gauss_bwd+S | densify | "
       "N_vis | I | contributing pairs | split |")

@@ -3,7 +3,7 @@
 // §4.3).
 //
 // Work decomposition (B200): one block per 16x16 tile and view, warp-specialised:
-//   * producer warps (2 in the forward, 1 in the backward) stage the tile's depth-ordered splats
+//   * one producer warp (forward and backward) stages the tile's depth-ordered splats
 //     into a ring of shared-memory buffers (5 in the forward, 3 in the backward) of kBatch splats:
 //     the 64-B records are copied with cp.async (ids prefetched two batches ahead), made
 //     tile-relative, and given the 8-bit mask of 8x4 sub-blocks their alpha support {m <= tau}
@@ -54,7 +54,7 @@ SGS_CHECKS_TU(render)
 namespace {
 
 constexpr int kConsumers = 8;                       // one pixel per thread, 8 warps per 16x16 tile
-constexpr int kFwdProducers = 2;                    // the forward's consumers are faster: 2 producer warps
+constexpr int kFwdProducers = 1;                    // one producer warp: 56 registers for the consumers (2 warps: 48, rematerialisation)
 constexpr int kThreadsFwd = 32 * (kConsumers + kFwdProducers);
 constexpr int kBatch = 128;                         // splats per staged batch
 constexpr int kStages = 3;                          // ring depth (backward: bounded by shared memory)

@@ -392,8 +392,11 @@ def main():
     # the stage boundaries stay eager so the per-stage CUDA events of the timed region bracket them.
     # The NCCL allreduce stays eager.  Kernels inside a graph are counted when it is captured.
     graphs = {}
+    step_graphs = {}
     graph_launches = [0]
-    launch_mode = ["eager" if args.no_graph else "per-stage CUDA graphs (NCCL allreduce eager)"]
+    launch_mode = ["eager" if args.no_graph else
+                   "one CUDA graph per step (NCCL allreduce eager, between two graphs) for the timed steps; "
+                   "per-stage CUDA graphs with CUDA events between them for the stage breakdown"]
 
     def capture(tgt):
         key = tgt.data_ptr()
@@ -415,6 +418,59 @@ def main():
                 continue
             gs[nm] = (g, _lib.launch_count() - l0)
         graphs[key] = gs
+        # the whole step as graph segments split after bin_sort (the e2e copy of the next step's targets
+        # waits for an event recorded there) and at the (eager) NCCL allreduce
+        segs, cur = [], []
+        for nm, fn in stage_fns(tgt):
+            if fn is None:
+                continue
+            if nm == "allreduce":
+                segs.append(cur)
+                segs.append("allreduce")
+                cur = []
+            else:
+                cur.append(fn)
+                if nm == "bin_sort":
+                    segs.append(cur)
+                    segs.append("sorted")
+                    cur = []
+        segs.append(cur)
+        out = []
+        for sg in segs:
+            if sg in ("allreduce", "sorted"):
+                out.append((sg, None, 0))
+                continue
+            if not sg:
+                continue
+            g = torch.cuda.CUDAGraph()
+            l0 = _lib.launch_count()
+            try:
+                with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                    for fn in sg:
+                        fn()
+            except RuntimeError as exc:
+                torch.cuda.synchronize()
+                print(f"bench: step-graph capture failed, per-stage graphs used: {exc}", file=sys.stderr)
+                return
+            out.append(("graph", g, _lib.launch_count() - l0))
+        step_graphs[key] = out
+
+    def step_whole(tgt=None, sorted_ev=None):
+        """One step through the step graphs (timed steps and e2e); falls back to step()."""
+        tgt = targets if tgt is None else tgt
+        sgs = step_graphs.get(tgt.data_ptr()) if not args.no_graph else None
+        if not sgs:
+            step(tgt=tgt, sorted_ev=sorted_ev)
+            return
+        for kind, g, nl in sgs:
+            if kind == "allreduce":
+                allreduce_accumulators(grad_S, n=n)
+            elif kind == "sorted":
+                if sorted_ev is not None:
+                    sorted_ev.record(stream)
+            else:
+                g.replay()
+                graph_launches[0] += nl
 
     def step(ev=None, tgt=None, sorted_ev=None):
         tgt = targets if tgt is None else tgt
@@ -457,18 +513,28 @@ def main():
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
     for k in range(args.steps):
-        step(evs[k])
+        step_whole()
     t_end.record(stream)
+    barrier()
+    launches = _lib.launch_count() - launches0 + graph_launches[0]   # kernels of the timed steps
+    # stage breakdown: the same steps again with per-stage graphs and CUDA events between them (each
+    # event costs ~4 us of device time, so this pass is not the headline)
+    t_st0 = torch.cuda.Event(enable_timing=True)
+    t_st1 = torch.cuda.Event(enable_timing=True)
+    t_st0.record(stream)
+    for k in range(args.steps):
+        step(evs[k])
+    t_st1.record(stream)
     barrier()
     clocks = sampler.stop()
     clocks["probe_mhz"] = clock_probe(stream)
-    launches = _lib.launch_count() - launches0 + graph_launches[0]
     elapsed = t_start.elapsed_time(t_end)
     if ws > 1:
         tt = torch.tensor([elapsed], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         elapsed = float(tt.item())
     ms_step = elapsed / args.steps
+    ms_step_staged = t_st0.elapsed_time(t_st1) / args.steps
     # stage i spans from the last event recorded before it to its own (empty stages: 0)
     recorded = [0] + [i + 1 for i, (_, fn) in enumerate(stage_fns(targets)) if fn is not None]
     stage_ms = {}
@@ -594,7 +660,7 @@ def main():
                 if k + 1 < nsteps and args.h2d_at == "start":
                     h2d(slot ^ 1)
                 stream.wait_event(copied[slot])
-                step(tgt=tbuf[slot], sorted_ev=sorted_evs[slot])
+                step_whole(tgt=tbuf[slot], sorted_ev=sorted_evs[slot])
                 if k + 1 < nsteps and args.h2d_at == "after_sort":
                     h2d(slot ^ 1, after=sorted_evs[slot])
                 consumed[slot].record(stream)
@@ -645,7 +711,7 @@ def main():
     if rank == 0:
         out = dict(
             metric=METRIC, value=round(value, 5), unit=UNIT, n_gpus=ws, steps=args.steps, warmup=args.warmup,
-            ms_per_step=round(ms_step, 4), higher_is_better=False, scaling="weak", vs_baseline=None, dtype="f32",
+            ms_per_step=round(ms_step, 4), ms_per_step_with_stage_events=round(ms_step_staged, 4), higher_is_better=False, scaling="weak", vs_baseline=None, dtype="f32",
             data="synthetic",
             config=dict(workload=f"{cfg.name}: {cfg.cite}" + (f" + SH degree {shd}" if shd is not None else "")
                         + (f" + SSIM loss (lambda {args.ssim})" if args.ssim is not None else "")

@@ -658,10 +658,6 @@ __global__ void __launch_bounds__(32 * (kC2 + kProd2), kMinBlocks) k_render_bwd2
   u64 T2 = pk2(Ta, Tb);
   u64 B0 = bc2(rk.bg[0]), B1 = bc2(rk.bg[1]), B2 = bc2(rk.bg[2]);
   const u64 dl0 = pk2(dla[0], dlb[0]), dl1 = pk2(dla[1], dlb[1]), dl2 = pk2(dla[2], dlb[2]);
-  u64 dla01, dlb01;   // a second packing of the same values (own registers: asm volatile is not rematerialised)
-  asm volatile("mov.b64 %0, {%1, %2};" : "=l"(dla01) : "f"(dla[0]), "f"(dla[1]));
-  asm volatile("mov.b64 %0, {%1, %2};" : "=l"(dlb01) : "f"(dlb[0]), "f"(dlb[1]));
-  const float dla2 = dla[2], dlb2 = dlb[2];
   const uint32_t wbits = (1u << (4 * by + bx)) | (1u << (4 * by + 2 + bx));   // the block's two 8x4 strips
   float4(*sst)[33] = sc.st[warp];
   float(*su2)[33] = sc.u2[warp];
@@ -775,10 +771,9 @@ __global__ void __launch_bounds__(32 * (kC2 + kProd2), kMinBlocks) k_render_bwd2
         B2 = fma2(al, d2, B2);
         const u64 w = mul2(mul2(T2, gs), pk2(sa, sb));      // dL/dalpha sigma (Z3)
         const u64 aT = mul2(al, T2);
-        const float aTa = lo2(aT), aTb = hi2(aT);
-        const u64 u01 = fma2(bc2(aTb), dlb01, mul2(bc2(aTa), dla01));   // (u0, u1) packed, no horizontal add
-        sst[e][lane] = make_float4(lo2(w), hi2(w), lo2(u01), hi2(u01));
-        su2[e][lane] = fmaf(aTb, dlb2, __fmul_rn(aTa, dla2));
+        const u64 p0 = mul2(aT, dl0), p1 = mul2(aT, dl1), p2 = mul2(aT, dl2);   // aT dL/dC per pixel
+        sst[e][lane] = make_float4(lo2(w), hi2(w), lo2(p0) + hi2(p0), lo2(p1) + hi2(p1));
+        su2[e][lane] = lo2(p2) + hi2(p2);
       };
       int t = t_hi - 1;
       for (; t - 3 >= t_lo; t -= 4) {

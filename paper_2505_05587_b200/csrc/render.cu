@@ -410,46 +410,40 @@ __global__ void __launch_bounds__(kThreadsFwd, 4) k_render_fwd(const steepgs_spl
       // t, bit 0 is position t, bit k position t - k.  Every 32 positions (at the top of the loop, lanes
       // converged) and after the batch the warp's OR of the lanes' words is stored to cflag[w], with
       // position 32 w + i at bit 31 - i.
-      uint32_t lb = 0u;
-      int t = 0;
-      for (; t + 3 < nl; t += 4) {
-        if (t && (t & 31) == 0) {
-          const uint32_t wb = __reduce_or_sync(0xffffffffu, lb);
-          if (lane == 0) cfl[(t >> 5) - 1] = wb;
-        }
-        int jj[4];
-        float ee[4];
+      // the list in words of 32 entries: groups of four, then the word's tail, then the word's flush
+      for (int w0 = 0; w0 < nl; w0 += 32) {
+        const int tend = min(nl, w0 + 32);
+        uint32_t lb = 0u;
+        int t = w0;
+        for (; t + 3 < tend; t += 4) {
+          int jj[4];
+          float ee[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          jj[u] = lst[t + u];
-          const float4 g = B.geo[jj[u]];
-          const float2 p = *reinterpret_cast<const float2*>(&B.par[jj[u]]);
-          ee[u] = pair_e(__fsub_rn(fx, g.x), __fsub_rn(fy, g.y), g, make_float4(p.x, p.y, 0.f, 0.f));
-        }
-        if (done) {
-          lb <<= 4;
-          continue;
-        }
+          for (int u = 0; u < 4; ++u) {
+            jj[u] = lst[t + u];
+            const float4 g = B.geo[jj[u]];
+            const float2 p = *reinterpret_cast<const float2*>(&B.par[jj[u]]);
+            ee[u] = pair_e(__fsub_rn(fx, g.x), __fsub_rn(fy, g.y), g, make_float4(p.x, p.y, 0.f, 0.f));
+          }
+          if (done) {
+            lb <<= 4;
+            continue;
+          }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) lb = (lb << 1) | (uint32_t)blend(ee[u], jj[u]);
-      }
-      const int t4 = t;   // the tail's positions t4 .. nl - 1 share the word of t4
-      if (t4 && (t4 & 31) == 0 && t4 < nl) {
-        const uint32_t wb = __reduce_or_sync(0xffffffffu, lb);
-        if (lane == 0) cfl[(t4 >> 5) - 1] = wb;
-      }
-      for (; t < nl; ++t) {
-        const int ja = lst[t];
-        const float4 ga = B.geo[ja];
-        const float2 pa = *reinterpret_cast<const float2*>(&B.par[ja]);
-        bool c = false;
-        if (!done) c = blend(pair_e(__fsub_rn(fx, ga.x), __fsub_rn(fy, ga.y), ga, make_float4(pa.x, pa.y, 0.f, 0.f)), ja);
-        lb = (lb << 1) | (uint32_t)c;
-      }
-      __syncwarp();
-      if (nl > 0) {   // the last (partial) word: positions 32 w .. nl - 1 at bits (nl - 1 - pos)
-        const uint32_t wb = __reduce_or_sync(0xffffffffu, lb) << (31 - ((nl - 1) & 31));
-        if (lane == 0) cfl[(nl - 1) >> 5] = wb;
+          for (int u = 0; u < 4; ++u) lb = (lb << 1) | (uint32_t)blend(ee[u], jj[u]);
+        }
+        for (; t < tend; ++t) {
+          const int ja = lst[t];
+          const float4 ga = B.geo[ja];
+          const float2 pa = *reinterpret_cast<const float2*>(&B.par[ja]);
+          bool c = false;
+          if (!done) c = blend(pair_e(__fsub_rn(fx, ga.x), __fsub_rn(fy, ga.y), ga, make_float4(pa.x, pa.y, 0.f, 0.f)), ja);
+          lb = (lb << 1) | (uint32_t)c;
+        }
+        // position w0 + i at bit 31 - i (a partial word is shifted up)
+        const uint32_t wb = __reduce_or_sync(0xffffffffu, lb) << ((32 - (tend - w0)) & 31);
+        if (lane == 0) cfl[w0 >> 5] = wb;
+        if (__all_sync(0xffffffffu, done)) break;   // the rest of the list composites nothing here
       }
       __syncwarp();
       for (int tt = lane; tt < nl; tt += 32)

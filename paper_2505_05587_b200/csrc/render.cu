@@ -429,8 +429,10 @@ __global__ void __launch_bounds__(kThreadsFwd, 4) k_render_fwd(const steepgs_spl
             lb <<= 4;
             continue;
           }
+          bool cb[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) lb = (lb << 1) | (uint32_t)blend(ee[u], jj[u]);
+          for (int u = 0; u < 4; ++u) cb[u] = blend(ee[u], jj[u]);
+          lb = (lb << 4) | (cb[0] ? 8u : 0u) | (cb[1] ? 4u : 0u) | (cb[2] ? 2u : 0u) | (cb[3] ? 1u : 0u);
         }
         for (; t < tend; ++t) {
           const int ja = lst[t];

@@ -33,21 +33,31 @@ def allreduce_accumulators(acc: torch.Tensor, group=None, n: int | None = None) 
     return allreduce_planes(acc, 0, acc.shape[0], n, group)
 
 
+_COALESCE = [True]
+
+
 def allreduce_planes(acc: torch.Tensor, first: int, count: int, n: int, group=None) -> torch.Tensor:
     """Sum planes [first, first + count), columns [0, n) of a planar accumulator over ranks, in place
     (one asynchronous allreduce per contiguous row slice, no staging copies)."""
     if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
         return acc
     rows = [acc[k, :n] for k in range(first, first + count)]
-    if dist.get_backend(group) == "nccl":
+    if dist.get_backend(group) == "nccl" and _COALESCE[0]:
         # one NCCL group (ncclGroupStart/End) over the contiguous row slices: a single fused
-        # collective launch for the 20 planes instead of 20 (VERDICT r1 weak #15), still no staging copy
-        from torch.distributed.distributed_c10d import _coalescing_manager
-        with _coalescing_manager(group=group, device=acc.device, async_ops=True) as cm:
-            for r in rows:
-                dist.all_reduce(r, op=dist.ReduceOp.SUM, group=group)
-        cm.wait()
-        return acc
+        # collective launch for the 20 planes instead of 20 (VERDICT r1 weak #15), still no staging copy.
+        # _coalescing_manager is a private torch API: if it is missing or refuses, fall back (once, for
+        # the process) to the per-row asynchronous allreduces below, which NCCL pipelines.
+        try:
+            from torch.distributed.distributed_c10d import _coalescing_manager
+            with _coalescing_manager(group=group, device=acc.device, async_ops=True) as cm:
+                for r in rows:
+                    dist.all_reduce(r, op=dist.ReduceOp.SUM, group=group)
+            cm.wait()
+            return acc
+        except (ImportError, AttributeError, TypeError, NotImplementedError) as exc:
+            import warnings
+            warnings.warn(f"coalesced allreduce unavailable ({exc}); per-plane allreduces")
+            _COALESCE[0] = False
     works = [dist.all_reduce(r, op=dist.ReduceOp.SUM, group=group, async_op=True) for r in rows]
     for w in works:
         w.wait()

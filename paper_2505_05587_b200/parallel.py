@@ -54,7 +54,7 @@ def allreduce_planes(acc: torch.Tensor, first: int, count: int, n: int, group=No
                     dist.all_reduce(r, op=dist.ReduceOp.SUM, group=group)
             cm.wait()
             return acc
-        except (ImportError, AttributeError, TypeError, NotImplementedError) as exc:
+        except (ImportError, AttributeError, TypeError, NotImplementedError, RuntimeError) as exc:
             import warnings
             warnings.warn(f"coalesced allreduce unavailable ({exc}); per-plane allreduces")
             _COALESCE[0] = False

@@ -523,16 +523,8 @@ __device__ __forceinline__ u64 pk2(float a, float b) {
   asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
   return r;
 }
-__device__ __forceinline__ float lo2(u64 r) {
-  float a, b;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
-  return a;
-}
-__device__ __forceinline__ float hi2(u64 r) {
-  float a, b;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
-  return b;
-}
+__device__ __forceinline__ float lo2(u64 r) { return __uint_as_float((uint32_t)r); }
+__device__ __forceinline__ float hi2(u64 r) { return __uint_as_float((uint32_t)(r >> 32)); }
 __device__ __forceinline__ u64 add2(u64 a, u64 b) {
   u64 d;
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
@@ -659,7 +651,6 @@ __global__ void __launch_bounds__(32 * (kC2 + kProd2), kMinBlocks) k_render_bwd2
   float(*su2)[33] = sc.u2[warp];
   float2* smean = sc.emean[warp];
   float** sptr = sc.eptr[warp];
-  constexpr int kG = 32 / kChunk2;              // phase-2 lanes per entry; each sums kChunk2 source lanes
   const int e2 = lane & (kChunk2 - 1), half = lane / kChunk2;
   const float cxw = (float)(8 * bx + 4), cyw = (float)(8 * by + 4);   // block centre (tile-relative)
 

@@ -329,6 +329,9 @@ def main():
                          "DMA writes then overlap the ALU-bound render kernels, not the L2-resident sort)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-v1", action="store_true", help="skip the 1-view-per-step line (SURVEY §8(d1))")
+    ap.add_argument("--collective", default="nccl", choices=["nccl", "fused"],
+                    help="N > 1: NCCL allreduce of grads + S, or k_gauss_bwd scattering to the column owners over "
+                         "peer memory + owner reduce/broadcast (torch symmetric memory)")
     args = ap.parse_args()
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
         return relaunch_under_torchrun(args)
@@ -364,6 +367,19 @@ def main():
     pristine[:, :n] = torch.from_numpy(p_np).to(dev)
     params = pristine.clone()
     grad_S = torch.zeros(20, cap, dtype=torch.float32, device=dev)
+    reducer = None
+    if args.collective == "fused" and ws > 1:
+        if args.sh_degree is not None:
+            raise SystemExit("bench.py: --collective fused has no SH colour path (use nccl)")
+        from paper_2505_05587_b200.parallel import FusedGradReduce
+        reducer = FusedGradReduce(cap, device=dev)   # symmetric-memory grad_S + partial buffers
+        grad_S = reducer.grad_S
+
+    def collective():
+        if reducer is not None:
+            reducer.exchange(n, accumulate=0)         # owners reduce + broadcast over NVLink (P2P)
+        else:
+            allreduce_accumulators(grad_S, n=n)       # NCCL, [k, :n] rows in one group
     targets = torch.from_numpy(tg_np).to(dev)
     rz = Rasterizer(cap, V, cfg.width, cfg.height, max_instances=int(3.0 * V * n), device=dev)
     shd = args.sh_degree
@@ -388,6 +404,9 @@ def main():
             _lib.copy_planes(params, pristine, n, 10, 1)     # opacity) -- checkpoint restore, no kernel
 
         def bwd():
+            if reducer is not None:                   # a6 with its output scattered to the column owners
+                reducer.scatter(rz, params, n)
+                return
             if shd is not None:
                 rz.sh_bwd(params, grad_S, sh_rest, shd, grad_sh, 0)
             rz.gauss_bwd(params, grad_S, accumulate=0 | (4 if shd is not None else 0))
@@ -402,7 +421,7 @@ def main():
                                                                       loss_ws))),
             ("render_bwd", rz.render_bwd_moments),
             ("gauss_bwd_S", bwd),
-            ("allreduce", (lambda: allreduce_accumulators(grad_S, n=n)) if ws > 1 else None),   # NCCL, [k, :n]
+            ("allreduce", collective if ws > 1 else None),
             ("densify", lambda: rz.densify(params, grad_S, n, cap, denom=float(V * ws), want_lambda=False,
                                            budget=None if args.budget_frac is None else int(args.budget_frac * n))),
         ]
@@ -484,7 +503,7 @@ def main():
             return
         for kind, g, nl in sgs:
             if kind == "allreduce":
-                allreduce_accumulators(grad_S, n=n)
+                collective()
             elif kind == "sorted":
                 if sorted_ev is not None:
                     sorted_ev.record(stream)
@@ -738,7 +757,9 @@ def main():
                         + (f" + densify budget {args.budget_frac:g} n" if args.budget_frac is not None else ""),
                         n=n, width=cfg.width, height=cfg.height,
                         views_per_gpu_per_step=V, views_per_step=V * ws, capacity=cap,
-                        parallelism=f"view-sharded dp{ws}" + (" + NCCL allreduce(grads+S)" if ws > 1 else ""),
+                        parallelism=f"view-sharded dp{ws}" + ((" + NCCL allreduce(grads+S)" if reducer is None else
+                                                                " + fused gauss_bwd reduce-scatter / owner broadcast "
+                                                                "over NVLink (symmetric memory)") if ws > 1 else ""),
                         l2="no flush: per-step working set (params 56 MB + splats 48 B x V x n + sort/moment "
                            "buffers) exceeds the 126 MB L2",
                         scene="synthetic surface-like (SURVEY 8(d1)), procedural targets",

@@ -350,6 +350,29 @@ uint64_t steepgs_launch_count(void);
 /* Library version / build string. */
 const char* steepgs_version(void);
 
+/* ---- a7 fused with a6 (SURVEY §8(e) B200-native variant of the allreduce of grads + S): the
+ * columns [0, n) are split into R owner ranges of `chunk` columns (rank q owns [q chunk, q chunk +
+ * chunk) ∩ [0, n); chunk = steepgs_scatter_chunk(n, R), a multiple of 32).
+ * steepgs_gauss_bwd_scatter is steepgs_gauss_bwd_split whose per-Gaussian result (20 planes, as
+ * accumulate = 0 would write them) goes straight to the owner: rank `rank` stores the columns of
+ * range q into peer_partials[q] + (rank * 20 + plane) * chunk (each peer buffer [R][20][chunk] fp32;
+ * device pointers valid on this device — peer / P2P-mapped memory of the other ranks, e.g. torch
+ * symmetric memory; [host] array of R pointers).  No SH colour, no view_grad_stats on this path.
+ * Then, after a cross-rank barrier (the caller's), steepgs_reduce_bcast on rank q sums the R partials
+ * of its range in rank order, applies `accumulate` (0, 1 or 2 as in steepgs_gauss_bwd_split, against
+ * its own grad_S, which equals every rank's) and stores the result into every rank's grad_S
+ * (peer_grad_S [host][R] device pointers, planar [20][ldg]); a second barrier ends the exchange.
+ * Together they replace the allreduce: the reduce-scatter is fused into the compute kernel and the
+ * all-gather into the reduction.  R <= 8. */
+steepgs_status steepgs_scatter_chunk(int64_t n, int32_t R, int64_t* chunk /*[host]*/);
+steepgs_status steepgs_gauss_bwd_scatter(const float* params, int64_t ld, int64_t n, const steepgs_camera* cams,
+                                         int32_t V, const steepgs_raster_params* rp, float* moments_ws,
+                                         const uint64_t* peer_partials /*[host][R]*/, int32_t R, int32_t rank,
+                                         int64_t chunk, void* stream);
+steepgs_status steepgs_reduce_bcast(const float* partials, int32_t R, int32_t rank, int64_t n, int64_t chunk,
+                                    const uint64_t* peer_grad_S /*[host][R]*/, int64_t ldg, int32_t accumulate,
+                                    void* stream);
+
 /* Debugging: the device-side invariant checks of the checked build (libsteepgs_checked.so, built with
  * -DSTEEPGS_CHECKS): ring-stage identity under the mbarrier protocol of the raster kernels, list / row
  * / instance-id bounds, radix scatter bounds, densify offspring slots.  *compiled = 0 in the release

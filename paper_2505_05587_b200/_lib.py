@@ -98,6 +98,9 @@ def lib():
             "steepgs_loss_workspace_size": [I32, I32, I32, P],
             "steepgs_l1_ssim_grad": [P, P, I32, I32, I32, F, F, P, P, P, C.c_size_t, P],
             "steepgs_debug_checks": [P, P, P, I32],
+            "steepgs_scatter_chunk": [I64, I32, P],
+            "steepgs_gauss_bwd_scatter": [P, I64, I64, P, I32, P, P, P, I32, I32, I64, P],
+            "steepgs_reduce_bcast": [P, I32, I32, I64, I64, P, I64, I32, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -351,3 +354,30 @@ def debug_checks(reset: bool = False) -> dict:
     c, f, l = C.c_int32(0), C.c_uint64(0), C.c_uint32(0)
     _check("steepgs_debug_checks", lib().steepgs_debug_checks(C.byref(c), C.byref(f), C.byref(l), int(bool(reset))))
     return dict(compiled=bool(c.value), failures=int(f.value), first_line=int(l.value))
+
+
+def scatter_chunk(n: int, R: int) -> int:
+    c = C.c_int64(0)
+    _check("steepgs_scatter_chunk", lib().steepgs_scatter_chunk(int(n), int(R), C.byref(c)))
+    return int(c.value)
+
+
+def _ptr_array(ptrs):
+    arr = (C.c_uint64 * len(ptrs))()
+    for k, p in enumerate(ptrs):
+        arr[k] = int(p)
+    return arr
+
+
+def gauss_bwd_scatter(params, ld, n, cams_arr, V, rp, moments, peer_partials, R, rank, chunk, stream=None):
+    """peer_partials: R device pointers (ints) of the owners' [R][20][chunk] partial buffers."""
+    _check("steepgs_gauss_bwd_scatter",
+           lib().steepgs_gauss_bwd_scatter(ptr(params), ld, n, cams_arr, V, C.byref(rp), ptr(moments),
+                                           _ptr_array(peer_partials), R, rank, chunk, stream_ptr(stream)))
+
+
+def reduce_bcast(partials, R, rank, n, chunk, peer_grad_S, ldg, accumulate=0, stream=None):
+    """peer_grad_S: R device pointers (ints) of the ranks' [20][ldg] grad_S."""
+    _check("steepgs_reduce_bcast",
+           lib().steepgs_reduce_bcast(ptr(partials), R, rank, n, chunk, _ptr_array(peer_grad_S), ldg, int(accumulate),
+                                      stream_ptr(stream)))

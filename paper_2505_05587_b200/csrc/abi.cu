@@ -474,6 +474,62 @@ steepgs_status steepgs_gauss_bwd_split(const float* params, int64_t ld, int64_t 
   return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_gauss_bwd_split");
 }
 
+steepgs_status steepgs_scatter_chunk(int64_t n, int32_t R, int64_t* chunk) {
+  if (!chunk || n < 0 || R < 1 || R > kMaxRanks) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "bad scatter arguments");
+  const int64_t c = (n + R - 1) / R;
+  *chunk = ((c + 31) / 32) * 32;   // owners' column ranges start on 128-B boundaries
+  return STEEPGS_OK;
+}
+
+steepgs_status steepgs_gauss_bwd_scatter(const float* params, int64_t ld, int64_t n, const steepgs_camera* cams,
+                                         int32_t V, const steepgs_raster_params* rp, float* moments_ws,
+                                         const uint64_t* peer_partials, int32_t R, int32_t rank, int64_t chunk,
+                                         void* stream) {
+  SGS_NVTX("steepgs_gauss_bwd_scatter");
+  steepgs_status s;
+  if ((s = device_ok()) != STEEPGS_OK) return s;
+  CamPack pack;
+  if ((s = check_views(cams, V, &pack)) != STEEPGS_OK) return s;
+  if ((s = check_raster(rp)) != STEEPGS_OK) return s;
+  if (n < 0 || ld < n || R < 1 || R > kMaxRanks || rank < 0 || rank >= R || !peer_partials)
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "bad scatter arguments");
+  int64_t need = 0;
+  steepgs_scatter_chunk(n, R, &need);
+  if (chunk != need) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "chunk must be steepgs_scatter_chunk(n, R)");
+  if (n > 0 && (!params || !moments_ws)) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "null pointer");
+  if (!aligned(moments_ws, 16)) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "moments_ws must be 16-byte aligned");
+  ScatterOut sc{};
+  for (int q = 0; q < R; ++q) {
+    sc.peers[q] = reinterpret_cast<float*>(peer_partials[q]);
+    if (!sc.peers[q]) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "null peer partial buffer");
+  }
+  sc.R = R; sc.rank = rank; sc.chunk = chunk;
+  const cudaError_t e = launch_gauss_bwd(params, ld, n, pack, V, raster_k(rp), moments_ws, nullptr, 0, 0, nullptr,
+                                         nullptr, (cudaStream_t)stream, sc);
+  return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_gauss_bwd_scatter");
+}
+
+steepgs_status steepgs_reduce_bcast(const float* partials, int32_t R, int32_t rank, int64_t n, int64_t chunk,
+                                    const uint64_t* peer_grad_S, int64_t ldg, int32_t accumulate, void* stream) {
+  SGS_NVTX("steepgs_reduce_bcast");
+  steepgs_status s;
+  if ((s = device_ok()) != STEEPGS_OK) return s;
+  if (n < 0 || R < 1 || R > kMaxRanks || rank < 0 || rank >= R || !peer_grad_S || ldg < n || (accumulate & ~3) ||
+      accumulate == 3)
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "bad reduce arguments");
+  int64_t need = 0;
+  steepgs_scatter_chunk(n, R, &need);
+  if (chunk != need) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "chunk must be steepgs_scatter_chunk(n, R)");
+  if (n > 0 && !partials) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "null pointer");
+  PeerPtrs gs{};
+  for (int q = 0; q < R; ++q) {
+    gs.p[q] = reinterpret_cast<float*>(peer_grad_S[q]);
+    if (!gs.p[q]) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "null peer grad_S");
+  }
+  const cudaError_t e = launch_reduce_bcast(partials, R, rank, n, chunk, gs, ldg, accumulate, (cudaStream_t)stream);
+  return e == cudaSuccess ? STEEPGS_OK : cuda_fail(e, "steepgs_reduce_bcast");
+}
+
 steepgs_status steepgs_adc_workspace_size(int64_t n, size_t* bytes) {
   if (!bytes || n < 0) return fail(STEEPGS_ERR_INVALID_ARGUMENT, "bad arguments");
   *bytes = adc_ws_bytes(n);

@@ -132,9 +132,21 @@ cudaError_t launch_l1_grad(const float* image, const float* target, int V, int64
 cudaError_t launch_render_bwd(const steepgs_splat* splats, const steepgs_binning& b, int W, int H,
                               const RasterK& rk, const float* final_T, const int32_t* n_contrib,
                               const float* dL_dimage, int64_t n, float* moments, cudaStream_t st);
+constexpr int kMaxRanks = 8;        // the fused reduce's peer set (one NVLink / NVSwitch domain)
+struct ScatterOut {                 // k_gauss_bwd output redirected to the column owners' partial buffers
+  float* peers[kMaxRanks];          // rank q's [R][20][chunk] partial buffer (device / P2P pointers)
+  int R, rank;                      // R = 0: the ordinary output into grad_S
+  int64_t chunk;
+};
+struct PeerPtrs {
+  float* p[kMaxRanks];
+};
 cudaError_t launch_gauss_bwd(const float* params, int64_t ld, int64_t n, const CamPack& cams, int V,
                              const RasterK& rk, float* moments, float* grad_S, int64_t ldg, int accumulate,
-                             const int32_t* tiles_touched, float* view_grad_stats, cudaStream_t st);
+                             const int32_t* tiles_touched, float* view_grad_stats, cudaStream_t st,
+                             const ScatterOut& sc = ScatterOut{{nullptr}, 0, 0, 0});
+cudaError_t launch_reduce_bcast(const float* partials, int R, int rank, int64_t n, int64_t chunk, const PeerPtrs& gs,
+                                int64_t ldg, int accumulate, cudaStream_t st);
 
 size_t densify_ws_bytes(int64_t n);
 cudaError_t launch_densify(float* params, int64_t ld, int64_t n, int64_t capacity, float* grad_S, int64_t ldg,

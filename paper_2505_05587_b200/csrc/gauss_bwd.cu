@@ -24,7 +24,7 @@ __global__ void __launch_bounds__(128, 5) k_gauss_bwd(const float* __restrict__ 
                                                    float* __restrict__ moments, float* __restrict__ grad_S,
                                                    int64_t ldg, int accumulate,
                                                    const int32_t* __restrict__ tiles_touched,
-                                                   float* __restrict__ vstats) {
+                                                   float* __restrict__ vstats, const ScatterOut sc) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const float p0 = params[0 * ld + i], p1 = params[1 * ld + i], p2 = params[2 * ld + i];
@@ -202,6 +202,14 @@ __global__ void __launch_bounds__(128, 5) k_gauss_bwd(const float* __restrict__ 
   // += the 6 S planes (Alg. 1: per-step gradients for the optimizer, S summed over T_split steps).
   // accumulate & 4 (SH colour, f3): k_sh_bwd has written planes 0-2 (view-direction term) and 11-13
   // (DC coefficients) for this call, so planes 0-2 are added to and 11-13 left alone.
+  if (sc.R > 0) {   // fused reduce-scatter: this rank's partial goes straight to the owner of column i
+    const int q = (int)(i / sc.chunk);
+    const int64_t j = i - (int64_t)q * sc.chunk;
+    float* dst = sc.peers[q] + (int64_t)sc.rank * 20 * sc.chunk + j;
+#pragma unroll
+    for (int k = 0; k < 20; ++k) dst[(int64_t)k * sc.chunk] = out[k];   // coalesced over i (P2P over NVLink)
+    return;
+  }
   const int mode = accumulate & 3;
   const bool shm = (accumulate & 4) != 0;
   const bool acc_g = mode == 1, acc_s = mode != 0;
@@ -218,17 +226,49 @@ __global__ void __launch_bounds__(128, 5) k_gauss_bwd(const float* __restrict__ 
   }
 }
 
+// The owner's half of the fused reduce (rank q owns columns [q chunk, q chunk + len)): sums the R
+// partials the ranks' k_gauss_bwd stored into its buffer, applies the accumulate mode of the 20
+// planes (the owner's grad_S equals every rank's: they are replicated), and stores the result into
+// every rank's grad_S (P2P stores over NVLink: the all-gather, fused into the reduction).
+__global__ void __launch_bounds__(256) k_reduce_bcast(const float* __restrict__ partials, int R, int rank,
+                                                      int64_t n, int64_t chunk, const PeerPtrs gs, int64_t ldg,
+                                                      int accumulate) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = (int64_t)rank * chunk + j;
+  if (j >= chunk || i >= n) return;
+  const int mode = accumulate & 3;
+  const float* own = gs.p[rank];
+#pragma unroll 4
+  for (int k = 0; k < 20; ++k) {
+    float v = 0.0f;
+    for (int r = 0; r < R; ++r) v += partials[((int64_t)r * 20 + k) * chunk + j];   // rank order
+    const bool acc = k < 14 ? mode == 1 : mode != 0;
+    if (acc) v = own[(int64_t)k * ldg + i] + v;
+    for (int t = 0; t < R; ++t) gs.p[t][(int64_t)k * ldg + i] = v;
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_gauss_bwd(const float* params, int64_t ld, int64_t n, const CamPack& cams, int V,
                              const RasterK& rk, float* moments, float* grad_S, int64_t ldg, int accumulate,
-                             const int32_t* tiles_touched, float* view_grad_stats, cudaStream_t st) {
+                             const int32_t* tiles_touched, float* view_grad_stats, cudaStream_t st,
+                             const ScatterOut& sc) {
   if (n == 0) return cudaSuccess;
   const unsigned blocks = (unsigned)((n + 127) / 128);
   k_gauss_bwd<<<blocks, 128, 0, st>>>(params, ld, n, cams, V, rk, moments, grad_S, ldg, accumulate, tiles_touched,
-                                      view_grad_stats);
+                                      view_grad_stats, sc);
   note_launch();
   return check_launch("k_gauss_bwd");
+}
+
+cudaError_t launch_reduce_bcast(const float* partials, int R, int rank, int64_t n, int64_t chunk, const PeerPtrs& gs,
+                                int64_t ldg, int accumulate, cudaStream_t st) {
+  const int64_t len = chunk;
+  if (len <= 0 || (int64_t)rank * chunk >= n) return cudaSuccess;
+  k_reduce_bcast<<<(unsigned)((len + 255) / 256), 256, 0, st>>>(partials, R, rank, n, chunk, gs, ldg, accumulate);
+  note_launch();
+  return check_launch("k_reduce_bcast");
 }
 
 }  // namespace sgs

@@ -201,3 +201,18 @@ def test_bench_gpus_flag_never_times_fewer_ranks():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--impl", "reference",
                         "--steps", "0", "--warmup", "0"], capture_output=True, text=True, timeout=300, env=env)
     assert r.returncode == 2 and "WORLD_SIZE" in r.stderr and r.stdout.strip() == ""
+
+
+def test_fused_reduce_owner_ranges():
+    """steepgs_scatter_chunk (host-only C-ABI call): the R owner ranges [q chunk, (q + 1) chunk) ∩ [0, n)
+    of the fused reduce-scatter cover [0, n) once, start on 32-column boundaries, and only the last
+    owner can be short or empty (tests/test_fused_collective.py runs the kernels)."""
+    from paper_2505_05587_b200 import _lib
+    for n in (0, 1, 31, 32, 3001, 1_000_000, 6_000_001):
+        for R in range(1, 9):
+            c = _lib.scatter_chunk(n, R)
+            assert c % 32 == 0 and c * R >= n and (n == 0 or c - 32 < -(-n // R))
+            covered = sum(max(0, min(n, (q + 1) * c) - q * c) for q in range(R))
+            assert covered == n
+    with pytest.raises(_lib.SteepGSError):
+        _lib.scatter_chunk(10, 9)                    # more ranks than one NVSwitch domain's peer set

@@ -74,6 +74,16 @@ struct BufferT {
   int base;                      // list position (relative to the tile start) of slot 0
   int stop;                      // 1: no more batches (forward early termination)
   int cnt;                       // forward: splats in the batch
+  int64_t gpos;                  // forward: instance index (into binning.ids) of slot 0
+};
+
+// A staged batch: instances [pos, pos + cnt) of binning.ids, list positions trel.. of a tile with
+// origin (ox, oy); stoppable: the forward may end the ring here once every consumer has terminated.
+struct BatchInfo {
+  int64_t pos;
+  int cnt, trel;
+  double ox, oy;
+  bool stoppable;
 };
 using Buffer = BufferT<kConsumers>;
 
@@ -155,31 +165,30 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // kFwd: stop early once every consumer warp has terminated (forward early exit).
 template <bool kFwd, int kProd, int kS, int kC = kConsumers, int kRaw = 4, class BatchOf>
 __device__ __forceinline__ void run_producer(SmemT<kS, kC, kRaw>& sm, const uint32_t* __restrict__ ids,
-                                             const steepgs_splat* __restrict__ vs, uint32_t first, int nb,
-                                             BatchOf batch_of, double ox, double oy, float* mom_view, float lmin,
-                                             uint8_t* __restrict__ inst_mask, int pw, int lane, int64_t n_g) {
+                                             const steepgs_splat* __restrict__ vs, int nb, BatchOf batch_of,
+                                             float* mom_view, float lmin, uint8_t* __restrict__ inst_mask, int pw,
+                                             int lane, int64_t n_g) {
   // producer warp pw of kProd stages the batch slots kk = (q kProd + pw) * 32 + lane
   constexpr int kQ = kBatch / 32 / kProd;
   uint32_t gcur[kQ], gnext[kQ];
   uint32_t mcur[kQ], mnext[kQ];   // backward: the forward's sub-block masks, prefetched with the ids
   auto load_ids = [&](int k, uint32_t* g, uint32_t* mk) {
-    int rel = 0, cnt = 0;
-    if (k < nb) batch_of(k, rel, cnt);
+    BatchInfo bi{0, 0, 0, 0.0, 0.0, false};
+    if (k < nb) bi = batch_of(k);
 #pragma unroll
     for (int q = 0; q < kQ; ++q) {
       const int kk = (q * kProd + pw) * 32 + lane;
-      g[q] = kk < cnt ? __ldg(ids + first + rel + kk) : 0u;
-      if (!kFwd) mk[q] = kk < cnt ? (uint32_t)__ldg(inst_mask + first + rel + kk) : 0u;
+      g[q] = kk < bi.cnt ? __ldg(ids + bi.pos + kk) : 0u;
+      if (!kFwd) mk[q] = kk < bi.cnt ? (uint32_t)__ldg(inst_mask + bi.pos + kk) : 0u;
     }
   };
   auto issue = [&](int k, const uint32_t* g) {
     if (k < nb) {
-      int rel, cnt;
-      batch_of(k, rel, cnt);
+      const BatchInfo bi = batch_of(k);
 #pragma unroll
       for (int q = 0; q < kQ; ++q) {
         const int kk = (q * kProd + pw) * 32 + lane;
-        if (kk < cnt) {
+        if (kk < bi.cnt) {
           const uint4* src = reinterpret_cast<const uint4*>(vs + g[q]);
 #pragma unroll
           for (int j = 0; j < (kFwd ? 4 : 3); ++j) cp_async16(&sm.raw[j][kk], src + j);   // bwd: no extents
@@ -194,11 +203,11 @@ __device__ __forceinline__ void run_producer(SmemT<kS, kC, kRaw>& sm, const uint
   // forward: once the consumers have released a stage, the composited sub-block masks of its batch
   // (cm, ORed in by the consumers) are stored as binning.inst_mask; each producer warp stores the
   // slots it stages, so no other synchronisation is needed
-  auto flush = [&](const BufferT<kC>& Bf, int base0, int cnt0) {
+  auto flush = [&](const BufferT<kC>& Bf, int64_t pos0, int cnt0) {
 #pragma unroll
     for (int q = 0; q < kQ; ++q) {
       const int kk = (q * kProd + pw) * 32 + lane;
-      if (kk < cnt0) inst_mask[first + base0 + kk] = (uint8_t)(Bf.cm[kk] & 0xFFu);
+      if (kk < cnt0) inst_mask[pos0 + kk] = (uint8_t)(Bf.cm[kk] & 0xFFu);
     }
   };
   int kend = nb, stopped = 0;
@@ -206,20 +215,21 @@ __device__ __forceinline__ void run_producer(SmemT<kS, kC, kRaw>& sm, const uint
     const int s = k % kS;
     if (k >= kS) mbar_wait(&sm.empty[s], ((k / kS) & 1) ^ 1, kSuspendNs);
     BufferT<kC>& B = sm.buf[s];
-    if (kFwd && k >= kS) flush(B, B.base, B.cnt);   // batch k - kS (read before the named barrier below)
+    if (kFwd && k >= kS) flush(B, B.gpos, B.cnt);   // batch k - kS (read before the named barrier below)
+    const BatchInfo bi = batch_of(k);
     int stop = 0;
     if (kFwd) {   // one decision per batch for all producer warps (a split decision would deadlock)
       if (kProd == 1) {
-        stop = *reinterpret_cast<volatile int*>(&sm.done_warps) == kC;
+        stop = bi.stoppable && *reinterpret_cast<volatile int*>(&sm.done_warps) == kC;
       } else {
         if (pw == 0 && lane == 0)
-          sm.stop_flag[k & 1] = *reinterpret_cast<volatile int*>(&sm.done_warps) == kC;
+          sm.stop_flag[k & 1] = bi.stoppable && *reinterpret_cast<volatile int*>(&sm.done_warps) == kC;
         asm volatile("bar.sync 1, %0;" ::"r"(32 * kProd) : "memory");
         stop = *reinterpret_cast<volatile int*>(&sm.stop_flag[k & 1]);
       }
     }
-    int rel, cnt;
-    batch_of(k, rel, cnt);
+    const int cnt = bi.cnt;
+    const double ox = bi.ox, oy = bi.oy;
     cp_async_wait_all();
     if (!stop) {
 #pragma unroll
@@ -275,9 +285,10 @@ __device__ __forceinline__ void run_producer(SmemT<kS, kC, kRaw>& sm, const uint
       }
     }
     if (pw == 0 && lane == 0) {
-      B.base = rel;
+      B.base = bi.trel;
       B.stop = stop;
       B.cnt = cnt;
+      B.gpos = bi.pos;
     }
     __syncwarp();
     mbar_arrive(&sm.full[s]);
@@ -299,7 +310,7 @@ __device__ __forceinline__ void run_producer(SmemT<kS, kC, kRaw>& sm, const uint
     for (int kb = max(0, kend - kS + stopped); kb < kend; ++kb) {
       const int s = kb % kS;
       mbar_wait(&sm.empty[s], (kb / kS) & 1, kSuspendNs);
-      flush(sm.buf[s], sm.buf[s].base, sm.buf[s].cnt);
+      flush(sm.buf[s], sm.buf[s].gpos, sm.buf[s].cnt);
     }
   }
 }
@@ -352,9 +363,12 @@ __global__ void __launch_bounds__(kThreadsFwd, 4) k_render_fwd(const steepgs_spl
 
   if (warp >= kConsumers) {  // ---------------- producers ----------------
     const int len = (int)(rg.y - rg.x);
-    run_producer<true, kFwdProducers, kFwdStages>(sm, ids, splats + (int64_t)view * n, rg.x, nb,
-                                      [len](int k, int& rel, int& cnt) { rel = k * kBatch; cnt = min(len - rel, kBatch); },
-                                      ox, oy, nullptr, __log2f(rk.alpha_min), inst_mask, warp - kConsumers, lane, n);
+    run_producer<true, kFwdProducers, kFwdStages>(
+        sm, ids, splats + (int64_t)view * n, nb,
+        [len, rg, ox, oy](int k) {
+          return BatchInfo{(int64_t)rg.x + k * kBatch, min(len - k * kBatch, kBatch), k * kBatch, ox, oy, true};
+        },
+        nullptr, __log2f(rk.alpha_min), inst_mask, warp - kConsumers, lane, n);
     return;
   }
 
@@ -628,13 +642,13 @@ __global__ void __launch_bounds__(32 * (kC2 + kProd2), kMinBlocks) k_render_bwd2
   const int wmax = __reduce_max_sync(0xffffffffu, max(lasta, lastb));
 
   if (warp >= kC2) {  // ---------------- producers: batches from the back ----------------
-    run_producer<false, kProd2, kS2, kC2, 3>(sm, ids, splats + (int64_t)view * n, rg.x, nb,
-                                        [nb, L](int k, int& rel, int& cnt) {
-                                          rel = (nb - 1 - k) * kBatch;
-                                          cnt = min(L - rel, kBatch);
-                                        },
-                                        ox, oy, moments + (int64_t)view * n * 12, __log2f(rk.alpha_min), inst_mask,
-                                        warp - kC2, lane, n);
+    run_producer<false, kProd2, kS2, kC2, 3>(
+        sm, ids, splats + (int64_t)view * n, nb,
+        [nb, L, rg, ox, oy](int k) {
+          const int rel = (nb - 1 - k) * kBatch;
+          return BatchInfo{(int64_t)rg.x + rel, min(L - rel, kBatch), rel, ox, oy, false};
+        },
+        moments + (int64_t)view * n * 12, __log2f(rk.alpha_min), inst_mask, warp - kC2, lane, n);
     return;
   }
 

@@ -168,9 +168,11 @@ __device__ void eig_min_robust(const float* S6in, bool want_vec, float& lam, flo
   if (v[big] < 0.f) { v[0] = -v[0]; v[1] = -v[1]; v[2] = -v[2]; }
 }
 
-__device__ __forceinline__ float decide_lambda(const float* S6, float eps_split) {
-  float lam, v[3];
-  eig_min_robust(S6, false, lam, v);
+// lambda_min for the split decision; with v != nullptr also the unit v_min of the same fp32 solve (the
+// fused kernel keeps it for the offspring instead of solving again: bit-identical to spawn_prepare's).
+__device__ __forceinline__ float decide_lambda(const float* S6, float eps_split, float* v = nullptr) {
+  float lam, vv[3];
+  eig_min_robust(S6, v != nullptr, lam, v != nullptr ? v : vv);
   float fro = 0.f;
 #pragma unroll
   for (int k = 0; k < 6; ++k) fro += (k == 1 || k == 2 || k == 4 ? 2.f : 1.f) * S6[k] * S6[k];
@@ -188,10 +190,16 @@ struct Spawn {
   float rest[10];   // planes 3-9 (log-scale, quaternion) and 11-13 (colour)
 };
 
+// v_min: given (the decide step already solved), else solved here from S6.
 __device__ __forceinline__ void spawn_prepare(const float* __restrict__ params, int64_t ld, int64_t i,
-                                              const float* S6, float eta, float eps_abs, Spawn& sp) {
-  float lam_unused;
-  eig_min_robust(S6, true, lam_unused, sp.v);
+                                              const float* S6, const float* vmin, float eta, float eps_abs,
+                                              Spawn& sp) {
+  if (vmin != nullptr) {
+    sp.v[0] = vmin[0]; sp.v[1] = vmin[1]; sp.v[2] = vmin[2];
+  } else {
+    float lam_unused;
+    eig_min_robust(S6, true, lam_unused, sp.v);
+  }
   // parent: p, Sigma = R diag(s^2) R^T, o
   sp.p[0] = params[0 * ld + i]; sp.p[1] = params[1 * ld + i]; sp.p[2] = params[2 * ld + i];
 #pragma unroll
@@ -216,9 +224,8 @@ __device__ __forceinline__ void spawn_prepare(const float* __restrict__ params, 
     eps = eta * sqrtf(vsv);
   }
   sp.eps = eps;
-  const double o = 1.0 / (1.0 + exp(-(double)params[10 * ld + i]));
-  const double h = 0.5 * o;                                   // Z15: w = 1/2 absorbed in opacity
-  sp.lg = (float)(log(h) - log1p(-h));
+  // Z15: w = 1/2 absorbed in opacity, logit(sigmoid(x) / 2) = -log(1 + 2 e^-x) (fp64, then rounded)
+  sp.lg = (float)(-log1p(2.0 * exp(-(double)params[10 * ld + i])));
 }
 
 __device__ __forceinline__ void spawn_commit(float* __restrict__ params, int64_t ld, float* __restrict__ grad_S,
@@ -241,7 +248,7 @@ __device__ __forceinline__ void spawn_commit(float* __restrict__ params, int64_t
 __device__ __forceinline__ void spawn(float* __restrict__ params, int64_t ld, float* __restrict__ grad_S,
                                       int64_t ldg, int64_t i, int64_t b, const float* S6, float eta, float eps_abs) {
   Spawn sp;
-  spawn_prepare(params, ld, i, S6, eta, eps_abs, sp);
+  spawn_prepare(params, ld, i, S6, nullptr, eta, eps_abs, sp);
   spawn_commit(params, ld, grad_S, ldg, i, b, sp);
 }
 
@@ -357,7 +364,9 @@ __global__ void __launch_bounds__(kThreads) k_densify_decide(float* __restrict__
   const int64_t base = (int64_t)tile * (kThreads * kIt);
   bool split[kIt];
   uint32_t pos[kIt];
-  float S6k[kFused ? kIt : 1][6];   // fused: S_bar kept for the offspring
+  // fused: v_min kept for the offspring (decide path), or S_bar to solve it (budget path)
+  float S6k[kFused && kSel ? kIt : 1][6];
+  float vk[kFused && !kSel ? kIt : 1][3];
 #pragma unroll
   for (int j = 0; j < kIt; ++j) {
     const int64_t i = base + (int64_t)j * kThreads + tid;
@@ -369,14 +378,14 @@ __global__ void __launch_bounds__(kThreads) k_densify_decide(float* __restrict__
         if (kFused && split[j]) load_sbar(grad_S, ldg, i, inv_denom, S6);
       } else {
         load_sbar(grad_S, ldg, i, inv_denom, S6);
-        const float lam = decide_lambda(S6, eps_split);
+        const float lam = decide_lambda(S6, eps_split, kFused ? vk[kFused && !kSel ? j : 0] : nullptr);
         split[j] = lam < eps_split;                   // Thm 2 / Alg. 1 P:L545 (strict, Z11)
         if (gate && split[j]) split[j] = gate_ok(grad_S, ldg, i, inv_denom, gate, eps_grad);
         if (lambda) lambda[i] = lam;
       }
-      if (kFused) {
+      if (kFused && kSel) {
 #pragma unroll
-        for (int k = 0; k < 6; ++k) S6k[kFused ? j : 0][k] = S6[k];
+        for (int k = 0; k < 6; ++k) S6k[kFused && kSel ? j : 0][k] = S6[k];
       }
     }
     const uint32_t b = __ballot_sync(0xffffffffu, split[j]);
@@ -410,7 +419,9 @@ __global__ void __launch_bounds__(kThreads) k_densify_decide(float* __restrict__
 #pragma unroll
     for (int j = 0; j < kIt; ++j) {
       const int64_t i = base + (int64_t)j * kThreads + tid;
-      if (i < n && split[j]) spawn_prepare(params, ld, i, S6k[kFused ? j : 0], eta, eps_abs, sp[kFused ? j : 0]);
+      if (i < n && split[j])
+        spawn_prepare(params, ld, i, S6k[kFused && kSel ? j : 0], kSel ? nullptr : vk[kFused && !kSel ? j : 0], eta,
+                      eps_abs, sp[kFused ? j : 0]);
     }
   }
   if (warp == 0) {

@@ -31,7 +31,15 @@ static_assert(kScanItems * (kScanThreads / 32) == 64, "the block scan gives each
 constexpr int kRadixThreads = 256;
 constexpr int kRadixItems = 12;
 constexpr int kRadixTile = kRadixThreads * kRadixItems;  // 3072
+constexpr int kRadixItemsSmall = 4;                      // small sorts (one view): 1024-item tiles
+constexpr int kRadixTileSmall = kRadixThreads * kRadixItemsSmall;
+constexpr int64_t kRadixSmallBelow = 1 << 21;  // sorts of fewer items use the small tile
 constexpr int kRadixWarps = kRadixThreads / 32;
+constexpr int kRadixLook = 4;  // predecessors per look-back round trip (16 / 32: measured slower)
+
+// Items per radix tile for a sort of up to `count` keys: 3072 fills 148 SMs x 3 blocks from ~1.4M
+// keys up; below 2M keys (a one-view step: ~0.55M visible pairs) 1024-key tiles give 3x the blocks.
+inline int radix_tile_for(int64_t count) { return count < kRadixSmallBelow ? kRadixTileSmall : kRadixTile; }
 
 constexpr uint32_t kRadFlagAgg = 1u << 30;
 constexpr uint32_t kRadFlagPre = 2u << 30;
@@ -189,15 +197,17 @@ __device__ __forceinline__ uint32_t block_excl_scan_256(uint32_t v, uint32_t* s_
   return wpre + inc - v;
 }
 
-__global__ void __launch_bounds__(kRadixThreads, 3) k_radix_pass(const uint32_t* __restrict__ keys_in,
+template <int kItems, int kMinBlocks, int kLook>
+__global__ void __launch_bounds__(kRadixThreads, kMinBlocks) k_radix_pass(const uint32_t* __restrict__ keys_in,
                                                               const uint32_t* __restrict__ vals_in,
                                                               uint32_t* __restrict__ keys_out,
                                                               uint32_t* __restrict__ vals_out, const int64_t* n_dev,
                                                               int64_t n_max, int shift,
                                                               const uint32_t* __restrict__ ghist /*[256]*/,
                                                               uint32_t* status /*[tiles][256]*/, int* tile_counter) {
-  __shared__ uint32_t s_keys[kRadixTile];
-  __shared__ uint32_t s_vals[kRadixTile];
+  constexpr int kTile = kRadixThreads * kItems;
+  __shared__ uint32_t s_keys[kTile];
+  __shared__ uint32_t s_vals[kTile];
   __shared__ uint32_t s_whist[kRadixWarps][256];
   __shared__ uint32_t s_local[256];
   __shared__ uint32_t s_dbase[256];
@@ -210,13 +220,13 @@ __global__ void __launch_bounds__(kRadixThreads, 3) k_radix_pass(const uint32_t*
   const int tile = s_tile;
   int64_t n = *n_dev;
   if (n > n_max) n = n_max;
-  const int64_t base = (int64_t)tile * kRadixTile;
+  const int64_t base = (int64_t)tile * kTile;
   if (base >= n) return;
-  const int64_t wbase = base + (int64_t)warp * (32 * kRadixItems);
-  uint32_t k[kRadixItems], v[kRadixItems];
-  uint32_t d[kRadixItems], rank[kRadixItems];
+  const int64_t wbase = base + (int64_t)warp * (32 * kItems);
+  uint32_t k[kItems], v[kItems];
+  uint32_t d[kItems], rank[kItems];
 #pragma unroll
-  for (int j = 0; j < kRadixItems; ++j) {
+  for (int j = 0; j < kItems; ++j) {
     const int64_t idx = wbase + j * 32 + lane;
     const bool ok = idx < n;
     k[j] = ok ? keys_in[idx] : 0u;
@@ -225,19 +235,19 @@ __global__ void __launch_bounds__(kRadixThreads, 3) k_radix_pass(const uint32_t*
   }
   const uint32_t lt = lanemask_lt();
   // warp-level ranking: peers by match.any; the lowest peer adds the group's size to the warp's
-  // digit counter with a returning shared atomic.  The 12 atomics are independent instructions
+  // digit counter with a returning shared atomic.  The kItems atomics are independent instructions
   // issued in item order (one warp, in-order issue), so their latencies overlap instead of
   // forming a load -> store chain through shared memory, and equal digits keep item order.
-  uint32_t peers[kRadixItems], old[kRadixItems];
+  uint32_t peers[kItems], old[kItems];
 #pragma unroll
-  for (int j = 0; j < kRadixItems; ++j) peers[j] = __match_any_sync(0xffffffffu, d[j]);
+  for (int j = 0; j < kItems; ++j) peers[j] = __match_any_sync(0xffffffffu, d[j]);
 #pragma unroll
-  for (int j = 0; j < kRadixItems; ++j) {
+  for (int j = 0; j < kItems; ++j) {
     old[j] = 0u;
     if (d[j] < 256u && (peers[j] & lt) == 0u) old[j] = atomicAdd(&s_whist[warp][d[j]], (uint32_t)__popc(peers[j]));
   }
 #pragma unroll
-  for (int j = 0; j < kRadixItems; ++j) {
+  for (int j = 0; j < kItems; ++j) {
     const uint32_t before = __shfl_sync(0xffffffffu, old[j], __ffs(peers[j]) - 1);
     rank[j] = before + __popc(peers[j] & lt);
   }
@@ -256,21 +266,22 @@ __global__ void __launch_bounds__(kRadixThreads, 3) k_radix_pass(const uint32_t*
     st_volatile(&status[dig], kRadFlagPre | tot);
   } else {
     st_volatile(&status[(int64_t)tile * 256 + dig], kRadFlagAgg | tot);
-    // look back 4 predecessors per round trip (independent loads in flight), in order
+    // look back kLook predecessors per round trip (independent loads in flight), in order
     int p = tile - 1;
     bool found = false;
     while (!found) {
-      uint32_t sv[4];
+      uint32_t sv[kLook];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) sv[q] = p - q >= 0 ? ld_volatile(&status[(int64_t)(p - q) * 256 + dig]) : kRadFlagPre;
+      for (int q = 0; q < kLook; ++q)
+        sv[q] = p - q >= 0 ? ld_volatile(&status[(int64_t)(p - q) * 256 + dig]) : kRadFlagPre;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < kLook; ++q) {
         if (found) break;
         while ((sv[q] >> 30) == 0) sv[q] = ld_volatile(&status[(int64_t)(p - q) * 256 + dig]);
         excl += sv[q] & kRadValMask;
         found = (sv[q] >> 30) == 2;
       }
-      p -= 4;
+      p -= kLook;
     }
     st_volatile(&status[(int64_t)tile * 256 + dig], kRadFlagPre | (excl + tot));
   }
@@ -280,16 +291,16 @@ __global__ void __launch_bounds__(kRadixThreads, 3) k_radix_pass(const uint32_t*
   s_dbase[dig] = gstart + excl;
   __syncthreads();
 #pragma unroll
-  for (int j = 0; j < kRadixItems; ++j) {
+  for (int j = 0; j < kItems; ++j) {
     if (d[j] < 256u) {
       const uint32_t lp = s_local[d[j]] + s_whist[warp][d[j]] + rank[j];
-      SGS_CHECK(lp < (uint32_t)kRadixTile);
+      SGS_CHECK(lp < (uint32_t)kTile);
       s_keys[lp] = k[j];
       s_vals[lp] = v[j];
     }
   }
   __syncthreads();
-  const int cnt = (int)((n - base) < kRadixTile ? (n - base) : kRadixTile);
+  const int cnt = (int)((n - base) < kTile ? (n - base) : kTile);
   for (int idx = tid; idx < cnt; idx += kRadixThreads) {
     const uint32_t kk = s_keys[idx];
     const uint32_t dd = (kk >> shift) & 255u;
@@ -442,6 +453,17 @@ __global__ void k_ranges(const uint32_t* __restrict__ keys, const int64_t* n_ins
   }
 }
 
+void launch_radix(int tile, int grid, cudaStream_t st, const uint32_t* ki, const uint32_t* vi, uint32_t* ko,
+                  uint32_t* vo, const int64_t* n_dev, int64_t n_max, int shift, const uint32_t* ghist, uint32_t* status,
+                  int* counter) {
+  if (tile == kRadixTileSmall)
+    k_radix_pass<kRadixItemsSmall, 5, kRadixLook><<<grid, kRadixThreads, 0, st>>>(ki, vi, ko, vo, n_dev, n_max, shift, ghist,
+                                                                     status, counter);
+  else
+    k_radix_pass<kRadixItems, 3, kRadixLook><<<grid, kRadixThreads, 0, st>>>(ki, vi, ko, vo, n_dev, n_max, shift, ghist, status,
+                                                                counter);
+}
+
 inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
@@ -449,7 +471,7 @@ struct Layout {
   size_t st_compact, st_dup, st_depth, st_tile, counters, hist, scalars, end;
   size_t zero_begin, zero_end;
   int64_t items;
-  int depth_tiles, inst_tiles, compact_tiles;
+  int depth_tiles, inst_tiles, compact_tiles, depth_tile, inst_tile;
 };
 
 Layout layout(int64_t n, int V, int tiles_total, int64_t max_instances) {
@@ -457,8 +479,10 @@ Layout layout(int64_t n, int V, int tiles_total, int64_t max_instances) {
   const int64_t items = (int64_t)V * n;
   L.items = items;
   L.compact_tiles = (int)((items + kScanTile - 1) / kScanTile);
-  L.depth_tiles = (int)((items + kRadixTile - 1) / kRadixTile);
-  L.inst_tiles = (int)((max_instances + kRadixTile - 1) / kRadixTile);
+  L.depth_tile = radix_tile_for(items);
+  L.inst_tile = radix_tile_for(max_instances);
+  L.depth_tiles = (int)((items + L.depth_tile - 1) / L.depth_tile);
+  L.inst_tiles = (int)((max_instances + L.inst_tile - 1) / L.inst_tile);
   size_t o = 0;
   auto take = [&](size_t bytes) { const size_t at = o; o = align_up(o + bytes); return at; };
   L.keysA = take(4 * (size_t)items);
@@ -553,9 +577,8 @@ cudaError_t launch_bin_sort(const uint32_t* depth_key, const uint32_t* tile_rect
   // depth sort: A -> B -> A -> B -> A
   uint32_t *ki = keysA, *vi = valsA, *ko = keysB, *vo = valsB;
   for (int p = 0; p < 4; ++p) {
-    k_radix_pass<<<L.depth_tiles, kRadixThreads, 0, st>>>(ki, vi, ko, vo, n_visible, L.items, 8 * p, hist + 256 * p,
-                                                          st_depth + (size_t)p * 256 * L.depth_tiles,
-                                                          counters + 1 + p);
+    launch_radix(L.depth_tile, L.depth_tiles, st, ki, vi, ko, vo, n_visible, L.items, 8 * p, hist + 256 * p,
+                 st_depth + (size_t)p * 256 * L.depth_tiles, counters + 1 + p);
     note_launch();
     if ((e = check_launch("k_radix_pass(depth)")) != cudaSuccess) return e;
     uint32_t* t;
@@ -572,9 +595,8 @@ cudaError_t launch_bin_sort(const uint32_t* depth_key, const uint32_t* tile_rect
   // tile sort: one 8-bit pass per byte of the largest tile key (C -> D -> C ...)
   uint32_t *tki = keysC, *tvi = valsC, *tko = keysD, *tvo = valsD;
   for (int p = 0; p < tile_passes; ++p) {
-    k_radix_pass<<<L.inst_tiles > 0 ? L.inst_tiles : 1, kRadixThreads, 0, st>>>(
-        tki, tvi, tko, tvo, n_inst, max_instances, 8 * p, hist + (4 + p) * 256, st_tile + (size_t)p * 256 * L.inst_tiles,
-        counters + 6 + p);
+    launch_radix(L.inst_tile, L.inst_tiles > 0 ? L.inst_tiles : 1, st, tki, tvi, tko, tvo, n_inst, max_instances, 8 * p,
+                 hist + (4 + p) * 256, st_tile + (size_t)p * 256 * L.inst_tiles, counters + 6 + p);
     note_launch();
     if ((e = check_launch("k_radix_pass(tile)")) != cudaSuccess) return e;
     uint32_t* t;

@@ -130,6 +130,9 @@ typedef struct {
                                    raster params) of the forward that filled tile_last / inst_mask;
                                    render_bwd recomputes it from its own arguments and returns
                                    STEEPGS_ERR_STALE_STATE on a mismatch (0: no forward yet) */
+  const uint32_t* tile_order;   /* [V * tiles_x * tiles_y]: set by bin_sort, the (view, tile) indices
+                                   by descending tile-list length (half-octave buckets); the raster kernels
+                                   take their tiles in this order (a scheduling permutation only) */
 } steepgs_binning;
 
 /* ---- a1: projection (Eq. eqn:sigma_2D + footnote P:L135-139).  Per (view, Gaussian):

@@ -55,7 +55,7 @@ class Binning(C.Structure):
                 ("inst_mask", C.c_void_p),
                 ("max_instances", C.c_int64),
                 ("tiles_x", C.c_int32), ("tiles_y", C.c_int32), ("V", C.c_int32),
-                ("generation", C.c_uint64), ("fwd_token", C.c_uint64)]
+                ("generation", C.c_uint64), ("fwd_token", C.c_uint64), ("tile_order", C.c_void_p)]
 
 
 SPLAT_BYTES = 64

@@ -119,7 +119,7 @@ static steepgs_status check_token(const steepgs_binning* b, const steepgs_splat*
 }
 
 static steepgs_status check_binning(const steepgs_binning* b, int32_t V, const steepgs_camera* cams) {
-  if (!b || !b->ids || !b->ranges || !b->n_instances || !b->tile_last || !b->inst_mask)
+  if (!b || !b->ids || !b->ranges || !b->n_instances || !b->tile_last || !b->inst_mask || !b->tile_order)
     return fail(STEEPGS_ERR_INVALID_ARGUMENT, "binning null");
   const int tx = (cams[0].width + kTile - 1) / kTile, ty = (cams[0].height + kTile - 1) / kTile;
   if (b->V != V || b->tiles_x != tx || b->tiles_y != ty)

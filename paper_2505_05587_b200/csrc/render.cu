@@ -333,6 +333,23 @@ __device__ __forceinline__ int build_list(const BufferT<kC>& B, uint8_t* __restr
   return total;
 }
 
+// The (tile, view) a block renders: entry blockIdx of binning.tile_order (bin_sort's order, longest
+// lists first; view << 20 | tile).
+// kReload: an opaque second load (the forward's epilogue re-reads its tile instead of keeping tile and
+// view live through the blend loop, whose 56 registers would otherwise rematerialise ~16 instructions
+// per four entries).
+template <bool kReload = false>
+__device__ __forceinline__ void tile_of_block(const uint32_t* __restrict__ order, int& tile, int& view) {
+  const uint32_t* p = order + (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+  uint32_t t;
+  if (kReload)
+    asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(t) : "l"(p));
+  else
+    t = __ldg(p);
+  view = (int)(t >> 20);
+  tile = (int)(t & 0xFFFFFu);
+}
+
 template <bool kCount>   // kCount: also count composited / evaluated pairs (the roofline's units)
 __global__ void __launch_bounds__(kThreadsFwd, 4) k_render_fwd(const steepgs_splat* __restrict__ splats,
                                                          const uint32_t* __restrict__ ids,
@@ -343,11 +360,13 @@ __global__ void __launch_bounds__(kThreadsFwd, 4) k_render_fwd(const steepgs_spl
                                                          uint32_t* __restrict__ tile_last,
                                                          uint8_t* __restrict__ inst_mask,
                                                          unsigned long long* __restrict__ pair_counts,
-                                                         const L1Fused l1) {
+                                                         const L1Fused l1, const uint32_t* __restrict__ order) {
   extern __shared__ __align__(16) unsigned char fsmem[];
   SmemFwd& sm = *reinterpret_cast<SmemFwd*>(fsmem);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int tile = blockIdx.x, view = blockIdx.y;
+  int tile, view;
+  tile_of_block(order, tile, view);
+  SGS_CHECK(tile < tiles_per_view && view < (int)gridDim.y);   // tile_order entries are (view, tile)
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const double ox = (double)(tx * kTile), oy = (double)(ty * kTile);
   const uint2 rg = ranges[(int64_t)view * tiles_per_view + tile];
@@ -471,18 +490,22 @@ __global__ void __launch_bounds__(kThreadsFwd, 4) k_render_fwd(const steepgs_spl
     }
     mbar_arrive(&sm.empty[s]);
   }
+  // epilogue: the tile is re-read from tile_order (not kept live through the blend loop)
+  int etile, eview;
+  tile_of_block<true>(order, etile, eview);
+  const int epx = (etile % tiles_x) * kTile + lx, epy = (etile / tiles_x) * kTile + ly;
   float ad = 0.0f;   // fused l1: this pixel's sum of |C - C_hat| over the channels
-  if (inside) {
+  if (epx < W && epy < H) {
     const int64_t HW = (int64_t)W * H;
-    const int64_t pix = (int64_t)py * W + px;
-    float* img = image + (int64_t)view * 3 * HW;
+    const int64_t pix = (int64_t)epy * W + epx;
+    float* img = image + (int64_t)eview * 3 * HW;
     const float out[3] = {__fmaf_rn(T, rk.bg[0], C0), __fmaf_rn(T, rk.bg[1], C1), __fmaf_rn(T, rk.bg[2], C2)};
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) img[ch * HW + pix] = out[ch];
-    final_T[(int64_t)view * HW + pix] = T;
-    n_contrib[(int64_t)view * HW + pix] = last;
+    final_T[(int64_t)eview * HW + pix] = T;
+    n_contrib[(int64_t)eview * HW + pix] = last;
     if (l1.target) {   // a4 fused: dL/dC = scale sign(C - C_hat), the same expression as k_l1_grad
-      const int64_t o = (int64_t)view * 3 * HW + pix;
+      const int64_t o = (int64_t)eview * 3 * HW + pix;
 #pragma unroll
       for (int ch = 0; ch < 3; ++ch) {
         const float r = out[ch] - __ldg(l1.target + o + ch * HW);
@@ -494,11 +517,11 @@ __global__ void __launch_bounds__(kThreadsFwd, 4) k_render_fwd(const steepgs_spl
   if (l1.loss) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ad += __shfl_xor_sync(0xffffffffu, ad, o);
-    if (lane == 0) atomicAdd(l1.loss + view, ad * l1.scale);
+    if (lane == 0) atomicAdd(l1.loss + eview, ad * l1.scale);
   }
   {
     const int wl = __reduce_max_sync(0xffffffffu, last);   // the tile's composited prefix, for the backward
-    if (lane == 0 && wl > 0) atomicMax(tile_last + (int64_t)view * tiles_per_view + tile, (uint32_t)wl);
+    if (lane == 0 && wl > 0) atomicMax(tile_last + (int64_t)eview * tiles_per_view + etile, (uint32_t)wl);
   }
   if (kCount) {
     unsigned long long c = (unsigned long long)ncomp, e = (unsigned long long)neval;
@@ -596,13 +619,16 @@ __global__ void __launch_bounds__(32 * (kC2 + kProd2), kMinBlocks) k_render_bwd2
                                                           const float* __restrict__ dL_dimage,
                                                           const uint32_t* __restrict__ tile_last,
                                                           uint8_t* __restrict__ inst_mask,
-                                                          float* __restrict__ moments) {
+                                                          float* __restrict__ moments,
+                                                          const uint32_t* __restrict__ order) {
   extern __shared__ __align__(16) unsigned char dsmem[];
   using Smem2 = Smem2T<kS2>;
   Smem2& sm = *reinterpret_cast<Smem2*>(dsmem);
   BwdScratch2<kChunk2>& sc = *reinterpret_cast<BwdScratch2<kChunk2>*>(dsmem + ((sizeof(Smem2) + 15) & ~size_t(15)));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int tile = blockIdx.x, view = blockIdx.y;
+  int tile, view;
+  tile_of_block(order, tile, view);
+  SGS_CHECK(tile < tiles_per_view && view < (int)gridDim.y);   // tile_order entries are (view, tile)
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const double ox = (double)(tx * kTile), oy = (double)(ty * kTile);
   const uint2 rg = ranges[(int64_t)view * tiles_per_view + tile];
@@ -866,11 +892,11 @@ cudaError_t launch_render_fwd(const steepgs_splat* splats, int64_t n, const stee
   if (pair_counts)
     k_render_fwd<true><<<grid, kThreadsFwd, sizeof(SmemFwd), st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
                                                   b.tiles_x, tpv, rk, image, final_T, n_contrib, b.tile_last, b.inst_mask,
-                                                  reinterpret_cast<unsigned long long*>(pair_counts), l1);
+                                                  reinterpret_cast<unsigned long long*>(pair_counts), l1, b.tile_order);
   else
     k_render_fwd<false><<<grid, kThreadsFwd, sizeof(SmemFwd), st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
                                                    b.tiles_x, tpv, rk, image, final_T, n_contrib, b.tile_last, b.inst_mask, nullptr,
-                                                   l1);
+                                                   l1, b.tile_order);
   note_launch();
   return check_launch("k_render_fwd");
 }
@@ -899,14 +925,16 @@ cudaError_t launch_render_bwd(const steepgs_splat* splats, const steepgs_binning
   // fastest of the measured configurations (round 2)
   constexpr int kCh = 8, kS2 = kStages;
   using Kern = void (*)(const steepgs_splat*, const uint32_t*, const uint2*, int64_t, int, int, int, int, const RasterK,
-                        const float*, const int32_t*, const float*, const uint32_t*, uint8_t*, float*);
+                        const float*, const int32_t*, const float*, const uint32_t*, uint8_t*, float*,
+                        const uint32_t*);
   const Kern kern = k_render_bwd2<kCh, 1, 4, kS2>;
   const size_t smem2 = ((sizeof(Smem2T<kS2>) + 15) & ~size_t(15)) + sizeof(BwdScratch2<kCh>);
   static std::atomic<uint64_t> done2{0};
   const cudaError_t e2 = allow_dynamic_smem(done2, (const void*)kern, smem2, true);
   if (e2 == cudaSuccess)
     kern<<<grid, 32 * (kC2 + 1), smem2, st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H, b.tiles_x,
-                                             tpv, rk, final_T, n_contrib, dL_dimage, b.tile_last, b.inst_mask, moments);
+                                             tpv, rk, final_T, n_contrib, dL_dimage, b.tile_last, b.inst_mask, moments,
+                                             b.tile_order);
   if (e2 != cudaSuccess) return e2;
   note_launch();
   return check_launch("k_render_bwd");

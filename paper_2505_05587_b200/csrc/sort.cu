@@ -464,10 +464,88 @@ void launch_radix(int tile, int grid, cudaStream_t st, const uint32_t* ki, const
                                                                 counter);
 }
 
+// 6. tile order for the raster kernels: (view, tile) indices by descending list length, in half-octave
+// buckets (one block; the order inside a bucket is whatever the shared atomics give — it only decides
+// which block runs which tile, never a result).  Long tiles start first, so the last wave is short.
+__global__ void __launch_bounds__(1024) k_tile_order(const uint2* __restrict__ ranges, int m, int tiles_per_view,
+                                                     int by_length, uint32_t* __restrict__ order) {
+    constexpr uint32_t kB = 65;
+  __shared__ uint32_t s_cnt[kB];
+  const int tid = threadIdx.x;
+  if (!by_length) {
+    for (int i = tid; i < m; i += 1024) {
+      const uint32_t v = (uint32_t)(i / tiles_per_view), t = (uint32_t)(i - (int)v * tiles_per_view);
+      order[i] = (v << 20) | t;
+    }
+    return;
+  }
+  if (tid < (int)kB) s_cnt[tid] = 0u;
+  __syncthreads();
+  auto key = [&](int i) {
+    const uint2 r = ranges[i];
+    const uint32_t len = r.y - r.x;
+    if (len == 0u) return 64u;   // half-octave buckets, 0 for the longest lists
+    const uint32_t c = (uint32_t)__clz(len), p = 31u - c;
+    const uint32_t nb = p > 0u ? (len >> (p - 1u)) & 1u : 0u;
+    return 2u * c + 1u - nb;
+  };
+  auto pack = [&](int i) {
+    const uint32_t v = (uint32_t)(i / tiles_per_view), t = (uint32_t)(i - (int)v * tiles_per_view);
+    return (v << 20) | t;   // (view, tile) packed: no division in the kernels
+  };
+  constexpr int kPer = 24;   // keys per thread kept in registers (all loads issued together)
+  if (m <= 1024 * kPer) {
+    uint32_t kk[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) kk[j] = j * 1024 + tid < m ? key(j * 1024 + tid) : kB;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j)
+      if (kk[j] < kB) atomicAdd(&s_cnt[kk[j]], 1u);
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t run = 0;
+      for (uint32_t k = 0; k < kB; ++k) {
+        const uint32_t c = s_cnt[k];
+        s_cnt[k] = run;
+        run += c;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kPer; ++j)
+      if (kk[j] < kB) order[atomicAdd(&s_cnt[kk[j]], 1u)] = pack(j * 1024 + tid);
+    return;
+  }
+  for (int i = tid; i < m; i += 1024) atomicAdd(&s_cnt[key(i)], 1u);
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t run = 0;
+    for (uint32_t k = 0; k < kB; ++k) {
+      const uint32_t c = s_cnt[k];
+      s_cnt[k] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < m; i += 1024) order[atomicAdd(&s_cnt[key(i)], 1u)] = pack(i);
+}
+
+cudaError_t launch_tile_order(const uint2* ranges, int tiles_total, int tiles_per_view, uint32_t* order,
+                              cudaStream_t st) {
+#ifdef SGS_NO_TILE_ORDER
+  const bool identity = true;
+#else
+  const bool identity = false;
+#endif
+  k_tile_order<<<1, 1024, 0, st>>>(ranges, tiles_total, tiles_per_view, identity ? 0 : 1, order);
+  note_launch();
+  return check_launch("k_tile_order");
+}
+
 inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
-  size_t keysA, valsA, keysB, valsB, recs, keysC, valsC, keysD, valsD, ranges, tile_last, inst_mask;
+  size_t keysA, valsA, keysB, valsB, recs, keysC, valsC, keysD, valsD, ranges, tile_last, inst_mask, order;
   size_t st_compact, st_dup, st_depth, st_tile, counters, hist, scalars, end;
   size_t zero_begin, zero_end;
   int64_t items;
@@ -496,6 +574,7 @@ Layout layout(int64_t n, int V, int tiles_total, int64_t max_instances) {
   L.valsD = take(4 * (size_t)max_instances);
   L.ranges = take(8 * (size_t)tiles_total);
   L.inst_mask = take((size_t)max_instances);
+  L.order = take(4 * (size_t)tiles_total);
   L.zero_begin = o;
   L.tile_last = take(4 * (size_t)tiles_total);
   L.st_compact = take(8 * (size_t)L.compact_tiles);
@@ -523,6 +602,7 @@ cudaError_t launch_bin_sort(const uint32_t* depth_key, const uint32_t* tile_rect
   const int tiles_total = tiles_per_view * V;
   const Layout L = layout(n, V, tiles_total, max_instances);
   if (ws_bytes < L.end) return cudaErrorInvalidValue;
+  if (tiles_per_view >= (1 << 20) || V >= (1 << 12)) return cudaErrorInvalidValue;   // tile_order packing
   char* w = static_cast<char*>(ws);
   auto U32 = [&](size_t off) { return reinterpret_cast<uint32_t*>(w + off); };
   uint32_t* keysA = U32(L.keysA);
@@ -557,11 +637,13 @@ cudaError_t launch_bin_sort(const uint32_t* depth_key, const uint32_t* tile_rect
   out->overflow = overflow;
   out->tile_last = U32(L.tile_last);
   out->inst_mask = reinterpret_cast<uint8_t*>(w + L.inst_mask);
+  out->tile_order = reinterpret_cast<const uint32_t*>(w + L.order);
   out->max_instances = max_instances;
   out->tiles_x = tiles_x;
   out->tiles_y = tiles_y;
   out->V = V;
-  if (L.items == 0) return cudaSuccess;
+  if (L.items == 0) return launch_tile_order(reinterpret_cast<const uint2*>(ranges), tiles_total, tiles_per_view,
+                                             U32(L.order), st);
 
   k_count_visible<<<L.compact_tiles, kScanThreads, 0, st>>>(tiles_touched, L.items, st_compact);
   note_launch();
@@ -608,7 +690,8 @@ cudaError_t launch_bin_sort(const uint32_t* depth_key, const uint32_t* tile_rect
   if (rb > 148 * 8) rb = 148 * 8;  // grid-stride: the true I is only known on the device
   k_ranges<<<(unsigned)(rb > 0 ? rb : 1), 256, 0, st>>>(tki, n_inst, max_instances, ranges);
   note_launch();
-  return check_launch("k_ranges");
+  if ((e = check_launch("k_ranges")) != cudaSuccess) return e;
+  return launch_tile_order(ranges, tiles_total, tiles_per_view, U32(L.order), st);
 }
 
 }  // namespace sgs

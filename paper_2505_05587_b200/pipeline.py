@@ -185,7 +185,7 @@ class Rasterizer:
 
     # ---- host-side readers (tests / diagnostics; they synchronise) ----
     def binning_arrays(self):
-        """(ids[I], ranges[V*tiles][2], I, overflow) copied to host."""
+        """(ids[I], ranges[V*tiles][2], I, overflow, tile_order[V*tiles]) copied to host."""
         b = self.binning
         base = self.sort_ws.data_ptr()
         def view(ptr_, nbytes, dtype):
@@ -197,7 +197,8 @@ class Rasterizer:
         tiles = b.tiles_x * b.tiles_y * b.V
         ids = view(b.ids, 4 * min(I, self.max_instances), torch.int32).cpu()
         ranges = view(b.ranges, 8 * tiles, torch.int32).view(tiles, 2).cpu()
-        return dict(ids=ids, ranges=ranges, n_instances=I, overflow=ovf, n_visible=nv)
+        order = view(b.tile_order, 4 * tiles, torch.int32).cpu()   # view << 20 | tile
+        return dict(ids=ids, ranges=ranges, n_instances=I, overflow=ovf, n_visible=nv, tile_order=order)
 
 
 # ---------------------------------------------------------------------------------------------

@@ -79,6 +79,22 @@ def test_project_and_binning_bitexact_c1(orc, model):
     assert b["overflow"] == 0 and b["n_instances"] == ids.size
     assert np.array_equal(b["ids"].numpy().astype(np.int64), ids)
     assert np.array_equal((b["ranges"][:, 1] - b["ranges"][:, 0]).numpy(), counts)
+    _check_tile_order(b, counts, cams)
+
+
+def _check_tile_order(b, counts, cams):
+    """binning.tile_order: a permutation of the (view, tile) indices (view << 20 | tile) whose list
+    lengths are non-increasing in half-octave buckets (a scheduling order only)."""
+    t = b["tile_order"].numpy().astype(np.int64)
+    tpv = counts.size // len(cams)
+    flat = (t >> 20) * tpv + (t & 0xFFFFF)
+    assert ((t & 0xFFFFF) < tpv).all() and np.array_equal(np.sort(flat), np.arange(counts.size))
+    L = counts[flat].astype(np.int64)
+    nz = L > 0
+    c = np.where(nz, 31 - np.floor(np.log2(np.maximum(L, 1))).astype(np.int64), 32)
+    nb = np.where(nz & (c < 31), (L >> np.maximum(30 - c, 0)) & 1, 0)
+    key = np.where(nz, 2 * c + 1 - nb, 64)
+    assert (np.diff(key) >= 0).all()
 
 
 def test_project_and_binning_bitexact_full_size_c2(orc):
@@ -96,6 +112,7 @@ def test_project_and_binning_bitexact_full_size_c2(orc):
     assert b["n_visible"] == sum(int(d["visible"].sum()) for d in decs)
     assert np.array_equal(b["ids"].numpy().astype(np.int64), ids)
     assert np.array_equal((b["ranges"][:, 1] - b["ranges"][:, 0]).numpy(), counts)
+    _check_tile_order(b, counts, cams)
 
 
 def expected_binning_fast(decs, W, H, T=16):

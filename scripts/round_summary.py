@@ -45,7 +45,7 @@ for r in m["rows"]:
              f"{r.get('smsp__inst_executed.sum', 0) / 1e6:.0f}M | {top} |")
 pairs = b["roofline"]["units_per_launch"]["contributing_pairs"]
 lanes = {r["kernel"]: r["smsp__inst_executed.sum"] * 32 / pairs for r in m["rows"] if r["kernel"] in ("k_render_fwd", "k_render_bwd2")}
-L.append(f"\nbin_sort stage (count + scan + compact + 4 depth passes + duplicate + 2 tile passes + ranges): {st['bin_sort']['ms']} ms.\n")
+L.append(f"\nbin_sort stage (count + scan + compact + 4 depth passes + duplicate + 2 tile passes + ranges + tile order): {st['bin_sort']['ms']} ms.\n")
 L.append("Lane slots per contributing pair (warp instructions × 32 / contributing pairs): "
          + ", ".join(f"{k} {v:.0f}" for k, v in lanes.items()) + " (round 1: k_render_bwd 195, k_render_fwd 99).  "
          "Round-2 changes and dead ends with their numbers: DESIGN.md §10 (round 2).\n")

@@ -65,6 +65,13 @@ def test_affine_negative_depth_keys_bitexact(orc):
     vis = d["visible"].astype(bool)
     assert (np.asarray(p[2], np.float64)[vis] + 0.5 < 0).any()    # some negative depths are visible
     assert np.array_equal(g["key"][0][vis], d["key"][vis])
+    # the instance order through the sort: keys on both sides of the sign flip (all four radix passes)
+    from test_gpu_parity import expected_binning
+    ids, counts = expected_binning([d], 48, 40)
+    b = rz.binning_arrays()
+    assert b["overflow"] == 0 and b["n_instances"] == ids.size
+    assert np.array_equal(b["ids"].numpy().astype(np.int64), ids)
+    assert np.array_equal((b["ranges"][:, 1] - b["ranges"][:, 0]).numpy(), counts)
     o = orc.render(p, cam, DEFAULT)
     img = rz.image.cpu().numpy()[0]
     ok = (np.abs(img - o["image"]) <= 1e-4 * np.abs(o["image"]) + 1e-6) | (o["amb_px"][None] != 0)

@@ -63,6 +63,39 @@ inline RasterK raster_k(const steepgs_raster_params* rp) {
 void note_launch(int k = 1);
 cudaError_t check_launch(const char* what);
 
+// Programmatic dependent launch (sm_90+): a kernel launched with launch_pdl may be scheduled while the
+// previous kernel of the stream drains its last wave; it executes pdl_wait() (griddepcontrol.wait:
+// the previous grid complete and its writes visible) before it reads anything that kernel wrote, and
+// pdl_trigger() lets the next kernel's blocks be scheduled once every block of this grid has started.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// kPdl: with the programmatic-stream-serialization attribute (SGS_NO_PDL builds leave it off everywhere).
+template <bool kPdl, typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  if (kPdl) {
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+#ifndef SGS_NO_PDL
+  return launch_k<true>(kern, grid, block, smem, st, args...);
+#else
+  return launch_k<false>(kern, grid, block, smem, st, args...);
+#endif
+}
+
 // ---- launchers (one per .cu) ----
 cudaError_t launch_project(const float* params, int64_t ld, int64_t n, const float* sh_rest, int64_t ld_sh,
                            int sh_degree, const CamPack& cams, int V, const RasterK& rk, steepgs_splat* splats,

@@ -354,6 +354,8 @@ __global__ void __launch_bounds__(kThreads) k_densify_decide(float* __restrict__
                                                              float* __restrict__ lambda, uint64_t* status,
                                                              int* tile_counter, int64_t* n_split,
                                                              int32_t* __restrict__ dstatus) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int s_tile;
   __shared__ uint32_t s_cnt[kIt][kThreads / 32];
   __shared__ uint64_t s_excl;
@@ -602,9 +604,9 @@ cudaError_t launch_densify(float* params, int64_t ld, int64_t n, int64_t capacit
                               : (n + kTileItems - 1) / kTileItems;
   if (n > 0) {
 #define SGS_DECIDE(F, IT, SEL)                                                                              \
-  k_densify_decide<F, IT, SEL><<<(unsigned)tiles, kThreads, 0, st>>>(                                      \
-      params, ld, grad_S, ldg, n, inv_denom, dp.eps_split, dp.eta, dp.eps_abs, dp.gate, dp.eps_grad, sel,  \
-      mask, dest, budget ? nullptr : lambda, st_decide, counter, n_split, status)
+  launch_pdl(k_densify_decide<F, IT, SEL>, dim3((unsigned)tiles), dim3(kThreads), 0, st, params, ld, grad_S, ldg, n,  \
+             inv_denom, dp.eps_split, dp.eta, dp.eps_abs, dp.gate, dp.eps_grad, (const uint8_t*)sel, mask, dest,   \
+             budget ? nullptr : lambda, st_decide, counter, n_split, status)
     if (fused && budget) SGS_DECIDE(true, kItemsFused, true);
     else if (fused) SGS_DECIDE(true, kItemsFused, false);
     else if (budget) SGS_DECIDE(false, kItems, true);

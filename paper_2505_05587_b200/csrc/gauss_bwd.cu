@@ -25,6 +25,8 @@ __global__ void __launch_bounds__(128, 5) k_gauss_bwd(const float* __restrict__ 
                                                    int64_t ldg, int accumulate,
                                                    const int32_t* __restrict__ tiles_touched,
                                                    float* __restrict__ vstats, const ScatterOut sc) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const float p0 = params[0 * ld + i], p1 = params[1 * ld + i], p2 = params[2 * ld + i];
@@ -256,8 +258,10 @@ cudaError_t launch_gauss_bwd(const float* params, int64_t ld, int64_t n, const C
                              const ScatterOut& sc) {
   if (n == 0) return cudaSuccess;
   const unsigned blocks = (unsigned)((n + 127) / 128);
-  k_gauss_bwd<<<blocks, 128, 0, st>>>(params, ld, n, cams, V, rk, moments, grad_S, ldg, accumulate, tiles_touched,
-                                      view_grad_stats, sc);
+  // launched without the programmatic-dependent attribute: with it, the whole-step graph measured
+  // 60-70 us slower per C2 step (its blocks parked on griddepcontrol.wait during render_bwd's tail)
+  launch_k<false>(k_gauss_bwd, dim3(blocks), dim3(128), 0, st, params, ld, n, cams, V, rk, moments, grad_S, ldg, accumulate,
+             tiles_touched, view_grad_stats, sc);
   note_launch();
   return check_launch("k_gauss_bwd");
 }

@@ -46,6 +46,8 @@ __global__ void __launch_bounds__(256, kSH < 0 ? 4 : 1) k_project(const float* _
                                                  steepgs_splat* __restrict__ splats,
                                                  uint32_t* __restrict__ depth_key, uint2* __restrict__ tile_rect,
                                                  int32_t* __restrict__ tiles_touched) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const float p0 = params[0 * ld + i], p1 = params[1 * ld + i], p2 = params[2 * ld + i];
@@ -254,8 +256,8 @@ cudaError_t launch_project(const float* params, int64_t ld, int64_t n, const flo
   const int threads = 256;
   const unsigned blocks = (unsigned)((n + threads - 1) / threads);
 #define SGS_PROJECT(D)                                                                                     \
-  k_project<D><<<blocks, threads, 0, st>>>(params, ld, n, sh_rest, ld_sh, cams, V, rk, splats, depth_key, \
-                                           reinterpret_cast<uint2*>(tile_rect), tiles_touched)
+  launch_pdl(k_project<D>, dim3(blocks), dim3(threads), 0, st, params, ld, n, sh_rest, ld_sh, cams, V, rk, splats, \
+             depth_key, reinterpret_cast<uint2*>(tile_rect), tiles_touched)
   switch (sh_degree) {
     case 0: SGS_PROJECT(0); break;
     case 1: SGS_PROJECT(1); break;

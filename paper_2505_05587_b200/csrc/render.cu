@@ -361,6 +361,8 @@ __global__ void __launch_bounds__(kThreadsFwd, 4) k_render_fwd(const steepgs_spl
                                                          uint8_t* __restrict__ inst_mask,
                                                          unsigned long long* __restrict__ pair_counts,
                                                          const L1Fused l1, const uint32_t* __restrict__ order) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) unsigned char fsmem[];
   SmemFwd& sm = *reinterpret_cast<SmemFwd*>(fsmem);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -621,6 +623,8 @@ __global__ void __launch_bounds__(32 * (kC2 + kProd2), kMinBlocks) k_render_bwd2
                                                           uint8_t* __restrict__ inst_mask,
                                                           float* __restrict__ moments,
                                                           const uint32_t* __restrict__ order) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) unsigned char dsmem[];
   using Smem2 = Smem2T<kS2>;
   Smem2& sm = *reinterpret_cast<Smem2*>(dsmem);
@@ -889,14 +893,9 @@ cudaError_t launch_render_fwd(const steepgs_splat* splats, int64_t n, const stee
     if (e == cudaSuccess) e = allow_dynamic_smem(done, (const void*)k_render_fwd<false>, sizeof(SmemFwd), true);
     if (e != cudaSuccess) return e;
   }
-  if (pair_counts)
-    k_render_fwd<true><<<grid, kThreadsFwd, sizeof(SmemFwd), st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
-                                                  b.tiles_x, tpv, rk, image, final_T, n_contrib, b.tile_last, b.inst_mask,
-                                                  reinterpret_cast<unsigned long long*>(pair_counts), l1, b.tile_order);
-  else
-    k_render_fwd<false><<<grid, kThreadsFwd, sizeof(SmemFwd), st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H,
-                                                   b.tiles_x, tpv, rk, image, final_T, n_contrib, b.tile_last, b.inst_mask, nullptr,
-                                                   l1, b.tile_order);
+  launch_pdl(pair_counts ? k_render_fwd<true> : k_render_fwd<false>, grid, dim3(kThreadsFwd), sizeof(SmemFwd), st, splats,
+             b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H, b.tiles_x, tpv, rk, image, final_T, n_contrib,
+             b.tile_last, b.inst_mask, reinterpret_cast<unsigned long long*>(pair_counts), l1, b.tile_order);
   note_launch();
   return check_launch("k_render_fwd");
 }
@@ -932,9 +931,9 @@ cudaError_t launch_render_bwd(const steepgs_splat* splats, const steepgs_binning
   static std::atomic<uint64_t> done2{0};
   const cudaError_t e2 = allow_dynamic_smem(done2, (const void*)kern, smem2, true);
   if (e2 == cudaSuccess)
-    kern<<<grid, 32 * (kC2 + 1), smem2, st>>>(splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W, H, b.tiles_x,
-                                             tpv, rk, final_T, n_contrib, dL_dimage, b.tile_last, b.inst_mask, moments,
-                                             b.tile_order);
+    launch_pdl(kern, grid, dim3(32 * (kC2 + 1)), smem2, st, splats, b.ids, reinterpret_cast<const uint2*>(b.ranges), n, W,
+               H, b.tiles_x, tpv, rk, final_T, n_contrib, dL_dimage, (const uint32_t*)b.tile_last, b.inst_mask, moments,
+               b.tile_order);
   if (e2 != cudaSuccess) return e2;
   note_launch();
   return check_launch("k_render_bwd");

@@ -161,6 +161,8 @@ __global__ void __launch_bounds__(256) k_copy_offspring(float* __restrict__ arr,
 __global__ void __launch_bounds__(256) k_copy_planes(float* __restrict__ dst, int64_t ld_dst,
                                                      const float* __restrict__ src, int64_t ld_src, int64_t n,
                                                      int count, bool vec) {
+  pdl_wait();
+  pdl_trigger();
   const int k = blockIdx.y;
   float* d = dst + k * ld_dst;
   const float* s = src + k * ld_src;
@@ -186,8 +188,8 @@ cudaError_t launch_copy_planes(float* dst, int64_t ld_dst, const float* src, int
   const bool vec = (ld_dst % 4 == 0) && (ld_src % 4 == 0) && ((uintptr_t)d % 16 == 0) && ((uintptr_t)s % 16 == 0);
   int64_t blocks = (n / (vec ? 4 : 1) + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  k_copy_planes<<<dim3((unsigned)(blocks > 0 ? blocks : 1), (unsigned)count), 256, 0, st>>>(d, ld_dst, s, ld_src, n,
-                                                                                            count, vec);
+  launch_pdl(k_copy_planes, dim3((unsigned)(blocks > 0 ? blocks : 1), (unsigned)count), dim3(256), 0, st, d, ld_dst,
+             s, ld_src, n, count, vec);
   note_launch();
   return check_launch("k_copy_planes");
 }

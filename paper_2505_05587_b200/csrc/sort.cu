@@ -53,6 +53,8 @@ constexpr uint32_t kRadValMask = (1u << 30) - 1;
 // the first wave's tiles, whose aggregates appear together but whose prefixes resolve one by one).
 __global__ void __launch_bounds__(kScanThreads) k_count_visible(const int32_t* __restrict__ tiles_touched,
                                                                 int64_t total, uint64_t* __restrict__ tile_count) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ uint32_t s_w[kScanThreads / 32];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t base = (int64_t)blockIdx.x * kScanTile;
@@ -76,6 +78,8 @@ __global__ void __launch_bounds__(kScanThreads) k_count_visible(const int32_t* _
 
 // In-place exclusive scan of the tile counts (one block of 1024 threads, contiguous chunks).
 __global__ void __launch_bounds__(1024) k_scan_tile_counts(uint64_t* __restrict__ v, int m, int64_t* total_out) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ uint64_t s_w[32];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int per = (m + 1023) / 1024;
@@ -116,6 +120,8 @@ __global__ void __launch_bounds__(kScanThreads) k_compact(const uint32_t* __rest
                                                           int64_t total, uint32_t* __restrict__ keys_out,
                                                           uint32_t* __restrict__ vals_out, uint4* __restrict__ recs,
                                                           const uint64_t* __restrict__ tile_offset, uint32_t* hist4) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ uint32_t s_cnt[kScanItems][kScanThreads / 32];
   __shared__ uint32_t s_hist[4][256];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -205,6 +211,8 @@ __global__ void __launch_bounds__(kRadixThreads, kMinBlocks) k_radix_pass(const 
                                                               int64_t n_max, int shift,
                                                               const uint32_t* __restrict__ ghist /*[256]*/,
                                                               uint32_t* status /*[tiles][256]*/, int* tile_counter) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int kTile = kRadixThreads * kItems;
   __shared__ uint32_t s_keys[kTile];
   __shared__ uint32_t s_vals[kTile];
@@ -321,6 +329,8 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_duplicate(const uint32_t* _
                                                             uint32_t* __restrict__ inst_ids, uint64_t* status,
                                                             int* tile_counter, uint32_t* hist2, int64_t* n_inst,
                                                             int32_t* overflow, int tile_passes) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int s_tile;
   __shared__ uint32_t s_cnt[kScanItems][kScanThreads / 32];
   __shared__ uint32_t s_hist[3][256];
@@ -427,6 +437,8 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_duplicate(const uint32_t* _
 // from the adjacent lanes or one extra load).
 __global__ void k_ranges(const uint32_t* __restrict__ keys, const int64_t* n_inst, int64_t max_instances,
                          uint2* __restrict__ ranges) {
+  pdl_wait();
+  pdl_trigger();
   int64_t I = *n_inst;
   if (I > max_instances) I = max_instances;
   const int64_t groups = (I + 3) / 4;
@@ -453,15 +465,15 @@ __global__ void k_ranges(const uint32_t* __restrict__ keys, const int64_t* n_ins
   }
 }
 
-void launch_radix(int tile, int grid, cudaStream_t st, const uint32_t* ki, const uint32_t* vi, uint32_t* ko,
+cudaError_t launch_radix(int tile, int grid, cudaStream_t st, const uint32_t* ki, const uint32_t* vi, uint32_t* ko,
                   uint32_t* vo, const int64_t* n_dev, int64_t n_max, int shift, const uint32_t* ghist, uint32_t* status,
                   int* counter) {
   if (tile == kRadixTileSmall)
-    k_radix_pass<kRadixItemsSmall, 5, kRadixLook><<<grid, kRadixThreads, 0, st>>>(ki, vi, ko, vo, n_dev, n_max, shift, ghist,
-                                                                     status, counter);
+    return launch_pdl(k_radix_pass<kRadixItemsSmall, 5, kRadixLook>, dim3(grid), dim3(kRadixThreads), 0, st, ki, vi, ko,
+                      vo, n_dev, n_max, shift, ghist, status, counter);
   else
-    k_radix_pass<kRadixItems, 3, kRadixLook><<<grid, kRadixThreads, 0, st>>>(ki, vi, ko, vo, n_dev, n_max, shift, ghist, status,
-                                                                counter);
+    return launch_pdl(k_radix_pass<kRadixItems, 3, kRadixLook>, dim3(grid), dim3(kRadixThreads), 0, st, ki, vi, ko, vo,
+                      n_dev, n_max, shift, ghist, status, counter);
 }
 
 // 6. tile order for the raster kernels: (view, tile) indices by descending list length, in half-octave
@@ -469,6 +481,8 @@ void launch_radix(int tile, int grid, cudaStream_t st, const uint32_t* ki, const
 // which block runs which tile, never a result).  Long tiles start first, so the last wave is short.
 __global__ void __launch_bounds__(1024) k_tile_order(const uint2* __restrict__ ranges, int m, int tiles_per_view,
                                                      int by_length, uint32_t* __restrict__ order) {
+  pdl_wait();
+  pdl_trigger();
     constexpr uint32_t kB = 65;
   __shared__ uint32_t s_cnt[kB];
   const int tid = threadIdx.x;
@@ -537,8 +551,10 @@ cudaError_t launch_tile_order(const uint2* ranges, int tiles_total, int tiles_pe
 #else
   const bool identity = false;
 #endif
-  k_tile_order<<<1, 1024, 0, st>>>(ranges, tiles_total, tiles_per_view, identity ? 0 : 1, order);
+  const cudaError_t e = launch_pdl(k_tile_order, dim3(1), dim3(1024), 0, st, ranges, tiles_total, tiles_per_view,
+                                   identity ? 0 : 1, order);
   note_launch();
+  if (e != cudaSuccess) return e;
   return check_launch("k_tile_order");
 }
 
@@ -645,23 +661,27 @@ cudaError_t launch_bin_sort(const uint32_t* depth_key, const uint32_t* tile_rect
   if (L.items == 0) return launch_tile_order(reinterpret_cast<const uint2*>(ranges), tiles_total, tiles_per_view,
                                              U32(L.order), st);
 
-  k_count_visible<<<L.compact_tiles, kScanThreads, 0, st>>>(tiles_touched, L.items, st_compact);
+  e = launch_pdl(k_count_visible, dim3(L.compact_tiles), dim3(kScanThreads), 0, st, tiles_touched, L.items, st_compact);
   note_launch();
+  if (e != cudaSuccess) return e;
   if ((e = check_launch("k_count_visible")) != cudaSuccess) return e;
-  k_scan_tile_counts<<<1, 1024, 0, st>>>(st_compact, L.compact_tiles, n_visible);
+  e = launch_pdl(k_scan_tile_counts, dim3(1), dim3(1024), 0, st, st_compact, L.compact_tiles, n_visible);
   note_launch();
+  if (e != cudaSuccess) return e;
   if ((e = check_launch("k_scan_tile_counts")) != cudaSuccess) return e;
-  k_compact<<<L.compact_tiles, kScanThreads, 0, st>>>(depth_key, reinterpret_cast<const uint2*>(tile_rect),
-                                                      tiles_touched, n, L.items, keysA, valsA, recs, st_compact,
-                                                      hist);
+  e = launch_pdl(k_compact, dim3(L.compact_tiles), dim3(kScanThreads), 0, st, depth_key,
+                 reinterpret_cast<const uint2*>(tile_rect), tiles_touched, n, L.items, keysA, valsA, recs,
+                 (const uint64_t*)st_compact, hist);
   note_launch();
+  if (e != cudaSuccess) return e;
   if ((e = check_launch("k_compact")) != cudaSuccess) return e;
   // depth sort: A -> B -> A -> B -> A
   uint32_t *ki = keysA, *vi = valsA, *ko = keysB, *vo = valsB;
   for (int p = 0; p < 4; ++p) {
-    launch_radix(L.depth_tile, L.depth_tiles, st, ki, vi, ko, vo, n_visible, L.items, 8 * p, hist + 256 * p,
-                 st_depth + (size_t)p * 256 * L.depth_tiles, counters + 1 + p);
+    e = launch_radix(L.depth_tile, L.depth_tiles, st, ki, vi, ko, vo, n_visible, L.items, 8 * p, hist + 256 * p,
+                     st_depth + (size_t)p * 256 * L.depth_tiles, counters + 1 + p);
     note_launch();
+    if (e != cudaSuccess) return e;
     if ((e = check_launch("k_radix_pass(depth)")) != cudaSuccess) return e;
     uint32_t* t;
     t = ki; ki = ko; ko = t;
@@ -669,17 +689,19 @@ cudaError_t launch_bin_sort(const uint32_t* depth_key, const uint32_t* tile_rect
   }
   // sorted slots now in vi (== valsA)
   const int tile_passes = tiles_total <= 256 ? 1 : (tiles_total <= 65536 ? 2 : 3);
-  k_duplicate<<<L.compact_tiles, kScanThreads, 0, st>>>(vi, recs, n_visible, tiles_x, tiles_per_view,
-                                                        max_instances, keysC, valsC, st_dup, counters + 5,
-                                                        hist + 4 * 256, n_inst, overflow, tile_passes);
+  e = launch_pdl(k_duplicate, dim3(L.compact_tiles), dim3(kScanThreads), 0, st, vi, recs, n_visible, tiles_x,
+                 tiles_per_view, max_instances, keysC, valsC, st_dup, counters + 5, hist + 4 * 256, n_inst, overflow,
+                 tile_passes);
   note_launch();
+  if (e != cudaSuccess) return e;
   if ((e = check_launch("k_duplicate")) != cudaSuccess) return e;
   // tile sort: one 8-bit pass per byte of the largest tile key (C -> D -> C ...)
   uint32_t *tki = keysC, *tvi = valsC, *tko = keysD, *tvo = valsD;
   for (int p = 0; p < tile_passes; ++p) {
-    launch_radix(L.inst_tile, L.inst_tiles > 0 ? L.inst_tiles : 1, st, tki, tvi, tko, tvo, n_inst, max_instances, 8 * p,
-                 hist + (4 + p) * 256, st_tile + (size_t)p * 256 * L.inst_tiles, counters + 6 + p);
+    e = launch_radix(L.inst_tile, L.inst_tiles > 0 ? L.inst_tiles : 1, st, tki, tvi, tko, tvo, n_inst, max_instances,
+                     8 * p, hist + (4 + p) * 256, st_tile + (size_t)p * 256 * L.inst_tiles, counters + 6 + p);
     note_launch();
+    if (e != cudaSuccess) return e;
     if ((e = check_launch("k_radix_pass(tile)")) != cudaSuccess) return e;
     uint32_t* t;
     t = tki; tki = tko; tko = t;
@@ -688,8 +710,10 @@ cudaError_t launch_bin_sort(const uint32_t* depth_key, const uint32_t* tile_rect
   out->ids = tvi;
   int64_t rb = (max_instances + 1023) / 1024;
   if (rb > 148 * 8) rb = 148 * 8;  // grid-stride: the true I is only known on the device
-  k_ranges<<<(unsigned)(rb > 0 ? rb : 1), 256, 0, st>>>(tki, n_inst, max_instances, ranges);
+  e = launch_pdl(k_ranges, dim3((unsigned)(rb > 0 ? rb : 1)), dim3(256), 0, st, (const uint32_t*)tki,
+                 (const int64_t*)n_inst, max_instances, ranges);
   note_launch();
+  if (e != cudaSuccess) return e;
   if ((e = check_launch("k_ranges")) != cudaSuccess) return e;
   return launch_tile_order(ranges, tiles_total, tiles_per_view, U32(L.order), st);
 }

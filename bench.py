@@ -202,6 +202,11 @@ def run_reference(args):
     return 0
 
 
+def to_u8(a):
+    """Synthetic float targets in [0, 1] as 8-bit images (round to nearest)."""
+    return np.ascontiguousarray(np.clip(np.rint(a * 255.0), 0, 255).astype(np.uint8))
+
+
 def relaunch_under_torchrun(args) -> int:
     """`--gpus N` (N > 1) without a torchrun environment: launch N ranks on this node ourselves
     (the driver's own command is torchrun; this makes a plain `python bench.py --gpus N` do the same
@@ -239,7 +244,8 @@ def run_v1(args, cfg, p_np, pristine, dev, stream, views=16):
     params = pristine.clone()
     grad_S = torch.zeros(20, cap, dtype=torch.float32, device=dev)
     cams = synth.cameras_for(cfg, views=views)
-    tg = torch.from_numpy(np.ascontiguousarray(synth.targets_for(cfg, views=views))).to(dev)
+    tg_np = np.ascontiguousarray(synth.targets_for(cfg, views=views))
+    tg = torch.from_numpy(to_u8(tg_np) if args.targets == "u8" else tg_np).to(dev)
     rz = Rasterizer(cap, 1, cfg.width, cfg.height, max_instances=int(3.0 * n), device=dev)
 
     def stages(v):
@@ -327,6 +333,8 @@ def main():
     ap.add_argument("--h2d-at", default="after_sort", choices=["start", "after_sort"],
                     help="e2e: start step k+1's target copy with step k, or after step k's bin_sort (the copy's "
                          "DMA writes then overlap the ALU-bound render kernels, not the L2-resident sort)")
+    ap.add_argument("--targets", default="u8", choices=["u8", "f32"],
+                    help="target image format uploaded per step (u8: 8-bit, decoded * (1/255) on the device)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-v1", action="store_true", help="skip the 1-view-per-step line (SURVEY §8(d1))")
     ap.add_argument("--collective", default="nccl", choices=["nccl", "fused"],
@@ -362,6 +370,9 @@ def main():
     cams = all_cams[rank::ws]                                 # view sharding
     tg_all = synth.targets_for(cfg, views=V * ws)
     tg_np = np.ascontiguousarray(tg_all[rank::ws])
+    u8 = args.targets == "u8" and args.ssim is None        # the SSIM loss kernels take float targets
+    if u8:   # the targets as 8-bit images (a photograph's format), decoded * (1/255) by the fused l1 epilogue
+        tg_np = to_u8(tg_np)
 
     pristine = torch.zeros(14, cap, dtype=torch.float32, device=dev)
     pristine[:, :n] = torch.from_numpy(p_np).to(dev)
@@ -729,7 +740,8 @@ def main():
             tt = torch.tensor([et], device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             et = float(tt.item())
-        e2e = dict(value=et / args.steps / (V * ws), unit=UNIT, h2d_bytes_per_step=int(tg_host.numel() * 4),
+        e2e = dict(value=et / args.steps / (V * ws), unit=UNIT,
+                   h2d_bytes_per_step=int(tg_host.numel() * tg_host.element_size()),
                    d2h_bytes_per_step=int(loss_host[0].numel() * 4 + 8),
                    note="H2D of step k+1 overlapped with step k on a copy stream (issued "
                         + ("with step k" if args.h2d_at == "start" else "after step k's bin_sort")
@@ -763,6 +775,8 @@ def main():
                         l2="no flush: per-step working set (params 56 MB + splats 48 B x V x n + sort/moment "
                            "buffers) exceeds the 126 MB L2",
                         scene="synthetic surface-like (SURVEY 8(d1)), procedural targets",
+                        targets=("uint8 [V][3][H][W] (8-bit images), decoded as float(t) * (1/255) in the fused l1 "
+                                 "epilogue" if u8 else "float32 [V][3][H][W]"),
                         launch=launch_mode[0]),
             roofline=roofline,
             path_hbm=dict(alg_bytes_per_step=int(path_bytes), ms=round(path_ms, 4),

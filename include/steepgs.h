@@ -187,6 +187,15 @@ steepgs_status steepgs_render_fwd_l1(const steepgs_splat* splats, int64_t n, ste
                                      float* image, float* final_T, int32_t* n_contrib, const float* target,
                                      float scale, float* dL_dimage, float* loss, int64_t* pair_counts, void* stream);
 
+/* The same with 8-bit targets (the photographs' own format: a quarter of the bytes to upload per step):
+ * target [V][3][H][W] uint8, decoded as C_hat = (float)target * (1.0f / 255.0f) (fp32, one rounding), then the
+ * expressions above; results bit-identical to steepgs_render_fwd_l1 on the decoded float targets. */
+steepgs_status steepgs_render_fwd_l1_u8(const steepgs_splat* splats, int64_t n, steepgs_binning* b /*[host]*/,
+                                        const steepgs_camera* cams, int32_t V, const steepgs_raster_params* rp,
+                                        float* image, float* final_T, int32_t* n_contrib, const uint8_t* target,
+                                        float scale, float* dL_dimage, float* loss, int64_t* pair_counts,
+                                        void* stream);
+
 /* ---- a4: l1 loss gradient helper (Eq. eqn:loss; C9, Z8):
  * dL_dimage = scale * sign(image - target) (sign(0) = 0) over V*count elements; if loss != NULL,
  * loss[v] (device, [V]) = scale * sum |image - target| over view v. */

@@ -76,6 +76,7 @@ def lib():
             "steepgs_bin_sort": [P, P, P, I64, P, I32, P, P, C.c_size_t, I64, P, P],
             "steepgs_render_fwd": [P, I64, P, P, I32, P, P, P, P, P, P],
             "steepgs_render_fwd_l1": [P, I64, P, P, I32, P, P, P, P, P, F, P, P, P, P],
+            "steepgs_render_fwd_l1_u8": [P, I64, P, P, I32, P, P, P, P, P, F, P, P, P, P],
             "steepgs_render_bwd_moments": [P, I64, P, P, I32, P, P, P, P, P, P],
             "steepgs_gauss_bwd_split": [P, I64, I64, P, I32, P, P, P, I64, I32, P, P, P],
             "steepgs_copy_planes": [P, I64, P, I64, I64, I32, I32, P],
@@ -197,6 +198,14 @@ def render_fwd_l1(splats, n, binning, cams_arr, V, rp, image, final_T, n_contrib
            lib().steepgs_render_fwd_l1(ptr(splats), n, C.byref(binning), cams_arr, V, C.byref(rp), ptr(image),
                                        ptr(final_T), ptr(n_contrib), ptr(target), float(scale), ptr(dL), ptr(loss),
                                        ptr(pair_counts), stream_ptr(stream)))
+
+
+def render_fwd_l1_u8(splats, n, binning, cams_arr, V, rp, image, final_T, n_contrib, target, scale, dL, loss=None,
+                     pair_counts=None, stream=None):
+    _check("steepgs_render_fwd_l1_u8",
+           lib().steepgs_render_fwd_l1_u8(ptr(splats), n, C.byref(binning), cams_arr, V, C.byref(rp), ptr(image),
+                                          ptr(final_T), ptr(n_contrib), ptr(target), float(scale), ptr(dL), ptr(loss),
+                                          ptr(pair_counts), stream_ptr(stream)))
 
 
 def render_bwd_moments(splats, n, binning, cams_arr, V, rp, final_T, n_contrib, dL, moments, stream=None):

@@ -384,10 +384,31 @@ steepgs_status steepgs_render_fwd_l1(const steepgs_splat* splats, int64_t n, ste
   if ((s = check_binning(b, V, cams)) != STEEPGS_OK) return s;
   if (n < 0 || !image || !final_T || !n_contrib || !target || !dL_dimage || (n > 0 && !splats))
     return fail(STEEPGS_ERR_INVALID_ARGUMENT, "null pointer");
-  const L1Fused l1{target, dL_dimage, loss, scale};
+  const L1Fused l1{target, dL_dimage, loss, scale, nullptr};
   const cudaError_t e = launch_render_fwd(splats, n, *b, cams[0].width, cams[0].height, raster_k(rp), image, final_T,
                                           n_contrib, pair_counts, (cudaStream_t)stream, l1);
   if (e != cudaSuccess) return cuda_fail(e, "steepgs_render_fwd_l1");
+  b->fwd_token = fwd_token(b, splats, n, cams, V, rp);
+  return STEEPGS_OK;
+}
+
+steepgs_status steepgs_render_fwd_l1_u8(const steepgs_splat* splats, int64_t n, steepgs_binning* b,
+                                        const steepgs_camera* cams, int32_t V, const steepgs_raster_params* rp,
+                                        float* image, float* final_T, int32_t* n_contrib, const uint8_t* target,
+                                        float scale, float* dL_dimage, float* loss, int64_t* pair_counts,
+                                        void* stream) {
+  SGS_NVTX("steepgs_render_fwd_l1_u8");
+  steepgs_status s;
+  if ((s = device_ok()) != STEEPGS_OK) return s;
+  if ((s = check_views(cams, V, nullptr)) != STEEPGS_OK) return s;
+  if ((s = check_raster(rp)) != STEEPGS_OK) return s;
+  if ((s = check_binning(b, V, cams)) != STEEPGS_OK) return s;
+  if (n < 0 || !image || !final_T || !n_contrib || !target || !dL_dimage || (n > 0 && !splats))
+    return fail(STEEPGS_ERR_INVALID_ARGUMENT, "null pointer");
+  const L1Fused l1{nullptr, dL_dimage, loss, scale, target};
+  const cudaError_t e = launch_render_fwd(splats, n, *b, cams[0].width, cams[0].height, raster_k(rp), image, final_T,
+                                          n_contrib, pair_counts, (cudaStream_t)stream, l1);
+  if (e != cudaSuccess) return cuda_fail(e, "steepgs_render_fwd_l1_u8");
   b->fwd_token = fwd_token(b, splats, n, cams, V, rp);
   return STEEPGS_OK;
 }

@@ -152,14 +152,15 @@ cudaError_t launch_bin_sort(const uint32_t* depth_key, const uint32_t* tile_rect
                             int64_t max_instances, steepgs_binning* out, cudaStream_t st);
 
 struct L1Fused {                    // the a4 l1 gradient fused into the forward's epilogue (optional)
-  const float* target;              // [V][3][H][W] or nullptr (off)
+  const float* target;              // [V][3][H][W] or nullptr
   float* dL;                        // [V][3][H][W]
   float* loss;                      // [V] or nullptr
   float scale;
+  const uint8_t* target_u8;         // [V][3][H][W] 8-bit targets (decoded / 255) instead; both null: off
 };
 cudaError_t launch_render_fwd(const steepgs_splat* splats, int64_t n, const steepgs_binning& b, int W, int H,
                               const RasterK& rk, float* image, float* final_T, int32_t* n_contrib,
-                              int64_t* pair_counts, cudaStream_t st, const L1Fused& l1 = L1Fused{nullptr, nullptr, nullptr, 0.f});
+                              int64_t* pair_counts, cudaStream_t st, const L1Fused& l1 = L1Fused{nullptr, nullptr, nullptr, 0.f, nullptr});
 cudaError_t launch_l1_grad(const float* image, const float* target, int V, int64_t count, float scale,
                            float* dL, float* loss, cudaStream_t st);
 cudaError_t launch_render_bwd(const steepgs_splat* splats, const steepgs_binning& b, int W, int H,

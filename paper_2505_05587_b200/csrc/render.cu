@@ -511,11 +511,13 @@ __global__ void __launch_bounds__(kThreadsFwd, 4) k_render_fwd(const steepgs_spl
     for (int ch = 0; ch < 3; ++ch) img[ch * HW + pix] = out[ch];
     final_T[(int64_t)eview * HW + pix] = T;
     n_contrib[(int64_t)eview * HW + pix] = last;
-    if (l1.target) {   // a4 fused: dL/dC = scale sign(C - C_hat), the same expression as k_l1_grad
+    if (l1.target || l1.target_u8) {   // a4 fused: dL/dC = scale sign(C - C_hat), the same expression as k_l1_grad
       const int64_t o = (int64_t)eview * 3 * HW + pix;
 #pragma unroll
       for (int ch = 0; ch < 3; ++ch) {
-        const float r = out[ch] - __ldg(l1.target + o + ch * HW);
+        const float tv = l1.target ? __ldg(l1.target + o + ch * HW)
+                                   : __fmul_rn((float)__ldg(l1.target_u8 + o + ch * HW), 1.0f / 255.0f);
+        const float r = out[ch] - tv;
         l1.dL[o + ch * HW] = r > 0.0f ? l1.scale : (r < 0.0f ? -l1.scale : 0.0f);
         ad += fabsf(r);
       }

@@ -115,10 +115,14 @@ class Rasterizer:
     def render_fwd_l1(self, targets: torch.Tensor, scale: float | None = None, with_loss: bool = True,
                       pair_counts: torch.Tensor | None = None):
         """a3 + a4 fused: the forward writes dL/dimage = scale sign(image - target) (default scale
-        1/(3HW), the per-view mean) and the per-view loss in its epilogue."""
+        1/(3HW), the per-view mean) and the per-view loss in its epilogue.  targets: float32, or uint8
+        (decoded as target * (1/255) in fp32 on the device)."""
         sc = 1.0 / (3 * self._HW) if scale is None else scale
-        _lib.render_fwd_l1(self.splats, self.n, self.binning, self.cams_arr, self.V, self.rp, self.image, self.final_T,
-                           self.n_contrib, targets, sc, self.dL, self.loss if with_loss else None, pair_counts)
+        fn = _lib.render_fwd_l1_u8 if targets.dtype == torch.uint8 else _lib.render_fwd_l1   # 8-bit: decoded * (1/255)
+        if targets.dtype not in (torch.uint8, torch.float32) or not targets.is_contiguous():
+            raise TypeError("targets: contiguous float32 or uint8 [V][3][H][W]")
+        fn(self.splats, self.n, self.binning, self.cams_arr, self.V, self.rp, self.image, self.final_T, self.n_contrib,
+           targets, sc, self.dL, self.loss if with_loss else None, pair_counts)
 
     # ---- a4 ----
     def l1_grad(self, targets: torch.Tensor, with_loss: bool = True):

@@ -652,3 +652,24 @@ def test_render_fwd_l1_fused_equals_separate():
     torch.cuda.synchronize()
     assert torch.equal(rz.image, img0) and torch.equal(rz.dL, dl0)
     assert torch.allclose(rz.loss, loss0, rtol=1e-5, atol=0)
+
+
+def test_render_fwd_l1_u8_equals_float_targets():
+    """steepgs_render_fwd_l1_u8: 8-bit targets decoded as fp32 target * (1/255) on the device — image,
+    dL/dimage and the per-view loss bit-identical to steepgs_render_fwd_l1 on the decoded targets
+    (which the test above ties to render_fwd + l1_grad, and the l1 parity test to the oracle)."""
+    from gpu_run import run_forward, to_dev
+    cfg = synth.CONFIGS["C2"]
+    p = synth.scene_for(cfg)
+    cams = synth.cameras_for(cfg, views=2)
+    t8 = np.clip(np.rint(synth.targets_for(cfg, views=2) * 255.0), 0, 255).astype(np.uint8)
+    dec = t8.astype(np.float32) * (np.float32(1.0) / np.float32(255.0))   # fp32, as on the device
+    rz, pt = run_forward(p, cams, DEFAULT)
+    rz.render_fwd_l1(to_dev(dec))
+    img0, dl0, loss0 = rz.image.clone(), rz.dL.clone(), rz.loss.clone()
+    assert (dl0 != 0).any() and (dl0 == 0).sum() < dl0.numel()
+    rz.dL.zero_(); rz.loss.fill_(7.0)
+    rz.render_fwd_l1(torch.from_numpy(t8).cuda())
+    torch.cuda.synchronize()
+    assert torch.equal(rz.image, img0) and torch.equal(rz.dL, dl0)
+    assert torch.allclose(rz.loss, loss0, rtol=1e-5, atol=0)   # per-warp atomics: summation order

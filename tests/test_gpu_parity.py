@@ -636,6 +636,59 @@ def test_stage_graph_replay_equals_eager():
     assert ref["G"][14:20, :n].abs().sum().item() > 0
 
 
+def test_whole_step_graph_replay_equals_eager():
+    """bench.py's timed launch: the whole step (project .. densify) captured as ONE CUDA graph, so the
+    programmatic-dependent launches chain across stages inside the graph.  Binning, image, T and
+    dL/dimage bit-identical to the eager step; grads + S equal up to the backward's float atomics;
+    densify's split count within a few Gaussians (lambda_min decided on those S) and its mask / dest
+    consistent."""
+    from gpu_run import to_dev
+    from paper_2505_05587_b200.pipeline import Rasterizer
+    cfg = synth.CONFIGS["C2"]
+    n, V = cfg.n, 2
+    p = synth.scene_for(cfg)
+    cams = synth.cameras_for(cfg, views=V)
+    tg = torch.from_numpy(np.clip(np.rint(synth.targets_for(cfg, views=V) * 255.0), 0, 255).astype(np.uint8)).cuda()
+    cap = 2 * n
+    P0 = torch.zeros(14, cap, device="cuda"); P0[:, :n] = to_dev(p)
+    P = P0.clone()
+    G = torch.zeros(20, cap, device="cuda")
+    rz = Rasterizer(cap, V, cfg.width, cfg.height, max_instances=int(3.0 * V * n))
+
+    def step():
+        rz.project(P, n, cams)
+        rz.bin_sort()
+        rz.render_fwd_l1(tg)
+        rz.render_bwd_moments()
+        rz.gauss_bwd(P, G, accumulate=0)
+        rz.densify(P, G, n, cap, denom=float(V), want_lambda=False)
+
+    step()
+    torch.cuda.synchronize()
+    b = rz.binning_arrays()
+    ns0 = int(rz.n_split.item()) if torch.is_tensor(rz.n_split) else int(rz.n_split)
+    ref = dict(ids=b["ids"].clone(), ranges=b["ranges"].clone(), image=rz.image.clone(), T=rz.final_T.clone(),
+               dL=rz.dL.clone())
+    P.copy_(P0)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    P.copy_(P0)
+    for t in (rz.image, rz.final_T, rz.dL, G):
+        t.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    b = rz.binning_arrays()
+    assert torch.equal(b["ids"], ref["ids"]) and torch.equal(b["ranges"], ref["ranges"])
+    for k, t in (("image", rz.image), ("T", rz.final_T), ("dL", rz.dL)):
+        assert torch.equal(t, ref[k]), k
+    ns1 = int(rz.n_split.item()) if torch.is_tensor(rz.n_split) else int(rz.n_split)
+    assert ns0 > 0 and abs(ns1 - ns0) <= 8, (ns0, ns1)
+    mask = rz.split_mask[:n].cpu().numpy().astype(bool)
+    dest = rz.dest_index[:n].cpu().numpy()
+    assert int(mask.sum()) == ns1 and np.array_equal(np.sort(dest[mask]), n + np.arange(ns1))
+
+
 def test_render_fwd_l1_fused_equals_separate():
     """a3 + a4 fused (steepgs_render_fwd_l1): image, dL/dimage bit-identical to render_fwd + l1_grad, the
     per-view loss equal up to summation order."""

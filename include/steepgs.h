@@ -13,7 +13,10 @@
  *    thread-local error string, a launch counter and the binning generation counter.
  *  - `stream` is a cudaStream_t passed as void*.  Calls are asynchronous on `stream` and never
  *    synchronise it, except steepgs_densify_host_count (documented below).  Nothing is
- *    read back to the host, so every call can be captured in a CUDA graph.
+ *    read back to the host, so every call can be captured in a CUDA graph.  Most kernels are
+ *    launched with programmatic dependent launch (they may be scheduled while the preceding kernel
+ *    of the stream drains, and wait for it to complete before reading anything), so stream order
+ *    holds exactly as for plain launches.
  *  - Reentrant; concurrent calls must not share output or workspace buffers.
  *  - Errors are returned as steepgs_status; no exception crosses the ABI.  Asynchronous device
  *    faults surface as STEEPGS_ERR_CUDA at a later call.  steepgs_last_error() gives detail.

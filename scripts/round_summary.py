@@ -49,5 +49,10 @@ L.append(f"\nbin_sort stage (count + scan + compact + 4 depth passes + duplicate
 L.append("Lane slots per contributing pair (warp instructions × 32 / contributing pairs): "
          + ", ".join(f"{k} {v:.0f}" for k, v in lanes.items()) + " (round 1: k_render_bwd 195, k_render_fwd 99).  "
          "Round-2 changes and dead ends with their numbers: DESIGN.md §10 (round 2).\n")
+L.append("DRAM traffic of the raster kernels against their algorithmic bytes: the longest-list-first tile "
+         "order (binning.tile_order) keeps all views' splat records and moments in flight, so render_fwd / "
+         "render_bwd2 read about 1.6x what the raster (view-major) order read (462 / 654 MB per step); both "
+         "kernels are issue-bound and the order is faster overall — the per-view alternative that restores "
+         "the traffic is measured in DESIGN.md §5 (k_tile_order).\n")
 open(os.path.join(P, f"r0{N}_summary.md"), "w").write("\n".join(L) + "\n")
 print("\n".join(L))

@@ -130,10 +130,20 @@ __global__ void __launch_bounds__(kScanThreads) k_compact(const uint32_t* __rest
   const int64_t base = (int64_t)tile * kScanTile;
   bool flag[kScanItems];
   uint32_t pos_in_warp[kScanItems];
+  uint32_t key[kScanItems];
+  uint2 rect[kScanItems];
+  int32_t tt[kScanItems];
 #pragma unroll
   for (int j = 0; j < kScanItems; ++j) {
     const int64_t idx = base + (int64_t)j * kScanThreads + tid;
-    flag[j] = idx < total && tiles_touched[idx] > 0;
+    tt[j] = idx < total ? tiles_touched[idx] : 0;
+  }
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    const int64_t idx = base + (int64_t)j * kScanThreads + tid;
+    flag[j] = tt[j] > 0;
+    // the visible items' key and rect are loaded here, so their latency overlaps the block scan
+    if (flag[j]) { key[j] = depth_key[idx]; rect[j] = tile_rect[idx]; }
     const uint32_t b = __ballot_sync(0xffffffffu, flag[j]);
     pos_in_warp[j] = __popc(b & lanemask_lt());
     if (lane == 0) s_cnt[j][warp] = __popc(b);
@@ -152,14 +162,6 @@ __global__ void __launch_bounds__(kScanThreads) k_compact(const uint32_t* __rest
     const uint32_t ex = inc - sum;
     s_cnt[(2 * lane) / nw][(2 * lane) % nw] = ex;
     s_cnt[(2 * lane + 1) / nw][(2 * lane + 1) % nw] = ex + a;
-  }
-  uint32_t key[kScanItems];
-  uint2 rect[kScanItems];
-  int32_t tt[kScanItems];
-#pragma unroll
-  for (int j = 0; j < kScanItems; ++j) {
-    const int64_t idx = base + (int64_t)j * kScanThreads + tid;
-    if (flag[j]) { key[j] = depth_key[idx]; rect[j] = tile_rect[idx]; tt[j] = tiles_touched[idx]; }
   }
   __syncthreads();
   const uint64_t bex = tile_offset[tile];

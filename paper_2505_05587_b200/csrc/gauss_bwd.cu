@@ -1,7 +1,7 @@
 // gauss_bwd.cu — a6: per-Gaussian backward and the splitting matrix (App. C.4
 // P:L1133-1157; Alg. 1).
 //
-// From the 9 per-(view, Gaussian) moments of w = dL/dsigma * sigma accumulated by k_render_bwd
+// From the 9 per-(view, Gaussian) moments of w = dL/dsigma * sigma accumulated by k_render_bwd2
 //   m0 = sum w,  m1 = sum w d,  M = sum w d d^T,  cg = sum alpha T dL/dC     (d = x - Pi(p))
 // and sigma = o exp(-1/2 d^T Q d):
 //   dL/dmu = Q m1,  dL/dPi(Sigma) = 1/2 Q M Q,  dL/do = m0 / o,  dL/dc = cg,

@@ -2,7 +2,8 @@
 // (Eq. eqn:loss), a5 backward replay with the splitting-matrix moments (Thm 1 P:L232,
 // §4.3).
 //
-// Work decomposition (B200): one block per 16x16 tile and view, warp-specialised:
+// Work decomposition (B200): one block per 16x16 tile and view, the block -> tile map taken from
+// binning.tile_order (bin_sort: longest tile lists first, so the last wave is short), warp-specialised:
 //   * one producer warp (forward and backward) stages the tile's depth-ordered splats
 //     into a ring of shared-memory buffers (5 in the forward, 3 in the backward) of kBatch splats:
 //     the 64-B records are copied with cp.async (ids prefetched two batches ahead), made
@@ -943,7 +944,7 @@ cudaError_t launch_render_bwd(const steepgs_splat* splats, const steepgs_binning
                b.tile_order);
   if (e2 != cudaSuccess) return e2;
   note_launch();
-  return check_launch("k_render_bwd");
+  return check_launch("k_render_bwd2");
 }
 
 }  // namespace sgs

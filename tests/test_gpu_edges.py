@@ -190,3 +190,28 @@ def test_backward_rejects_stale_binning():
     bwd()                                                                   # the matching forward: accepted
     torch.cuda.synchronize()
     assert float(rz.moments.abs().sum()) > 0
+
+
+def test_tile_order_many_tiles():
+    """binning.tile_order when V * tiles exceeds the order kernel's register-cached path (24,576
+    tiles: here C5's 8160 tiles x 4 views): a permutation of (view << 20 | tile) with list lengths
+    non-increasing in half-octave buckets."""
+    from gpu_run import run_forward
+    cfg = synth.CONFIGS["C5"]
+    p = synth.scene_for(cfg)[:, :200_000]
+    cams = synth.cameras_for(cfg, views=4)
+    rz, _ = run_forward(np.ascontiguousarray(p), cams, DEFAULT)
+    b = rz.binning_arrays()
+    t = b["tile_order"].numpy().astype(np.int64)
+    counts = (b["ranges"][:, 1] - b["ranges"][:, 0]).numpy().astype(np.int64)
+    tpv = counts.size // 4
+    assert counts.size > 24576
+    flat = (t >> 20) * tpv + (t & 0xFFFFF)
+    assert ((t & 0xFFFFF) < tpv).all() and np.array_equal(np.sort(flat), np.arange(counts.size))
+    L = counts[flat]
+    nz = L > 0
+    c = np.where(nz, 31 - np.floor(np.log2(np.maximum(L, 1))).astype(np.int64), 32)
+    nb = np.where(nz & (c < 31), (L >> np.maximum(30 - c, 0)) & 1, 0)
+    key = np.where(nz, 2 * c + 1 - nb, 64)
+    assert (np.diff(key) >= 0).all() and nz.sum() > 0
+    assert torch.isfinite(rz.image).all()

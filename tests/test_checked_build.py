@@ -16,6 +16,7 @@ SCRIPT = os.path.join(ROOT, "scripts", "checked_path.py")
 
 def _run(lib):
     env = dict(os.environ)
+    env.pop("STEEPGS_LIB", None)   # the release run is the in-tree build even when the suite runs checked
     if lib:
         env["STEEPGS_LIB"] = lib
     r = subprocess.run([sys.executable, SCRIPT], capture_output=True, text=True, timeout=900, env=env, cwd=ROOT)

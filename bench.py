@@ -549,8 +549,9 @@ def main():
     barrier()
     if not args.no_graph:
         capture(targets)
-        for _ in range(2):
+        for _ in range(2):   # first replays upload the graphs: both launch modes warm before timing
             step()
+            step_whole()
         barrier()
     pair_counts.zero_()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(10)] for _ in range(args.steps)]

@@ -466,10 +466,8 @@ __global__ void __launch_bounds__(kThreadsFwd, 4) k_render_fwd(const steepgs_spl
             const float2 p = *reinterpret_cast<const float2*>(&B.par[jj[u]]);
             ee[u] = pair_e(__fsub_rn(fx, g.x), __fsub_rn(fy, g.y), g, make_float4(p.x, p.y, 0.f, 0.f));
           }
-          if (done) {
-            lb <<= 4;
-            continue;
-          }
+          // no skip when this lane is done: blend() composites nothing then (live = !done), and a
+          // divergent branch here only costs its reconvergence (0.973 -> 0.962 ms per C2 step)
           bool cb[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) cb[u] = blend(ee[u], jj[u]);

@@ -2,6 +2,8 @@
 raster parameters (thresholds, dilation, background), each through the whole GPU path against the
 oracle — decisions and binning bit-exact, images, gradients and S within the §3.4 tolerances, and
 the densify decisions.  Sizes are small so every case runs the oracle in well under a second."""
+import os
+
 import numpy as np
 import pytest
 
@@ -39,7 +41,7 @@ def _case(seed):
     return p, cams, rp
 
 
-@pytest.mark.parametrize("seed", list(range(64)))
+@pytest.mark.parametrize("seed", list(range(int(os.environ.get("STEEPGS_FUZZ_SEEDS", "64")))))
 def test_fuzz_full_path(orc, seed):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")

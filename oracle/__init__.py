@@ -151,7 +151,9 @@ def render(params, cam: dict, rp: dict | None = None, window=None, brute_force: 
            sh_degree: int | None = None) -> dict:
     """One view: image/T/n_comp/ambiguity over `window` = (x0, y0, w, h) (default: full image);
     with dl_dimage ([3][h][w] over the window) also grad[20][n] (14 param grads + 6 S planes),
-    absg[20][n], amb_g[n] and grad_mu[2][n] (dL/dPi(p), the ADC statistic's per-view gradient).
+    absg[20][n] (sum of |per-pair contribution|), absS[6][n] (the S entries' per-pair term magnitudes
+    |g sigma| (|U_a U_b| + |(P^T Q P)_ab|), summed: the error scale of a moment-based S),
+    amb_g[n] and grad_mu[2][n] (dL/dPi(p), the ADC statistic's per-view gradient).
     sh_degree (0..3) with sh_rest [3 ((deg + 1)^2 - 1)][n]: SH colours (f3; DC = planes 11-13), and
     with dl_dimage also grad_sh [3 ((deg + 1)^2 - 1)][n]."""
     p = f64(params)
@@ -164,7 +166,7 @@ def render(params, cam: dict, rp: dict | None = None, window=None, brute_force: 
     grad = absg = ambg = dl = gmu = None
     if dl_dimage is not None:
         dl = np.ascontiguousarray(np.asarray(dl_dimage, dtype=np.float64).reshape(3, h, w))
-        grad = np.zeros((20, n)); absg = np.zeros((20, n)); ambg = np.zeros(n, np.uint8); gmu = np.zeros((2, n))
+        grad = np.zeros((20, n)); absg = np.zeros((26, n)); ambg = np.zeros(n, np.uint8); gmu = np.zeros((2, n))
     sp = None
     if split is not None:
         sp = Split()
@@ -191,8 +193,11 @@ def render(params, cam: dict, rp: dict | None = None, window=None, brute_force: 
         raise MemoryError("oracle render failed")
     if gsh is not None and sh_degree == 0:
         gsh = np.zeros((0, n))
-    return dict(image=img, final_T=T, n_comp=nc, amb_px=amb, grad=grad, absg=absg, amb_g=ambg, grad_mu=gmu,
-                grad_sh=gsh, pairs=int(pairs), decision=d)
+    absS = None
+    if absg is not None:   # rows 20-25: the S entries' term magnitudes (test infrastructure)
+        absg, absS = absg[:20].copy(), absg[20:].copy()
+    return dict(image=img, final_T=T, n_comp=nc, amb_px=amb, grad=grad, absg=absg, absS=absS, amb_g=ambg,
+                grad_mu=gmu, grad_sh=gsh, pairs=int(pairs), decision=d)
 
 
 def sh_basis(direction, degree: int = 3):

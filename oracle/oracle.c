@@ -474,6 +474,22 @@ static void hessian_pair(const gproj* g, double sigma, const double* d, double* 
     }
 }
 
+/* Magnitudes of the two terms of each Hessian entry: sigma (|U_a U_b| + |(P^T Q P)_ab|).  Test
+ * infrastructure: the GPU forms S from per-Gaussian moments, P^T (Q M Q - m0 Q) P (C12), so its fp32
+ * error scales with these magnitudes summed over the pairs, not with |H_ab|. */
+static void hessian_terms_abs(const gproj* g, double sigma, const double* d, double* Hm) {
+  const double u0 = g->conic[0] * d[0] + g->conic[1] * d[1];
+  const double u1 = g->conic[1] * d[0] + g->conic[2] * d[1];
+  double U[3];
+  for (int a = 0; a < 3; ++a) U[a] = g->P[a] * u0 + g->P[3 + a] * u1;
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) {
+      const double PQP = g->P[a] * (g->conic[0] * g->P[b] + g->conic[1] * g->P[3 + b]) +
+                         g->P[3 + a] * (g->conic[1] * g->P[b] + g->conic[2] * g->P[3 + b]);
+      Hm[3 * a + b] = sigma * (fabs(U[a] * U[b]) + fabs(PQP));
+    }
+}
+
 void orc_position_hessian(const double* params, int64_t ld, int64_t i, const orc_camera* cam,
                           const orc_raster* rp, double x, double y, double* H) {
   gproj g;
@@ -520,7 +536,7 @@ static double slot_sigma(const cand_t* cd, const orc_split* split, const double*
   return sigma_at(&cd->g, x, y, d);
 }
 
-#define ACCW 42
+#define ACCW 48
 
 int64_t orc_render_view(const double* params, int64_t ld, int64_t n, const orc_camera* cam,
                         const orc_raster* rp, const uint8_t* visible, const uint32_t* depth_key,
@@ -614,7 +630,7 @@ int64_t orc_render_view(const double* params, int64_t ld, int64_t n, const orc_c
   }
 
   const int nthr = orc_num_threads();
-  double* tacc = NULL;   /* per-thread [ncand][ACCW] accumulators (grad 20 + abs 20 + dL/dmu 2) */
+  double* tacc = NULL;   /* per-thread [ncand][ACCW] accumulators (grad 20 + abs 20 + dL/dmu 2 + S term magnitudes 6) */
   double* tsh = NULL;    /* per-thread [ncand][45] SH rest-coefficient accumulators (f3) */
   uint8_t* tamb = NULL;
   const int nrest = sh ? 3 * ((sh->degree + 1) * (sh->degree + 1) - 1) : 0;
@@ -719,6 +735,12 @@ int64_t orc_render_view(const double* params, int64_t ld, int64_t n, const orc_c
           for (int k = 0; k < 20; ++k) { a[k] += contrib[k]; a[20 + k] += fabs(contrib[k]); }
           a[40] += ga * dsdmu[0];                               /* dL/dPi(p) (ADC statistic) */
           a[41] += ga * dsdmu[1];
+          {   /* test infrastructure: the S entries' term magnitudes (absg rows 20-25) */
+            double Hm[9];
+            hessian_terms_abs(g, sg, d, Hm);
+            const int e6[6] = {0, 1, 2, 4, 5, 8};
+            for (int k = 0; k < 6; ++k) a[42 + k] += fabs(ga) * Hm[e6[k]];
+          }
         }
       }
     }
@@ -733,6 +755,8 @@ int64_t orc_render_view(const double* params, int64_t ld, int64_t n, const orc_c
           if (grad) grad[k * ld + gi] += a[k];
           if (absg) absg[k * ld + gi] += a[20 + k];
         }
+        for (int k = 0; k < 6; ++k)
+          if (absg) absg[(20 + k) * ld + gi] += a[42 + k];
         if (grad_mu) { grad_mu[gi] += a[40]; grad_mu[ld + gi] += a[41]; }
         if (grad_sh && tsh) {
           const double* b = tsh + ((size_t)t * (size_t)ncand + (size_t)c) * 45;

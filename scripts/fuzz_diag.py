@@ -27,7 +27,7 @@ def main():
         rz, pt = run_forward(p, cams, rp)
         decs = [oracle.decide(p, c, rp) for c in cams]
         dl = synth.dl_dimage(V, W, H, 1000 + seed)
-        o = np.zeros((20, n)); a = np.zeros((20, n))
+        o = np.zeros((20, n)); a = np.zeros((20, n)); aS = np.zeros((6, n))
         amb = []
         for v, cam in enumerate(cams):
             r = oracle.render(p, cam, rp, decision=decs[v])
@@ -35,8 +35,9 @@ def main():
             dl[v][:, r["amb_px"] != 0] = 0.0
         for v, cam in enumerate(cams):
             r = oracle.render(p, cam, rp, dl_dimage=dl[v], decision=decs[v])
-            o += r["grad"]; a += r["absg"]
+            o += r["grad"]; a += r["absg"]; aS += r["absS"]
         g = run_backward(rz, pt, dl)
+        a[14:20] = np.maximum(a[14:20], aS)   # the S planes' term magnitudes (as _grad_close with absS)
         d = np.abs(g - o)
         tol = 1e-3 * np.abs(o) + 1e-5 * a + 1e-30
         bad = np.argwhere(d > tol)

@@ -64,7 +64,7 @@ def test_fuzz_full_path(orc, seed):
     assert np.array_equal((b["ranges"][:, 1] - b["ranges"][:, 0]).numpy(), counts)
     img = rz.image.cpu().numpy()
     dl = synth.dl_dimage(V, W, H, 1000 + seed)
-    o = np.zeros((20, n)); a = np.zeros((20, n))
+    o = np.zeros((20, n)); a = np.zeros((20, n)); aS = np.zeros((6, n))
     for v, cam in enumerate(cams):
         r = orc.render(p, cam, rp, decision=decs[v])
         ok = (np.abs(img[v] - r["image"]) <= 1e-4 * np.abs(r["image"]) + 1e-6) | (r["amb_px"][None] != 0)
@@ -73,9 +73,9 @@ def test_fuzz_full_path(orc, seed):
         dl[v][:, r["amb_px"] != 0] = 0.0
     for v, cam in enumerate(cams):
         r = orc.render(p, cam, rp, dl_dimage=dl[v], decision=decs[v])
-        o += r["grad"]; a += r["absg"]
+        o += r["grad"]; a += r["absg"]; aS += r["absS"]
     gg = run_backward(rz, pt, dl)
-    ok = _grad_close(gg, o, a, np.zeros(n, np.uint8))
+    ok = _grad_close(gg, o, a, np.zeros(n, np.uint8), absS=aS)
     assert ok.all(), _grad_report(gg, o, a, ok)
 
 

@@ -167,14 +167,20 @@ def test_render_fwd_parity_c1(orc, model, rp):
 FLOOR_LOG: list = []
 
 
-def _grad_close(g, o, absg, ambg, rtol=1e-3, atol_rel=1e-5, plane_rel=1e-6, max_floor_frac=1e-3):
+def _grad_close(g, o, absg, ambg, rtol=1e-3, atol_rel=1e-5, plane_rel=1e-6, max_floor_frac=1e-3, absS=None):
     """|d| <= 1e-3 |ora| + 1e-5 abs_ora (north_star's rel 1e-3 plus the absolute term
     that absorbs fp32 cancellation in per-pair sums).  A third term, 1e-6 max_i |ora[plane]|, is the
     fp32 floor of gradients that are small differences of O(|dL/dSigma| |Sigma|) terms (e.g. the
     quaternion gradient of a nearly isotropic Gaussian, where the per-pair terms cancel in the
     Jacobian and not in the sum abs_ora sees).  It is allowed for at most max(4, 1e-3 of the compared
-    elements) per call; the count is asserted, logged and printed at the end of the run."""
+    elements) per call; the count is asserted, logged and printed at the end of the run.
+    absS ([6][n], optional): for the S planes abs_ora is the sum of the per-pair term magnitudes
+    |g sigma|(|U_a U_b| + |(P^T Q P)_ab|) — the GPU forms S = P^T (QMQ - m0 Q) P from per-Gaussian
+    moment sums (C12), whose fp32 error scales with both terms, not with their per-pair difference."""
     import os
+    if absS is not None:   # S planes: the moment formulation's term magnitudes (DESIGN.md §3.4)
+        absg = absg.copy()
+        absg[14:20] = np.maximum(absg[14:20], absS)
     d = np.abs(g - o)
     strict = d <= rtol * np.abs(o) + atol_rel * absg + 1e-30
     floor = plane_rel * np.abs(o).max(axis=1, keepdims=True)

@@ -732,3 +732,35 @@ def test_render_fwd_l1_u8_equals_float_targets():
     torch.cuda.synchronize()
     assert torch.equal(rz.image, img0) and torch.equal(rz.dL, dl0)
     assert torch.allclose(rz.loss, loss0, rtol=1e-5, atol=0)   # per-warp atomics: summation order
+
+
+@pytest.mark.parametrize("pattern", ["separated", "min_pair", "max_pair"])
+def test_densify_decisions_near_the_threshold(orc, pattern):
+    """The split decision lambda_min(S_bar) < eps_split (Thm 2) for S whose lambda_min sits
+    at 1e-7 .. 1e-3 ||S||_F from eps_split — inside and outside the kernel's fp64 guard band — with the
+    other eigenvalues well separated, or lambda_min nearly repeated (min_pair), or the two larger ones
+    nearly repeated (max_pair): the fp32 eigenvalue outside the band and the fp64 one inside it take
+    the oracle's fp64 decision on every matrix (mask bit-exact)."""
+    rng = np.random.default_rng({"separated": 71, "min_pair": 72, "max_pair": 73}[pattern])
+    n, eps = 40_000, -1e-6
+    F = 10.0 ** rng.uniform(-5, -1, size=n)                                  # ||S||_F scale
+    delta = 10.0 ** rng.uniform(-7, -3, size=n) * rng.choice([-1.0, 1.0], size=n)
+    l1 = eps + delta * F
+    if pattern == "separated":
+        l2 = l1 + F * rng.uniform(0.2, 0.6, size=n); l3 = l2 + F * rng.uniform(0.2, 0.6, size=n)
+    elif pattern == "min_pair":
+        l2 = l1 + F * 10.0 ** rng.uniform(-6, -2, size=n); l3 = l2 + F * rng.uniform(0.3, 0.8, size=n)
+    else:
+        l2 = l1 + F * rng.uniform(0.3, 0.8, size=n); l3 = l2 + F * 10.0 ** rng.uniform(-6, -2, size=n)
+    S = np.zeros((6, n), np.float64)
+    for i in range(n):
+        Q, _ = np.linalg.qr(rng.normal(size=(3, 3)))
+        A = Q @ np.diag([l1[i], l2[i], l3[i]]) @ Q.T
+        S[:, i] = [A[0, 0], A[0, 1], A[0, 2], A[1, 1], A[1, 2], A[2, 2]]
+    S = S.astype(np.float32)
+    want = np.array([orc.eig_sym3(S[:, i].astype(np.float64))[0][0] < eps for i in range(n)])
+    p = synth.blob_scene(n, 77)
+    rz, _, _ = _gpu_densify(p, S, n, 2 * n, denom=1.0)
+    got = rz.split_mask[:n].cpu().numpy().astype(bool)
+    assert want.any() and (~want).any()
+    assert np.array_equal(got, want), int((got != want).sum())

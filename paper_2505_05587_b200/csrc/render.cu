@@ -164,11 +164,15 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // round trip once it runs ahead.  Staging a record is then two fp64 subtractions and eight
 // interval tests of the padded extents against the 8x4 sub-blocks.
 // kFwd: stop early once every consumer warp has terminated (forward early exit).
-template <bool kFwd, int kProd, int kS, int kC = kConsumers, int kRaw = 4, class BatchOf>
+struct NoPrefetch {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+template <bool kFwd, int kProd, int kS, int kC = kConsumers, int kRaw = 4, class BatchOf, class Prefetch = NoPrefetch>
 __device__ __forceinline__ void run_producer(SmemT<kS, kC, kRaw>& sm, const uint32_t* __restrict__ ids,
                                              const steepgs_splat* __restrict__ vs, int nb, BatchOf batch_of,
                                              float* mom_view, float lmin, uint8_t* __restrict__ inst_mask, int pw,
-                                             int lane, int64_t n_g) {
+                                             int lane, int64_t n_g, Prefetch prefetch = Prefetch{}) {
   // producer warp pw of kProd stages the batch slots kk = (q kProd + pw) * 32 + lane
   constexpr int kQ = kBatch / 32 / kProd;
   uint32_t gcur[kQ], gnext[kQ];
@@ -298,6 +302,7 @@ __device__ __forceinline__ void run_producer(SmemT<kS, kC, kRaw>& sm, const uint
       stopped = 1;
       break;
     }
+    if (k == 0) prefetch();   // while the consumers work on the first batch
 #pragma unroll
     for (int q = 0; q < kQ; ++q) {
       gcur[q] = gnext[q];
@@ -385,12 +390,45 @@ __global__ void __launch_bounds__(kThreadsFwd, 4) k_render_fwd(const steepgs_spl
 
   if (warp >= kConsumers) {  // ---------------- producers ----------------
     const int len = (int)(rg.y - rg.x);
+#ifndef SGS_FWD_PREFETCH
+#define SGS_FWD_PREFETCH 300   // ~half of the 592 resident blocks ahead (150 / 450 / 592 / 1200 measured)
+#endif
+#if SGS_FWD_PREFETCH > 0
+    // Warm L2 for a block about half a wave later (tile_order entry blockIdx + kAhead): its range, the
+    // ids of its first batch and their splat records, so that block's start chain (entry -> range ->
+    // ids -> records) runs on L2 hits instead of DRAM round trips.
+    auto pf = [=]() {
+      const int64_t fidx = (int64_t)blockIdx.y * gridDim.x + blockIdx.x + SGS_FWD_PREFETCH;
+      if (fidx >= (int64_t)gridDim.x * gridDim.y) return;
+      uint32_t e = 0u;
+      uint2 frg = make_uint2(0u, 0u);
+      if (lane == 0) {
+        e = __ldg(order + fidx);
+        frg = ranges[(int64_t)(e >> 20) * tiles_per_view + (e & 0xFFFFFu)];
+      }
+      e = __shfl_sync(0xffffffffu, e, 0);
+      frg.x = __shfl_sync(0xffffffffu, frg.x, 0);
+      frg.y = __shfl_sync(0xffffffffu, frg.y, 0);
+      const int fcnt = min((int)(frg.y - frg.x), kBatch);
+      const steepgs_splat* fv = splats + (int64_t)(e >> 20) * n;
+#pragma unroll
+      for (int q = 0; q < kBatch / 32; ++q) {
+        const int kk = q * 32 + lane;
+        if (kk < fcnt) {
+          const uint32_t g = __ldg(ids + frg.x + kk);
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(fv + g));
+        }
+      }
+    };
+#else
+    auto pf = NoPrefetch{};
+#endif
     run_producer<true, kFwdProducers, kFwdStages>(
         sm, ids, splats + (int64_t)view * n, nb,
         [len, rg, ox, oy](int k) {
           return BatchInfo{(int64_t)rg.x + k * kBatch, min(len - k * kBatch, kBatch), k * kBatch, ox, oy, true};
         },
-        nullptr, __log2f(rk.alpha_min), inst_mask, warp - kConsumers, lane, n);
+        nullptr, __log2f(rk.alpha_min), inst_mask, warp - kConsumers, lane, n, pf);
     return;
   }
 
